@@ -1,0 +1,247 @@
+"""ORACLE — test infrastructure only (not the product path).
+
+Plain CPU reference for the Scepsy ALP allocation search (arXiv 2604.15186).
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` legs may
+import this package.  It never imports paper_2604_15186_b200 and shares no code with it.
+
+* O1  ``liboracle.so`` (alp_oracle.c): literal option terms + brute-force enumeration.
+* O2  ``oracle.dp``: multiple-choice-knapsack DP + lowest-index DFS + counting DP (independent
+      algorithm, used as a cross-check and for full-size C3-C5 answers).
+
+Function-level citations are in alp_oracle.c's header; the readings of the paper are listed in
+DESIGN.md §3.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Any
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(HERE, "alp_oracle.c")
+_LIB = os.path.join(HERE, "liboracle.so")
+PCT_KEYS = ("mean", "p50", "p90", "p99")
+
+
+def build_lib(force: bool = False) -> str:
+    """Compile the C oracle (plain gcc, no FMA contraction, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                               "-shared", "-pthread", _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Inst(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int), ("F", ctypes.c_int), ("nS", ctypes.c_int), ("nT", ctypes.c_int),
+                ("nR", ctypes.c_int), ("n", ctypes.c_void_p), ("p", ctypes.c_void_p), ("S", ctypes.c_void_p),
+                ("T", ctypes.c_void_p), ("R", ctypes.c_void_p), ("prof_off", ctypes.c_void_p),
+                ("rate", ctypes.c_void_p), ("lat", ctypes.c_void_p), ("tmax", ctypes.c_void_p),
+                ("min_units", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build_lib())
+        P = ctypes.POINTER(_Inst)
+        L.orc_lookup.restype = ctypes.c_double
+        L.orc_lookup.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double]
+        L.orc_option.restype = ctypes.c_int
+        L.orc_option.argtypes = [P, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_option_table.restype = None
+        L.orc_option_table.argtypes = [P, ctypes.c_double] + [ctypes.c_void_p] * 5
+        L.orc_predict.restype = ctypes.c_int
+        L.orc_predict.argtypes = [P, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p] + [ctypes.c_void_p] * 4
+        L.orc_search.restype = ctypes.c_int
+        L.orc_search.argtypes = [P, ctypes.c_double, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_candidate.restype = ctypes.c_int
+        L.orc_candidate.argtypes = [P, ctypes.c_double, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p,
+                                    ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+@dataclass
+class Instance:
+    """An ALP instance in the oracle's own flattened layout (kept alive with its numpy buffers)."""
+    M: int
+    F: int
+    S: np.ndarray
+    T: np.ndarray
+    R: np.ndarray
+    n: np.ndarray
+    p: np.ndarray
+    prof_off: np.ndarray
+    rate: np.ndarray
+    lat: np.ndarray
+    tmax: np.ndarray
+    min_units: np.ndarray | None
+    budget: int
+    raw: dict
+
+    @property
+    def K(self) -> int:
+        return len(self.S) * len(self.T) * len(self.R)
+
+    @property
+    def N(self) -> int:
+        return self.K ** self.M
+
+    def cstruct(self) -> _Inst:
+        return _Inst(self.M, self.F, len(self.S), len(self.T), len(self.R), self.n.ctypes.data, self.p.ctypes.data,
+                     self.S.ctypes.data, self.T.ctypes.data, self.R.ctypes.data, self.prof_off.ctypes.data,
+                     self.rate.ctypes.data, self.lat.ctypes.data, self.tmax.ctypes.data,
+                     self.min_units.ctypes.data if self.min_units is not None else None)
+
+
+def from_json(d: dict[str, Any], percentile: str | None = None) -> Instance:
+    pct = percentile or d.get("percentile", "mean")
+    M, T = d["M"], d["tp"]
+    off, rate, lat, tmax = [0], [], [], []
+    for m in range(M):
+        for ti in range(len(T)):
+            c = d["profiles"][m][ti]
+            rate += c["rate"]
+            lat += c["lat"][pct]
+            tmax.append(c["tmax"] if c.get("tmax") is not None else c["rate"][-1])
+            off.append(len(rate))
+    mu = d.get("min_units")
+    return Instance(M=M, F=d["F"], S=np.asarray(d["share_units"], np.int32), T=np.asarray(T, np.int32),
+                    R=np.asarray(d["replicas"], np.int32), n=np.asarray(d["n"], np.float64),
+                    p=np.asarray(d["p"], np.float64), prof_off=np.asarray(off, np.int32),
+                    rate=np.asarray(rate, np.float64), lat=np.asarray(lat, np.float64),
+                    tmax=np.asarray(tmax, np.float64),
+                    min_units=None if mu is None else np.asarray(mu, np.int32).reshape(-1),
+                    budget=int(d["budget_units"]), raw=d)
+
+
+def lookup(rates, lats, x: float) -> float:
+    r = np.ascontiguousarray(rates, np.float64)
+    l = np.ascontiguousarray(lats, np.float64)
+    return lib().orc_lookup(r.ctypes.data, l.ctypes.data, len(r), float(x))
+
+
+def option(I: Instance, lam: float, m: int, k: int):
+    tau = ctypes.c_float()
+    term = ctypes.c_double()
+    b = ctypes.c_double()
+    u = ctypes.c_int()
+    s = I.cstruct()
+    ok = lib().orc_option(ctypes.byref(s), lam, m, k, ctypes.byref(tau), ctypes.byref(term), ctypes.byref(b),
+                          ctypes.byref(u))
+    return {"ok": bool(ok), "tau": np.float32(tau.value), "term": term.value, "b": b.value, "u": u.value}
+
+
+def option_table(I: Instance, lam: float) -> dict[str, np.ndarray]:
+    K = I.K
+    tau = np.empty((I.M, K), np.float32)
+    term = np.empty((I.M, K), np.float64)
+    b = np.empty((I.M, K), np.float64)
+    u = np.empty((I.M, K), np.int32)
+    ok = np.empty((I.M, K), np.uint8)
+    s = I.cstruct()
+    lib().orc_option_table(ctypes.byref(s), lam, tau.ctypes.data, term.ctypes.data, b.ctypes.data, u.ctypes.data,
+                           ok.ctypes.data)
+    return {"tau": tau, "term": term, "b": b, "u": u, "ok": ok.astype(bool)}
+
+
+@dataclass
+class SearchResult:
+    found: bool
+    latency_key: float      # canonical FP32 objective (np.float32 value)
+    index: int              # canonical mixed-radix index (lowest among ties)
+    count: int              # feasible candidates
+
+
+def search(I: Instance, lam: float, budget: int | None = None, lo: int = 0, hi: int | None = None,
+           threads: int = 1) -> SearchResult:
+    """O1 brute force over canonical indices [lo, hi)."""
+    B = I.budget if budget is None else budget
+    hi = I.N if hi is None else hi
+    best = ctypes.c_float()
+    idx = ctypes.c_uint64()
+    cnt = ctypes.c_uint64()
+    s = I.cstruct()
+    found = lib().orc_search(ctypes.byref(s), lam, B, lo, hi, threads, ctypes.byref(best), ctypes.byref(idx),
+                             ctypes.byref(cnt))
+    return SearchResult(bool(found), float(np.float32(best.value)), int(idx.value) if found else -1, int(cnt.value))
+
+
+def decode(I: Instance, idx: int) -> list[int]:
+    """Canonical index -> per-LLM option index k_m (LLM 0 most significant)."""
+    K = I.K
+    out = []
+    for _ in range(I.M):
+        out.append(idx % K)
+        idx //= K
+    return out[::-1]
+
+
+def option_grid(I: Instance, k: int) -> tuple[int, int, int]:
+    """Option index k -> (share units, tp, replicas); k = (s_i*nT + t_i)*nR + r_i."""
+    nT, nR = len(I.T), len(I.R)
+    return int(I.S[k // (nT * nR)]), int(I.T[(k // nR) % nT]), int(I.R[k % nR])
+
+
+def predict(I: Instance, lam: float, opts: list[int], budget: int | None = None):
+    """FP64 Eq. 1 latency, Eq. 2 throughput, units, FP32 key, feasibility for one allocation."""
+    B = I.budget if budget is None else budget
+    o = np.asarray(opts, np.int32)
+    L = ctypes.c_double()
+    Tw = ctypes.c_double()
+    U = ctypes.c_int64()
+    l32 = ctypes.c_float()
+    s = I.cstruct()
+    ok = lib().orc_predict(ctypes.byref(s), lam, B, o.ctypes.data, ctypes.byref(L), ctypes.byref(Tw),
+                           ctypes.byref(U), ctypes.byref(l32))
+    return {"feasible": bool(ok), "latency": L.value, "throughput": Tw.value, "units": U.value,
+            "latency_key": float(np.float32(l32.value))}
+
+
+def candidate(I: Instance, lam: float, idx: int, budget: int | None = None):
+    """One candidate recomputed from the profiles (no hoisting)."""
+    B = I.budget if budget is None else budget
+    l32 = ctypes.c_float()
+    U = ctypes.c_int64()
+    s = I.cstruct()
+    ok = lib().orc_candidate(ctypes.byref(s), lam, B, idx, ctypes.byref(l32), ctypes.byref(U))
+    return bool(ok), float(np.float32(l32.value)), U.value
+
+
+def lambda_star(I: Instance, budget: int | None = None) -> float:
+    """Budget-aware maximum workflow throughput: the largest v among all Eq. 2 terms
+    b_m[k] such that sum_m min{u_m[k] : b_m[k] >= v and k passes the memory floor} <= B."""
+    B = I.budget if budget is None else budget
+    tab = option_table(I, 1.0)
+    b, u = tab["b"], tab["u"]
+    floor_ok = np.ones_like(b, dtype=bool)
+    if I.min_units is not None:
+        for m in range(I.M):
+            for k in range(I.K):
+                s_units, _t, _d = option_grid(I, k)
+                t_i = (k // len(I.R)) % len(I.T)
+                floor_ok[m, k] = s_units >= I.min_units[m * len(I.T) + t_i]
+    best = 0.0
+    for v in np.unique(b[floor_ok])[::-1]:
+        tot = 0
+        for m in range(I.M):
+            sel = u[m][(b[m] >= v) & floor_ok[m]]
+            if sel.size == 0:
+                tot = None
+                break
+            tot += int(sel.min())
+        if tot is not None and tot <= B:
+            best = float(v)
+            break
+    return best
