@@ -1,0 +1,307 @@
+"""Benchmark: exhaustive ALP allocation search (Scepsy, arXiv 2604.15186) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+A step = one full search of the workload: option-term kernel, exhaustive evaluation of all N
+candidates (sharded over ranks), NCCL all-reduce of the (key, count) pairs, device finalize and
+the D2H of the result.  value = candidates evaluated per second for the whole job (max over
+ranks of the device time); inputs (profile tables) are resident in HBM before the timed region.
+e2e = the same metric through the C ABI from HOST buffers: alp_build (H2D of the profiles and the
+plan) + search + D2H of the result + alp_destroy, per step.
+
+Rank 0 prints ONE JSON line.  See DESIGN.md §6 for the roofline definition.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ALP candidates evaluated/sec and time-to-optimum at 1/2/4/8 B200 vs CPU oracle"
+UNIT = "candidates/s"
+ISSUE_LANES_PER_SM_PER_CLK = 128   # 4 SMSPs x 1 warp-instruction/clk x 32 lanes
+INSTR_PER_CANDIDATE_MIN = 1.0      # 1/2 FADD2 + 1/2 FMNMX3
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_workload(name):
+    from workloads import generate
+    return generate.load(name)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU oracle leg
+def oracle_rate(d, seconds=12.0, threads=None):
+    """O1 brute force (the oracle as it stands) on a bounded contiguous sample of the workload,
+    all host cores; returns (cand/s, cores, sample description, elapsed s)."""
+    import oracle
+    I = oracle.from_json(d)
+    lam = d["targets"][0]
+    threads = threads or os.cpu_count() or 1
+    n = min(I.N, 4_000_000 * threads)
+    t0 = time.perf_counter()
+    oracle.search(I, lam, I.budget, lo=0, hi=n, threads=threads)
+    dt = time.perf_counter() - t0
+    n2 = int(min(I.N, max(n, n * seconds / max(dt, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.search(I, lam, I.budget, lo=0, hi=n2, threads=threads)
+    dt = time.perf_counter() - t0
+    return n2 / dt, threads, f"canonical indices [0, {n2}) of {d['name']} (N={I.N}), {threads} threads", dt
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    d = load_workload(args.workload)
+    import oracle
+    I = oracle.from_json(d)
+    threads = os.cpu_count() or 1
+    lam = d["targets"][0]
+    n = min(I.N, 30_000_000 * threads // 8)
+    for _ in range(args.warmup):
+        oracle.search(I, lam, I.budget, lo=0, hi=min(n, 1_000_000), threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.search(I, lam, I.budget, lo=0, hi=n, threads=threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    v = n * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _config(d, I.N, args.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"canonical indices [0, {n}) of {d['name']} per step (O1 brute force)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(d, N, world):
+    return {"workload": f"{d['name']}: {d['description']}", "candidates": N, "M": d["M"],
+            "options_per_llm": len(d["share_units"]) * len(d["tp"]) * len(d["replicas"]),
+            "budget_units": d["budget_units"], "F": d["F"], "target_req_s": d["targets"][0],
+            "n_targets": 1, "parallelism": f"index-space shard x{world} + NCCL allreduce-min",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# --------------------------------------------------------------------------- our path
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2604_15186_b200 import build as pbuild
+    if rank == 0 or world == 1:
+        pbuild.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2604_15186_b200 as P
+    from paper_2604_15186_b200.dist import reduce_keys
+
+    d = load_workload(args.workload)
+    B = int(d["budget_units"])
+    targets = [d["targets"][0]]
+    alp = P.Alp.from_instance(d)
+    N = alp.num_candidates
+    lo, hi = alp.shard_range(B, rank, world)
+    stream = torch.cuda.Stream(device=dev)
+    keys = torch.empty(1, dtype=torch.int64, device=dev)
+    counts = torch.empty(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        with torch.cuda.stream(stream):
+            alp.search_shard(targets, B, lo, hi, keys.data_ptr(), counts.data_ptr(), stream.cuda_stream)
+            reduce_keys(keys, counts)
+            return alp.finalize(targets, B, keys.data_ptr(), counts.data_ptr(), stream.cuda_stream)[0]
+
+    for _ in range(max(3, args.warmup)):
+        res = step()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    step_ms, kern_ms = [], []
+    launches = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            res = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(alp.last_kernel_ms)
+            launches += alp.last_launches
+    tot_ms = sum(step_ms)
+    kern_tot = sum(kern_ms)
+    t = torch.tensor([tot_ms, kern_tot], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms, kern_max = t.tolist()
+
+    # ---- end to end through the C ABI from host buffers (build + search + D2H + destroy)
+    e2e_ms = []
+    h2d = 0
+    for i in range(args.e2e_steps + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a2 = P.Alp.from_instance(d)
+        lo2, hi2 = a2.shard_range(B, rank, world)
+        with torch.cuda.stream(stream):
+            a2.search_shard(targets, B, lo2, hi2, keys.data_ptr(), counts.data_ptr(), stream.cuda_stream)
+            reduce_keys(keys, counts)
+            r2 = a2.finalize(targets, B, keys.data_ptr(), counts.data_ptr(), stream.cuda_stream)[0]
+        h2d = a2.h2d_bytes + 8 * len(targets)
+        a2.close()
+        dt = time.perf_counter() - t0
+        if i > 0:  # first one pays one-time context/module costs
+            e2e_ms.append(dt * 1e3)
+        assert r2.index == res.index
+    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_tot = te.item()
+
+    if rank == 0:
+        cs = clk.summary()
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        f_max = (cs["sm_max_mhz"] or 1965.0) * 1e6
+        cand_rank = N * (hi - lo) / max(1, alp.num_items(B))
+        achieved = cand_rank / (kern_max / len(kern_ms) * 1e-3)  # per GPU, dominant kernel
+        peak = sm_count * ISSUE_LANES_PER_SM_PER_CLK * f_max / INSTR_PER_CANDIDATE_MIN
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.workload)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": N * args.steps / (tot_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": tot_ms / args.steps,
+            "time_to_optimum_ms": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded profile tables, workloads/instances)",
+            "config": _config(d, N, world),
+            "result": {"index": res.index, "latency_key": res.latency_key, "latency_s": res.latency,
+                       "throughput_req_s": res.throughput, "units": res.units,
+                       "feasible_count": res.feasible_count},
+            "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcandidates/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_search (K2)", "kernel_ms": kern_max / len(kern_ms),
+                         "peak_def": f"{sm_count} SMs x 128 issue lanes/clk x {f_max / 1e6:.0f} MHz / 1 instr per candidate"},
+            "e2e": {"value": N * len(e2e_ms) / (e2e_tot * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(P.ctypes.sizeof(P._Result))},
+            "gpu_launches": launches,
+            "clocks": cs,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, sample, _dt = oracle_rate(d, seconds=args.cpu_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

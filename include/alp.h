@@ -1,0 +1,155 @@
+/*
+ * alp.h — C ABI of the B200-native exhaustive ALP allocation search (Scepsy, arXiv 2604.15186).
+ *
+ * The operation ("Workflow Predictions", Eq. 1 at PAPER.md:340-343, Eq. 2 at
+ * PAPER.md:346-349; scheduler goal "lowest latency within a target workflow-level arrival rate",
+ * PAPER.md:293): for every candidate allocation — each LLM m gets a per-shard GPU share
+ * f_m = share_units/F, a tensor-parallel degree tp_m and a replica count d_m — predict the
+ * workflow latency L_w (Eq. 1) and throughput T_w (Eq. 2) from the per-LLM profiles and the
+ * workflow statistics (n_m, p_m), reject candidates that exceed the GPU budget or
+ * miss the throughput target, and return the minimum-latency candidate (lowest canonical index
+ * on ties) plus the number of feasible candidates.  The exact arithmetic (FP64 option terms,
+ * canonical binary32 objective) is fixed in DESIGN.md §3 (readings R1-R13 of SURVEY.md §8(c)).
+ *
+ * Candidate order: option index inside an LLM k = (s_i*nT + t_i)*nR + r_i
+ * (share most significant, replicas least); candidate index idx = sum_m k_m * K^(M-1-m) (LLM 0
+ * most significant), K = nS*nT*nR.
+ *
+ * Conventions
+ *  - Every entry point returns alp_status; on error alp_last_error() names the offending field.
+ *    No C++ exception crosses this boundary.
+ *  - alp_build copies every input array; the caller may free them on return.  The handle owns
+ *    host copies plus device tables on the device current at build time.  A handle may be used
+ *    by one host thread at a time.
+ *  - Budgets are integer GPU units (1 unit = 1/F GPU); targets are workflow requests/second.
+ *  - All results are bit-identical for any rank count / grid shape (see alp_search_shard).
+ */
+#ifndef SCEPSY_ALP_H
+#define SCEPSY_ALP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALP_MAX_M 16        /* max LLMs per workflow */
+#define ALP_MAX_K 1024      /* max options per LLM (nS*nT*nR) */
+
+typedef struct alp_s alp_t; /* opaque, immutable after alp_build */
+
+typedef enum {
+  ALP_OK = 0,          /* success */
+  ALP_EINVAL = 1,      /* invalid argument (field named by alp_last_error) */
+  ALP_EINFEASIBLE = 2, /* search finished but no candidate is feasible (result.found = 0) */
+  ALP_EINTERNAL = 3,   /* internal inconsistency */
+  ALP_ECUDA = 4        /* CUDA runtime error (message in alp_last_error) */
+} alp_status;
+
+typedef enum { ALP_P_MEAN = 0, ALP_P50 = 1, ALP_P90 = 2, ALP_P99 = 3 } alp_percentile; /* PAPER.md:356 "percentile P" */
+
+/* Workflow + profile description (host pointers, caller-owned, copied by alp_build).
+ * Profiles: one piecewise-linear curve per (LLM m, tp index t), CSR over points:
+ * curve c = m*nT + t has points prof_off[c] .. prof_off[c+1]-1 (>= 1 point), rates strictly
+ * increasing, latencies > 0 and non-decreasing.  T_{m,t} = tmax[c] (>= last
+ * rate) or the last rate when tmax == NULL.  Sub-GPU shares use capacity scaling
+ * L'(x) = L(x/f)/f, T' = f*T (reading R2). */
+typedef struct {
+  int32_t M;                    /* number of LLMs, 1..ALP_MAX_M */
+  int32_t F;                    /* GPU units per GPU (share grid denominator), >= 1 */
+  const double *n;              /* [M] mean invocations per workflow request, > 0 */
+  const double *p;              /* [M] mean request-level parallelism, >= 1 */
+  int32_t nS, nT, nR;           /* grid sizes; K = nS*nT*nR <= ALP_MAX_K */
+  const int32_t *share_units;   /* [nS] strictly ascending, 1..F */
+  const int32_t *tp;            /* [nT] strictly ascending, >= 1 */
+  const int32_t *replicas;      /* [nR] strictly ascending, >= 1 */
+  const int32_t *prof_off;      /* [M*nT+1] CSR offsets, prof_off[0] = 0 */
+  const double *rate;           /* [prof_off[M*nT]] requests/s */
+  const double *lat[4];         /* per alp_percentile column, seconds; NULL = absent */
+  const double *tmax;           /* [M*nT] saturation throughput or NULL */
+  const int32_t *min_units;     /* [M*nT] memory floor in units per shard, or NULL */
+  int32_t pct;                  /* alp_percentile used by this handle */
+} alp_desc;
+
+/* One search result (all fields host-side after the call returns). */
+typedef struct {
+  int32_t found;                /* 0 => no feasible candidate */
+  int32_t M;
+  uint64_t index;               /* canonical candidate index (UINT64_MAX if !found) */
+  float latency_key;            /* canonical binary32 objective of the winner (R7) */
+  double latency;               /* FP64 Eq. 1 L_w of the winner, seconds */
+  double throughput;            /* FP64 Eq. 2 T_w of the winner, requests/s */
+  int64_t units;                /* GPU units used by the winner */
+  uint64_t feasible_count;      /* number of feasible candidates (R10) */
+  uint64_t candidates;          /* candidates evaluated = N (exhaustive) */
+  int32_t share_units[ALP_MAX_M], tp[ALP_MAX_M], replicas[ALP_MAX_M]; /* winner, per LLM */
+} alp_result;
+
+/* Validate, copy and plan.  Uploads the profile tables and the static search plan to the
+ * current CUDA device.  Errors: ALP_EINVAL naming the field; ALP_ECUDA. */
+alp_status alp_build(const alp_desc *desc, alp_t **out);
+
+/* Test-only constructor: search directly over given binary32 option terms tau[M*K] (+INF =
+ * infeasible option) and units u[M*K], bypassing the profiles (same for every target).  Used to
+ * inject exactly-representable terms and ties (SURVEY.md §8(c) "option-table injection"). */
+alp_status alp_build_from_terms(int32_t M, int32_t K, const float *tau, const int32_t *u, alp_t **out);
+
+void alp_destroy(alp_t *h);
+
+/* N = K^M candidates. */
+uint64_t alp_num_candidates(const alp_t *h);
+
+/* Host bytes copied to the device by alp_build (for end-to-end accounting). */
+uint64_t alp_h2d_bytes(const alp_t *h);
+
+/* Canonical index -> per-LLM (share units, tp, replicas); out arrays [M]. */
+alp_status alp_decode(const alp_t *h, uint64_t index, int32_t *share_units, int32_t *tp, int32_t *replicas);
+
+/* Per-option table at target lambda, computed by the device option-term kernel and copied back:
+ * tau[M*K] (binary32 Eq. 1 terms, +INF if infeasible), term[M*K] (FP64), b[M*K] (FP64 Eq. 2
+ * terms d*f*T/n), u[M*K] units.  Any output pointer may be NULL. */
+alp_status alp_option_table(alp_t *h, double lambda, float *tau, double *term, double *b, int32_t *u);
+
+/* FP64 prediction of n allocations at target lambda (device kernel; synchronous).
+ * opts[n*M] = option index k_m per LLM; outputs [n]: latency (INF if infeasible), throughput,
+ * units, feasible (budget_units applied). */
+alp_status alp_predict(alp_t *h, const int32_t *opts, int32_t n, double lambda, int64_t budget_units,
+                       double *latency, double *throughput, int64_t *units, int32_t *feasible);
+
+/* Single-device search on the current device (internal stream, synchronous).  Returns ALP_OK,
+ * or ALP_EINFEASIBLE with out->found = 0. */
+alp_status alp_search(alp_t *h, double target, int64_t budget_units, alp_result *out);
+
+/* Batched targets (Pareto sweep): out[n]. Returns ALP_OK if at least one target is feasible. */
+alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t budget_units, alp_result *out);
+
+/* ---- multi-GPU building blocks (PyTorch owns memory, streams and the process group) ----
+ * The candidate space is cut into equal-cost work items; rank r of world w gets the contiguous
+ * item range [lo, hi).  Every rank calls alp_search_shard on its range (async on `stream`),
+ * then all-reduces keys with MIN and counts with SUM as int64 (every key < 2^63), then calls
+ * alp_finalize with the reduced arrays.  Keys encode (binary32 objective, global segment id),
+ * so the reduced result does not depend on how items were split. */
+uint64_t alp_num_items(const alp_t *h, int64_t budget_units);
+alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, int32_t world, uint64_t *lo,
+                           uint64_t *hi);
+/* d_keys/d_counts: device int64[n] (initialised by this call).  stream: cudaStream_t or NULL. */
+alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
+                            uint64_t hi, void *stream, int64_t *d_keys, int64_t *d_counts);
+/* Decode reduced keys on the device (lowest index inside the winning segment, FP64 Eq. 1/Eq. 2
+ * of the winner) and copy n results to the host (synchronises `stream`). */
+alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
+                        const int64_t *d_keys, const int64_t *d_counts, void *stream, alp_result *out);
+
+/* Device time (ms) of the last search kernel launched through this handle (CUDA events on the
+ * launching stream), and the number of kernels the last search/finalize launched. */
+float alp_last_kernel_ms(const alp_t *h);
+int32_t alp_last_launches(const alp_t *h);
+
+/* Thread-local message for the last error (never NULL). */
+const char *alp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCEPSY_ALP_H */

@@ -1,0 +1,267 @@
+"""Python binding of the B200-native exhaustive ALP allocation search (Scepsy, arXiv 2604.15186).
+
+Thin ctypes layer over the in-tree C-ABI library ``lib/libscepsy_alp.so`` (include/alp.h): it
+marshals arguments only — every step of the search (option terms, candidate evaluation,
+argmin/count, winner decode and FP64 prediction) runs in the sm_100a kernels.  There is no CPU
+fallback: importing this package on a machine without the built library raises.
+
+    from paper_2604_15186_b200 import Alp
+    alp = Alp.from_instance(json_dict)          # alp_build
+    r = alp.search(target, budget_units)        # alp_search -> Result
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Any, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libscepsy_alp.so")
+MAX_M = 16
+PCT = {"mean": 0, "p50": 1, "p90": 2, "p99": 3}
+
+ALP_OK, ALP_EINVAL, ALP_EINFEASIBLE, ALP_EINTERNAL, ALP_ECUDA = range(5)
+
+
+class AlpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"alp status {status}: {msg}")
+        self.status = status
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("F", ctypes.c_int32), ("n", ctypes.c_void_p), ("p", ctypes.c_void_p),
+                ("nS", ctypes.c_int32), ("nT", ctypes.c_int32), ("nR", ctypes.c_int32),
+                ("share_units", ctypes.c_void_p), ("tp", ctypes.c_void_p), ("replicas", ctypes.c_void_p),
+                ("prof_off", ctypes.c_void_p), ("rate", ctypes.c_void_p), ("lat", ctypes.c_void_p * 4),
+                ("tmax", ctypes.c_void_p), ("min_units", ctypes.c_void_p), ("pct", ctypes.c_int32)]
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("found", ctypes.c_int32), ("M", ctypes.c_int32), ("index", ctypes.c_uint64),
+                ("latency_key", ctypes.c_float), ("latency", ctypes.c_double), ("throughput", ctypes.c_double),
+                ("units", ctypes.c_int64), ("feasible_count", ctypes.c_uint64), ("candidates", ctypes.c_uint64),
+                ("share_units", ctypes.c_int32 * MAX_M), ("tp", ctypes.c_int32 * MAX_M),
+                ("replicas", ctypes.c_int32 * MAX_M)]
+
+
+EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
+           "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
+           "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_error"]
+
+_lib = None
+
+
+def lib():
+    """Load the C-ABI library (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2604_15186_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, u64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+        sig = {
+            "alp_build": (i32, [vp, vp]), "alp_build_from_terms": (i32, [i32, i32, vp, vp, vp]),
+            "alp_destroy": (None, [vp]), "alp_num_candidates": (u64, [vp]), "alp_h2d_bytes": (u64, [vp]),
+            "alp_decode": (i32, [vp, u64, vp, vp, vp]), "alp_option_table": (i32, [vp, d, vp, vp, vp, vp]),
+            "alp_predict": (i32, [vp, vp, i32, d, i64, vp, vp, vp, vp]),
+            "alp_search": (i32, [vp, d, i64, vp]), "alp_search_batch": (i32, [vp, vp, i32, i64, vp]),
+            "alp_num_items": (u64, [vp, i64]), "alp_shard_range": (i32, [vp, i64, i32, i32, vp, vp]),
+            "alp_search_shard": (i32, [vp, vp, i32, i64, u64, u64, vp, vp, vp]),
+            "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp]),
+            "alp_last_kernel_ms": (ctypes.c_float, [vp]), "alp_last_launches": (i32, [vp]),
+            "alp_last_error": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, ok=(ALP_OK,)) -> int:
+    if st not in ok:
+        raise AlpError(st, lib().alp_last_error().decode())
+    return st
+
+
+@dataclass
+class Result:
+    found: bool
+    index: int
+    latency_key: float          # canonical binary32 objective
+    latency: float              # FP64 Eq. 1
+    throughput: float           # FP64 Eq. 2
+    units: int
+    feasible_count: int
+    candidates: int
+    share_units: list = field(default_factory=list)
+    tp: list = field(default_factory=list)
+    replicas: list = field(default_factory=list)
+
+    @staticmethod
+    def _from(r: _Result) -> "Result":
+        M = r.M
+        return Result(bool(r.found), int(r.index) if r.found else -1, float(np.float32(r.latency_key)), r.latency,
+                      r.throughput, int(r.units), int(r.feasible_count), int(r.candidates),
+                      list(r.share_units[:M]), list(r.tp[:M]), list(r.replicas[:M]))
+
+
+def _arr(x, dt):
+    return np.ascontiguousarray(np.asarray(x, dtype=dt))
+
+
+class Alp:
+    """Handle to an immutable ALP (alp_t).  Not thread-safe; one handle per host thread."""
+
+    def __init__(self, handle: int, M: int, keep: Any = None):
+        self._h = ctypes.c_void_p(handle)
+        self.M = M
+        self._keep = keep
+
+    # ------------------------------------------------------------------ construction
+    @classmethod
+    def from_instance(cls, d: dict, percentile: str | None = None) -> "Alp":
+        """alp_build from an instance dict (workloads/instances/*.json layout)."""
+        M, T = d["M"], d["tp"]
+        off, rate, lat, tmax = [0], [], {k: [] for k in PCT}, []
+        for m in range(M):
+            for ti in range(len(T)):
+                c = d["profiles"][m][ti]
+                rate += c["rate"]
+                for k in PCT:
+                    lat[k] += c["lat"][k] if k in c["lat"] else [float("nan")] * len(c["rate"])
+                tmax.append(c["tmax"] if c.get("tmax") is not None else c["rate"][-1])
+                off.append(len(rate))
+        keep = dict(n=_arr(d["n"], np.float64), p=_arr(d["p"], np.float64), S=_arr(d["share_units"], np.int32),
+                    T=_arr(T, np.int32), R=_arr(d["replicas"], np.int32), off=_arr(off, np.int32),
+                    rate=_arr(rate, np.float64), tmax=_arr(tmax, np.float64),
+                    **{f"lat_{k}": _arr(v, np.float64) for k, v in lat.items()})
+        mu = d.get("min_units")
+        if mu is not None:
+            keep["minu"] = _arr(mu, np.int32).reshape(-1)
+        desc = _Desc()
+        desc.M, desc.F = M, d["F"]
+        desc.n, desc.p = keep["n"].ctypes.data, keep["p"].ctypes.data
+        desc.nS, desc.nT, desc.nR = len(keep["S"]), len(keep["T"]), len(keep["R"])
+        desc.share_units, desc.tp, desc.replicas = keep["S"].ctypes.data, keep["T"].ctypes.data, keep["R"].ctypes.data
+        desc.prof_off, desc.rate = keep["off"].ctypes.data, keep["rate"].ctypes.data
+        for k, i in PCT.items():
+            desc.lat[i] = keep[f"lat_{k}"].ctypes.data
+        desc.tmax = keep["tmax"].ctypes.data
+        desc.min_units = keep["minu"].ctypes.data if "minu" in keep else None
+        desc.pct = PCT[percentile or d.get("percentile", "mean")]
+        h = ctypes.c_void_p()
+        _check(lib().alp_build(ctypes.byref(desc), ctypes.byref(h)))
+        return cls(h.value, M)
+
+    @classmethod
+    def from_terms(cls, tau: np.ndarray, u: np.ndarray) -> "Alp":
+        """Test-only: alp_build_from_terms over given binary32 option terms and units [M, K]."""
+        t = _arr(tau, np.float32)
+        uu = _arr(u, np.int32)
+        M, K = t.shape
+        h = ctypes.c_void_p()
+        _check(lib().alp_build_from_terms(M, K, t.ctypes.data, uu.ctypes.data, ctypes.byref(h)))
+        return cls(h.value, M)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().alp_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------------ queries
+    @property
+    def num_candidates(self) -> int:
+        return int(lib().alp_num_candidates(self._h))
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(lib().alp_h2d_bytes(self._h))
+
+    def decode(self, index: int):
+        s = np.zeros(self.M, np.int32)
+        t = np.zeros(self.M, np.int32)
+        r = np.zeros(self.M, np.int32)
+        _check(lib().alp_decode(self._h, index, s.ctypes.data, t.ctypes.data, r.ctypes.data))
+        return list(zip(s.tolist(), t.tolist(), r.tolist()))
+
+    def option_table(self, lam: float, K: int):
+        tau = np.empty((self.M, K), np.float32)
+        term = np.empty((self.M, K), np.float64)
+        b = np.empty((self.M, K), np.float64)
+        u = np.empty((self.M, K), np.int32)
+        _check(lib().alp_option_table(self._h, lam, tau.ctypes.data, term.ctypes.data, b.ctypes.data, u.ctypes.data))
+        return {"tau": tau, "term": term, "b": b, "u": u}
+
+    def predict(self, opts: Sequence[Sequence[int]], lam: float, budget: int):
+        o = _arr(opts, np.int32).reshape(-1, self.M)
+        n = o.shape[0]
+        lat = np.empty(n, np.float64)
+        thr = np.empty(n, np.float64)
+        units = np.empty(n, np.int64)
+        feas = np.empty(n, np.int32)
+        _check(lib().alp_predict(self._h, o.ctypes.data, n, lam, budget, lat.ctypes.data, thr.ctypes.data,
+                                 units.ctypes.data, feas.ctypes.data))
+        return {"latency": lat, "throughput": thr, "units": units, "feasible": feas.astype(bool)}
+
+    # ------------------------------------------------------------------ search
+    def search(self, target: float, budget: int) -> Result:
+        r = _Result()
+        _check(lib().alp_search(self._h, target, budget, ctypes.byref(r)), (ALP_OK, ALP_EINFEASIBLE))
+        return Result._from(r)
+
+    def search_batch(self, targets: Sequence[float], budget: int) -> list[Result]:
+        t = _arr(targets, np.float64)
+        out = (_Result * len(t))()
+        _check(lib().alp_search_batch(self._h, t.ctypes.data, len(t), budget, out), (ALP_OK, ALP_EINFEASIBLE))
+        return [Result._from(x) for x in out]
+
+    def num_items(self, budget: int) -> int:
+        return int(lib().alp_num_items(self._h, budget))
+
+    def shard_range(self, budget: int, rank: int, world: int) -> tuple[int, int]:
+        lo = ctypes.c_uint64()
+        hi = ctypes.c_uint64()
+        _check(lib().alp_shard_range(self._h, budget, rank, world, ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
+
+    def search_shard(self, targets: Sequence[float], budget: int, lo: int, hi: int, keys_ptr: int, counts_ptr: int,
+                     stream_ptr: int | None = None) -> None:
+        """Async: evaluate items [lo, hi) for every target into device int64 keys/counts."""
+        t = _arr(targets, np.float64)
+        _check(lib().alp_search_shard(self._h, t.ctypes.data, len(t), budget, lo, hi, stream_ptr, keys_ptr,
+                                      counts_ptr))
+
+    def finalize(self, targets: Sequence[float], budget: int, keys_ptr: int, counts_ptr: int,
+                 stream_ptr: int | None = None) -> list[Result]:
+        t = _arr(targets, np.float64)
+        out = (_Result * len(t))()
+        _check(lib().alp_finalize(self._h, t.ctypes.data, len(t), budget, keys_ptr, counts_ptr, stream_ptr, out),
+               (ALP_OK, ALP_EINFEASIBLE))
+        return [Result._from(x) for x in out]
+
+    @property
+    def last_kernel_ms(self) -> float:
+        return float(lib().alp_last_kernel_ms(self._h))
+
+    @property
+    def last_launches(self) -> int:
+        return int(lib().alp_last_launches(self._h))

@@ -1,0 +1,751 @@
+// Host side of the C ABI declared in include/alp.h: validation, the static search plan (sort
+// list, u-sorted b columns), per-search launch geometry, and the kernel launches.  All ALP
+// arithmetic (option terms, objective sums, mins, counts, FP64 winner prediction) runs in the
+// kernels of alp_kernels.cu; this file only moves integers and pointers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "alp_internal.h"
+
+using namespace alp;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+alp_status fail(alp_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) return fail(ALP_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    release();
+    n = count ? count : 1;
+    return cudaMalloc(&p, n * sizeof(T));
+  }
+};
+
+template <class T>
+cudaError_t upload(DBuf<T> &d, const std::vector<T> &h, uint64_t &bytes) {
+  cudaError_t e = d.ensure(h.size());
+  if (e != cudaSuccess) return e;
+  if (!h.empty()) {
+    e = cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    bytes += h.size() * sizeof(T);
+  }
+  return e;
+}
+
+int ceil_log2(int k) {
+  int b = 0;
+  while ((1 << b) < k) ++b;
+  return b ? b : 1;
+}
+
+}  // namespace
+
+struct alp_s {
+  // problem
+  int M = 0, F = 1, nS = 0, nT = 0, nR = 0, K = 0;
+  bool from_terms = false;
+  std::vector<double> n, p, rate, lat, tmax;
+  std::vector<int> S, T, R, prof_off, min_units;
+  std::vector<int> u;  // [M*K] units s*t*d (integer grid product)
+  std::vector<float> tau_fixed;
+  std::vector<double> term_fixed, b_fixed;
+  uint64_t N = 0;
+  // static plan
+  int a_llm = -1, b_llm = 0, Ka = 1, Kb = 1, g0 = 0, g1 = 0, ng = 0, dig_bits = 1;
+  uint32_t L = 1, n_chunks = 1, n_groups = 1, nQ = 1, A = 1;
+  uint32_t pw[ALP_MAX_M] = {0};
+  std::vector<int> tile_s, bperm, bu, dv, dcnt;
+  std::vector<uint32_t> tile_e;
+  int umax_a = 0, umax_b = 0;
+  long long umax_total = 0;
+  // device
+  int device = 0, sm_count = 148;
+  DBuf<double> d_n, d_p, d_rate, d_lat, d_tmax;
+  DBuf<int> d_S, d_T, d_R, d_off, d_minu, d_u, d_tile_s, d_bperm, d_dv, d_dcnt;
+  DBuf<uint32_t> d_tile_e;
+  DBuf<float> d_tau_fixed;
+  DBuf<double> d_term_fixed, d_b_fixed;
+  // per-search scratch
+  DBuf<double> d_targets, d_term, d_b;
+  DBuf<float> d_tau;
+  DBuf<alp_result> d_res;
+  DBuf<unsigned long long> d_keys, d_counts;
+  DBuf<int> d_opts, d_pfeas;
+  DBuf<double> d_plat, d_pthr;
+  DBuf<long long> d_punits;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool ev_pending = false;
+  float last_ms = 0.f;
+  int last_launches = 0;
+  uint64_t h2d = 0;
+  SearchArgs last_args{};
+
+  DevProfiles dprof() const {
+    DevProfiles d;
+    d.M = M; d.F = F; d.nS = nS; d.nT = nT; d.nR = nR; d.K = K;
+    d.n = d_n.p; d.p = d_p.p; d.S = d_S.p; d.T = d_T.p; d.R = d_R.p; d.prof_off = d_off.p;
+    d.rate = d_rate.p; d.lat = d_lat.p; d.tmax = d_tmax.p;
+    d.min_units = min_units.empty() ? nullptr : d_minu.p;
+    return d;
+  }
+
+  ~alp_s() {
+    for (auto *b : {&d_n, &d_p, &d_rate, &d_lat, &d_tmax, &d_term_fixed, &d_b_fixed, &d_targets, &d_term, &d_b,
+                    &d_plat, &d_pthr})
+      b->release();
+    for (auto *b : {&d_S, &d_T, &d_R, &d_off, &d_minu, &d_u, &d_tile_s, &d_bperm, &d_dv, &d_dcnt, &d_opts, &d_pfeas})
+      b->release();
+    d_tile_e.release();
+    d_tau_fixed.release();
+    d_tau.release();
+    d_res.release();
+    d_keys.release();
+    d_counts.release();
+    d_punits.release();
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- static plan (build time)
+alp_status make_plan(alp_s *h) {
+  const int M = h->M, K = h->K;
+  h->N = 1;
+  for (int m = 0; m < M; ++m) {
+    if (h->N > (1ull << 62) / (uint64_t)K) return fail(ALP_EINVAL, "K^M exceeds 2^62 candidates (K=%d, M=%d)", K, M);
+    h->N *= (uint64_t)K;
+  }
+  h->b_llm = M - 1;
+  h->a_llm = M >= 2 ? M - 2 : -1;
+  h->Kb = K;
+  h->Ka = h->a_llm >= 0 ? K : 1;
+  h->g1 = h->a_llm >= 0 ? h->a_llm : 0;
+  h->dig_bits = ceil_log2(K);
+  int ng = 0;
+  uint64_t L = 1;
+  while (ng < std::min(4, h->g1) && L * (uint64_t)K <= (1ull << 18) && (ng + 1) * h->dig_bits <= 31) {
+    ++ng;
+    L *= (uint64_t)K;
+  }
+  h->ng = ng;
+  h->g0 = h->g1 - ng;
+  h->L = (uint32_t)L;
+  uint64_t chunks = 1;
+  for (int m = 0; m < h->g0; ++m) {
+    chunks *= (uint64_t)K;
+    if (chunks >= (1ull << 32)) return fail(ALP_EINVAL, "too many prefix chunks (K=%d, M=%d)", K, M);
+  }
+  h->n_chunks = (uint32_t)chunks;
+  for (int m = 0; m < ALP_MAX_M; ++m) h->pw[m] = 0;
+  for (int m = 0; m < h->g0; ++m) {
+    uint32_t p = 1;
+    for (int j = m + 1; j < h->g0; ++j) p *= (uint32_t)K;
+    h->pw[m] = p;
+  }
+  auto U = [&](int m, int k) { return h->u[(size_t)m * K + k]; };
+  // sort list: entries of the sort group ordered by unit sum (stable in canonical order), padded
+  // so every lane tile holds kRowsPerLane entries of one unit sum.
+  std::vector<int> sum(L);
+  int smax = 0;
+  for (uint32_t e = 0; e < L; ++e) {
+    uint32_t rem = e;
+    int s = 0;
+    for (int j = ng - 1; j >= 0; --j) {
+      s += U(h->g0 + j, (int)(rem % (uint32_t)K));
+      rem /= (uint32_t)K;
+    }
+    sum[e] = s;
+    smax = std::max(smax, s);
+  }
+  std::vector<uint32_t> order(L);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return sum[a] < sum[b]; });
+  h->tile_s.clear();
+  h->tile_e.clear();
+  const int T = kRowsPerLane;
+  auto pack = [&](uint32_t e) {
+    uint32_t rem = e, v = 0;
+    for (int j = ng - 1; j >= 0; --j) {
+      v |= (rem % (uint32_t)K) << (j * h->dig_bits);
+      rem /= (uint32_t)K;
+    }
+    return v;
+  };
+  for (size_t i = 0; i < order.size();) {
+    const int s = sum[order[i]];
+    h->tile_s.push_back(s);
+    for (int r = 0; r < T; ++r) {
+      if (i < order.size() && sum[order[i]] == s) {
+        h->tile_e.push_back(pack(order[i]));
+        ++i;
+      } else {
+        h->tile_e.push_back(kDummy);
+      }
+    }
+  }
+  while (h->tile_s.size() % kWarpTiles) {
+    h->tile_s.push_back(h->tile_s.back());
+    for (int r = 0; r < T; ++r) h->tile_e.push_back(kDummy);
+  }
+  h->n_groups = (uint32_t)(h->tile_s.size() / kWarpTiles);
+  // b columns sorted by units (stable): the feasible set for a remaining budget is a prefix.
+  h->bperm.resize(K);
+  std::iota(h->bperm.begin(), h->bperm.end(), 0);
+  std::stable_sort(h->bperm.begin(), h->bperm.end(), [&](int a, int b) { return U(h->b_llm, a) < U(h->b_llm, b); });
+  h->bu.resize(K);
+  for (int j = 0; j < K; ++j) h->bu[j] = U(h->b_llm, h->bperm[j]);
+  h->dv.clear();
+  for (int j = 0; j < K; ++j)
+    if (h->dv.empty() || h->dv.back() != h->bu[j]) h->dv.push_back(h->bu[j]);
+  h->dcnt.assign(h->dv.size() + 1, 0);
+  for (size_t i = 1; i <= h->dv.size(); ++i)
+    h->dcnt[i] = (int)(std::upper_bound(h->bu.begin(), h->bu.end(), h->dv[i - 1]) - h->bu.begin());
+  h->umax_b = h->bu.back();
+  h->umax_a = 0;
+  if (h->a_llm >= 0)
+    for (int k = 0; k < K; ++k) h->umax_a = std::max(h->umax_a, U(h->a_llm, k));
+  h->umax_total = 0;
+  for (int m = 0; m < M; ++m) {
+    int mx = 0;
+    for (int k = 0; k < K; ++k) mx = std::max(mx, U(m, k));
+    h->umax_total += mx;
+  }
+  // a-ranges: enough equal-cost work items to balance ~8 items per resident warp.
+  const uint64_t want = (uint64_t)h->sm_count * 24 * 8;
+  uint32_t nQ = 1;
+  while ((uint64_t)h->n_chunks * h->n_groups * nQ < want && nQ < (uint32_t)h->Ka) ++nQ;
+  h->A = (uint32_t)((h->Ka + nQ - 1) / nQ);
+  h->nQ = (uint32_t)((h->Ka + h->A - 1) / h->A);
+  while ((uint64_t)h->n_chunks * h->L * h->nQ >= (1ull << 32)) {
+    if (h->nQ == 1) return fail(ALP_EINVAL, "problem too large: > 2^32 segments");
+    h->A *= 2;
+    h->nQ = (uint32_t)((h->Ka + h->A - 1) / h->A);
+  }
+  return ALP_OK;
+}
+
+alp_status upload_plan(alp_s *h) {
+  uint64_t &B = h->h2d;
+  CU(upload(h->d_tile_s, h->tile_s, B));
+  CU(upload(h->d_tile_e, h->tile_e, B));
+  CU(upload(h->d_bperm, h->bperm, B));
+  CU(upload(h->d_dv, h->dv, B));
+  CU(upload(h->d_dcnt, h->dcnt, B));
+  CU(upload(h->d_u, h->u, B));
+  return ALP_OK;
+}
+
+alp_status init_device(alp_s *h) {
+  CU(cudaGetDevice(&h->device));
+  CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
+  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CU(cudaEventCreate(&h->ev0));
+  CU(cudaEventCreate(&h->ev1));
+  return ALP_OK;
+}
+
+void compute_units(alp_s *h) {
+  h->u.assign((size_t)h->M * h->K, 0);
+  for (int m = 0; m < h->M; ++m)
+    for (int k = 0; k < h->K; ++k) {
+      const int r_i = k % h->nR, t_i = (k / h->nR) % h->nT, s_i = k / (h->nR * h->nT);
+      h->u[(size_t)m * h->K + k] = h->S[s_i] * h->T[t_i] * h->R[r_i];
+    }
+}
+
+bool ascending(const int32_t *v, int n, int lo) {
+  for (int i = 0; i < n; ++i) {
+    if (v[i] < lo) return false;
+    if (i && v[i] <= v[i - 1]) return false;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- per-search geometry
+struct Geometry {
+  SearchArgs a;
+  int grid;
+};
+
+alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, uint64_t hi, Geometry &g) {
+  if (budget < 0) return fail(ALP_EINVAL, "budget_units < 0");
+  const long long Reff = std::min<long long>(budget, h->umax_total);
+  if (Reff > 16384) return fail(ALP_EINVAL, "budget_units (capped at the total max units) exceeds 16384");
+  SearchArgs &a = g.a;
+  memset(&a, 0, sizeof(a));
+  a.M = h->M; a.K = h->K; a.g0 = h->g0; a.g1 = h->g1; a.a_llm = h->a_llm; a.b_llm = h->b_llm;
+  a.Ka = h->Ka; a.Kb = h->Kb; a.ng = h->ng; a.dig_bits = h->dig_bits; a.L = h->L; a.n_chunks = h->n_chunks;
+  a.n_groups = h->n_groups; a.nQ = h->nQ; a.A = h->A; a.item_lo = lo; a.item_hi = hi;
+  a.budget = (int)Reff;
+  a.Rc = (int)std::min<long long>(Reff, (long long)h->umax_a + h->umax_b);
+  a.n_targets = n_targets;
+  a.D = (int)(std::upper_bound(h->dv.begin(), h->dv.end(), (int)Reff) - h->dv.begin());
+  for (int m = 0; m < ALP_MAX_M; ++m) a.pw[m] = h->pw[m];
+  const int rows = a.D + 1;
+  a.rows_max = rows;
+  auto align16 = [](int x) { return (x + 15) & ~15; };
+  auto layout = [&](int W) {
+    a.bchunk_w = W;
+    a.n_bchunks = (h->Kb + W - 1) / W;
+    a.bchunk_wpad = W <= 34 ? (W + 1) / 2 * 2 : (W + 3) / 4 * 4;
+    a.row_stride = a.bchunk_wpad;
+    while (a.row_stride % 8 != 4) ++a.row_stride;
+    int off = 0;
+    a.off_tau = off; off = align16(off + h->g1 * h->K * 4);
+    a.off_u = off; off = align16(off + h->g0 * h->K * 4);
+    a.off_a = off; off = align16(off + h->Ka * 8);
+    a.off_lut = off; off = align16(off + 2 * (a.budget + 2) * 4);
+    a.off_cnt = off; off = align16(off + (int)h->nQ * (a.Rc + 2) * 4);
+    a.off_tmp = off; off = align16(off + (2 * h->Kb + 3 + rows) * 4);
+    a.off_btab = off; off = align16(off + rows * a.row_stride * 4);
+    a.smem_bytes = off;
+    return off;
+  };
+  int W = h->Kb;
+  while (layout(W) > 72 * 1024 && W > 64) W = (W + 1) / 2;
+  if (a.smem_bytes > 220 * 1024) return fail(ALP_EINVAL, "shared-memory tables too large (%d B)", a.smem_bytes);
+  a.tau = nullptr;  // set by caller
+  a.u = h->d_u.p; a.tile_s = h->d_tile_s.p; a.tile_e = h->d_tile_e.p; a.bperm = h->d_bperm.p;
+  a.dv = h->d_dv.p; a.dcnt = h->d_dcnt.p;
+  int bps = search_max_blocks_per_sm(a);
+  if (bps < 1) return fail(ALP_ECUDA, "search kernel cannot be resident (smem %d B)", a.smem_bytes);
+  g.grid = h->sm_count * bps;
+  return ALP_OK;
+}
+
+alp_status ensure_scratch(alp_s *h, int n) {
+  const size_t MK = (size_t)h->M * h->K;
+  CU(h->d_targets.ensure(n));
+  CU(h->d_tau.ensure(n * MK));
+  CU(h->d_term.ensure(n * MK));
+  CU(h->d_b.ensure(n * MK));
+  CU(h->d_res.ensure(n));
+  CU(h->d_keys.ensure(n));
+  CU(h->d_counts.ensure(n));
+  return ALP_OK;
+}
+
+// K1 for n targets into the scratch tables (profiles mode) or replicate the fixed terms.
+alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st, unsigned long long *keys,
+                         unsigned long long *counts) {
+  const size_t MK = (size_t)h->M * h->K;
+  CU(cudaMemcpyAsync(h->d_targets.p, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (h->from_terms) {
+    for (int t = 0; t < n; ++t) {
+      CU(cudaMemcpyAsync(h->d_tau.p + t * MK, h->d_tau_fixed.p, MK * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->d_term.p + t * MK, h->d_term_fixed.p, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->d_b.p + t * MK, h->d_b_fixed.p, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    if (keys) CU(launch_init_keys(keys, counts, n, st));
+    return ALP_OK;
+  }
+  OptionArgs o;
+  o.prof = h->dprof();
+  o.targets = h->d_targets.p;
+  o.n_targets = n;
+  o.tau = h->d_tau.p;
+  o.term = h->d_term.p;
+  o.b = h->d_b.p;
+  o.u = h->d_u.p;
+  o.keys = keys;
+  o.counts = counts;
+  CU(launch_option_table(o, st));
+  return ALP_OK;
+}
+
+alp_status check_targets(const double *targets, int n) {
+  if (!targets || n < 1) return fail(ALP_EINVAL, "targets: need n >= 1 targets");
+  for (int i = 0; i < n; ++i)
+    if (!(targets[i] > 0.0) || !std::isfinite(targets[i])) return fail(ALP_EINVAL, "targets[%d] must be finite and > 0", i);
+  return ALP_OK;
+}
+
+alp_status search_shard_impl(alp_s *h, const double *targets, int n, int64_t budget, uint64_t lo, uint64_t hi,
+                             cudaStream_t st, unsigned long long *keys, unsigned long long *counts) {
+  alp_status s = check_targets(targets, n);
+  if (s != ALP_OK) return s;
+  CU(cudaSetDevice(h->device));
+  Geometry g;
+  s = make_geometry(h, n, budget, 0, 0, g);
+  if (s != ALP_OK) return s;
+  const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
+  if (lo > hi || hi > items) return fail(ALP_EINVAL, "item range [%llu, %llu) outside [0, %llu)",
+                                         (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)items);
+  s = ensure_scratch(h, n);
+  if (s != ALP_OK) return s;
+  s = option_tables(h, targets, n, st, keys, counts);
+  if (s != ALP_OK) return s;
+  g.a.item_lo = lo;
+  g.a.item_hi = hi;
+  g.a.tau = h->d_tau.p;
+  g.a.keys = keys;
+  g.a.counts = counts;
+  CU(cudaEventRecord(h->ev0, st));
+  if (hi > lo) CU(launch_search(g.a, g.grid, st));
+  CU(cudaEventRecord(h->ev1, st));
+  h->ev_pending = true;
+  h->last_args = g.a;
+  h->last_launches = 2;
+  return ALP_OK;
+}
+
+alp_status finalize_impl(alp_s *h, const double *targets, int n, int64_t budget, const unsigned long long *keys,
+                         const unsigned long long *counts, cudaStream_t st, alp_result *out) {
+  if (!out) return fail(ALP_EINVAL, "out is NULL");
+  CU(cudaSetDevice(h->device));
+  Geometry g;
+  alp_status s = make_geometry(h, n, budget, 0, 0, g);
+  if (s != ALP_OK) return s;
+  s = ensure_scratch(h, n);
+  if (s != ALP_OK) return s;
+  // option tables must describe these targets (the shard call computed them on this handle)
+  (void)targets;
+  FinalizeArgs f;
+  f.s = g.a;
+  f.s.tau = h->d_tau.p;
+  f.term = h->d_term.p;
+  f.b = h->d_b.p;
+  f.S = h->from_terms ? nullptr : h->d_S.p;
+  f.T = h->d_T.p;
+  f.R = h->d_R.p;
+  f.nS = h->nS; f.nT = h->nT; f.nR = h->nR;
+  f.N = h->N;
+  f.keys = keys;
+  f.counts = counts;
+  f.out = h->d_res.p;
+  CU(launch_finalize(f, st));
+  CU(cudaMemcpyAsync(out, h->d_res.p, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  h->last_launches += 1;
+  if (h->ev_pending) {
+    CU(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
+    h->ev_pending = false;
+  }
+  int any = 0;
+  for (int i = 0; i < n; ++i) any |= out[i].found;
+  return any ? ALP_OK : ALP_EINFEASIBLE;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *alp_last_error(void) { return g_err.c_str(); }
+
+alp_status alp_build(const alp_desc *d, alp_t **out) {
+  if (!out) return fail(ALP_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!d) return fail(ALP_EINVAL, "desc is NULL");
+  if (d->M < 1 || d->M > ALP_MAX_M) return fail(ALP_EINVAL, "M must be in 1..%d (got %d)", ALP_MAX_M, d->M);
+  if (d->F < 1) return fail(ALP_EINVAL, "F must be >= 1");
+  if (!d->n || !d->p) return fail(ALP_EINVAL, "n/p is NULL");
+  for (int m = 0; m < d->M; ++m) {
+    if (!(d->n[m] > 0) || !std::isfinite(d->n[m])) return fail(ALP_EINVAL, "n[%d] must be finite and > 0", m);
+    if (!(d->p[m] >= 1) || !std::isfinite(d->p[m])) return fail(ALP_EINVAL, "p[%d] must be finite and >= 1", m);
+  }
+  if (d->nS < 1 || d->nT < 1 || d->nR < 1) return fail(ALP_EINVAL, "nS, nT, nR must be >= 1");
+  const long long K = (long long)d->nS * d->nT * d->nR;
+  if (K > ALP_MAX_K) return fail(ALP_EINVAL, "K = nS*nT*nR = %lld exceeds %d", K, ALP_MAX_K);
+  if (!d->share_units || !ascending(d->share_units, d->nS, 1) || d->share_units[d->nS - 1] > d->F)
+    return fail(ALP_EINVAL, "share_units must be strictly ascending within 1..F");
+  if (!d->tp || !ascending(d->tp, d->nT, 1)) return fail(ALP_EINVAL, "tp must be strictly ascending and >= 1");
+  if (!d->replicas || !ascending(d->replicas, d->nR, 1))
+    return fail(ALP_EINVAL, "replicas must be strictly ascending and >= 1");
+  if (d->pct < 0 || d->pct > 3) return fail(ALP_EINVAL, "pct must be 0..3");
+  const double *lat = d->lat[d->pct];
+  if (!lat) return fail(ALP_EINVAL, "lat[%d] (selected percentile column) is NULL", d->pct);
+  if (!d->prof_off || !d->rate) return fail(ALP_EINVAL, "prof_off/rate is NULL");
+  const int C = d->M * d->nT;
+  if (d->prof_off[0] != 0) return fail(ALP_EINVAL, "prof_off[0] must be 0");
+  double term_bound = 0.0;
+  for (int c = 0; c < C; ++c) {
+    const int a = d->prof_off[c], b = d->prof_off[c + 1];
+    if (b <= a) return fail(ALP_EINVAL, "profile of LLM %d tp index %d has no points", c / d->nT, c % d->nT);
+    for (int i = a; i < b; ++i) {
+      if (!std::isfinite(d->rate[i]) || d->rate[i] < 0) return fail(ALP_EINVAL, "rate[%d] must be finite and >= 0", i);
+      if (i > a && !(d->rate[i] > d->rate[i - 1]))
+        return fail(ALP_EINVAL, "rates of LLM %d tp index %d not strictly increasing", c / d->nT, c % d->nT);
+      if (!(lat[i] > 0) || !std::isfinite(lat[i])) return fail(ALP_EINVAL, "lat[%d] must be finite and > 0", i);
+      if (i > a && lat[i] < lat[i - 1])
+        return fail(ALP_EINVAL, "latencies of LLM %d tp index %d decrease", c / d->nT, c % d->nT);
+    }
+    if (d->tmax && (!std::isfinite(d->tmax[c]) || d->tmax[c] < d->rate[b - 1]))
+      return fail(ALP_EINVAL, "tmax[%d] must be finite and >= the last profiled rate", c);
+    if (d->min_units && d->min_units[c] < 0) return fail(ALP_EINVAL, "min_units[%d] < 0", c);
+  }
+  for (int m = 0; m < d->M; ++m) {
+    double lmax = 0;
+    for (int t = 0; t < d->nT; ++t) lmax = std::max(lmax, lat[d->prof_off[m * d->nT + t + 1] - 1]);
+    term_bound += lmax * ((double)d->F / d->share_units[0]) * (d->n[m] / d->p[m]) * 1.0000001;
+  }
+  if (!(term_bound < 1e37)) return fail(ALP_EINVAL, "latency terms could overflow binary32 (sum bound %g)", term_bound);
+
+  alp_s *h = new alp_s();
+  h->M = d->M; h->F = d->F; h->nS = d->nS; h->nT = d->nT; h->nR = d->nR; h->K = (int)K;
+  h->n.assign(d->n, d->n + d->M);
+  h->p.assign(d->p, d->p + d->M);
+  h->S.assign(d->share_units, d->share_units + d->nS);
+  h->T.assign(d->tp, d->tp + d->nT);
+  h->R.assign(d->replicas, d->replicas + d->nR);
+  h->prof_off.assign(d->prof_off, d->prof_off + C + 1);
+  const int P = d->prof_off[C];
+  h->rate.assign(d->rate, d->rate + P);
+  h->lat.assign(lat, lat + P);
+  h->tmax.resize(C);
+  for (int c = 0; c < C; ++c) h->tmax[c] = d->tmax ? d->tmax[c] : d->rate[d->prof_off[c + 1] - 1];
+  if (d->min_units) h->min_units.assign(d->min_units, d->min_units + C);
+  compute_units(h);
+  alp_status s = init_device(h);
+  if (s == ALP_OK) s = make_plan(h);
+  if (s == ALP_OK) s = upload_plan(h);
+  if (s == ALP_OK) {
+    uint64_t &B = h->h2d;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = upload(h->d_n, h->n, B);
+    if (e == cudaSuccess) e = upload(h->d_p, h->p, B);
+    if (e == cudaSuccess) e = upload(h->d_S, h->S, B);
+    if (e == cudaSuccess) e = upload(h->d_T, h->T, B);
+    if (e == cudaSuccess) e = upload(h->d_R, h->R, B);
+    if (e == cudaSuccess) e = upload(h->d_off, h->prof_off, B);
+    if (e == cudaSuccess) e = upload(h->d_rate, h->rate, B);
+    if (e == cudaSuccess) e = upload(h->d_lat, h->lat, B);
+    if (e == cudaSuccess) e = upload(h->d_tmax, h->tmax, B);
+    if (e == cudaSuccess && !h->min_units.empty()) e = upload(h->d_minu, h->min_units, B);
+    if (e != cudaSuccess) s = fail(ALP_ECUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  if (s != ALP_OK) {
+    delete h;
+    return s;
+  }
+  *out = h;
+  return ALP_OK;
+}
+
+alp_status alp_build_from_terms(int32_t M, int32_t K, const float *tau, const int32_t *u, alp_t **out) {
+  if (!out) return fail(ALP_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (M < 1 || M > ALP_MAX_M) return fail(ALP_EINVAL, "M must be in 1..%d", ALP_MAX_M);
+  if (K < 1 || K > ALP_MAX_K) return fail(ALP_EINVAL, "K must be in 1..%d", ALP_MAX_K);
+  if (!tau || !u) return fail(ALP_EINVAL, "tau/u is NULL");
+  double bound = 0;
+  for (int m = 0; m < M; ++m) {
+    double mx = 0;
+    for (int k = 0; k < K; ++k) {
+      const float t = tau[m * K + k];
+      if (std::isnan(t) || t < 0) return fail(ALP_EINVAL, "tau[%d] must be >= 0 or +inf", m * K + k);
+      if (u[m * K + k] < 0) return fail(ALP_EINVAL, "u[%d] < 0", m * K + k);
+      if (std::isfinite(t)) mx = std::max(mx, (double)t);
+    }
+    bound += mx;
+  }
+  if (!(bound < 1e37)) return fail(ALP_EINVAL, "terms could overflow binary32");
+  alp_s *h = new alp_s();
+  h->from_terms = true;
+  h->M = M; h->K = K; h->F = 1; h->nS = 1; h->nT = 1; h->nR = K;
+  h->u.assign(u, u + (size_t)M * K);
+  h->tau_fixed.assign(tau, tau + (size_t)M * K);
+  h->term_fixed.resize((size_t)M * K);
+  h->b_fixed.assign((size_t)M * K, INFINITY);
+  for (size_t i = 0; i < h->tau_fixed.size(); ++i) h->term_fixed[i] = (double)h->tau_fixed[i];
+  h->S = {1};
+  h->T = {1};
+  h->R.resize(K);
+  std::iota(h->R.begin(), h->R.end(), 1);
+  alp_status s = init_device(h);
+  if (s == ALP_OK) s = make_plan(h);
+  if (s == ALP_OK) s = upload_plan(h);
+  if (s == ALP_OK) {
+    cudaError_t e = upload(h->d_tau_fixed, h->tau_fixed, h->h2d);
+    if (e == cudaSuccess) e = upload(h->d_term_fixed, h->term_fixed, h->h2d);
+    if (e == cudaSuccess) e = upload(h->d_b_fixed, h->b_fixed, h->h2d);
+    if (e == cudaSuccess) e = upload(h->d_T, h->T, h->h2d);
+    if (e == cudaSuccess) e = upload(h->d_R, h->R, h->h2d);
+    if (e != cudaSuccess) s = fail(ALP_ECUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  if (s != ALP_OK) {
+    delete h;
+    return s;
+  }
+  *out = h;
+  return ALP_OK;
+}
+
+void alp_destroy(alp_t *h) { delete h; }
+
+uint64_t alp_num_candidates(const alp_t *h) { return h ? h->N : 0; }
+
+uint64_t alp_h2d_bytes(const alp_t *h) { return h ? h->h2d : 0; }
+
+alp_status alp_decode(const alp_t *h, uint64_t index, int32_t *s, int32_t *t, int32_t *r) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (index >= h->N) return fail(ALP_EINVAL, "index %llu >= N", (unsigned long long)index);
+  for (int m = h->M - 1; m >= 0; --m) {
+    const int k = (int)(index % (uint64_t)h->K);
+    index /= (uint64_t)h->K;
+    const int r_i = k % h->nR, t_i = (k / h->nR) % h->nT, s_i = k / (h->nR * h->nT);
+    if (s) s[m] = h->S[s_i];
+    if (t) t[m] = h->T[t_i];
+    if (r) r[m] = h->R[r_i];
+  }
+  return ALP_OK;
+}
+
+alp_status alp_option_table(alp_t *h, double lambda, float *tau, double *term, double *b, int32_t *u) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  alp_status s = check_targets(&lambda, 1);
+  if (s != ALP_OK) return s;
+  CU(cudaSetDevice(h->device));
+  s = ensure_scratch(h, 1);
+  if (s != ALP_OK) return s;
+  s = option_tables(h, &lambda, 1, h->stream, nullptr, nullptr);
+  if (s != ALP_OK) return s;
+  const size_t MK = (size_t)h->M * h->K;
+  if (tau) CU(cudaMemcpyAsync(tau, h->d_tau.p, MK * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (term) CU(cudaMemcpyAsync(term, h->d_term.p, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (b) CU(cudaMemcpyAsync(b, h->d_b.p, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (u) memcpy(u, h->u.data(), MK * sizeof(int32_t));
+  return ALP_OK;
+}
+
+alp_status alp_predict(alp_t *h, const int32_t *opts, int32_t n, double lambda, int64_t budget, double *latency,
+                       double *throughput, int64_t *units, int32_t *feasible) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (h->from_terms) return fail(ALP_EINVAL, "alp_predict needs a profile-built handle");
+  if (!opts || n < 1) return fail(ALP_EINVAL, "opts: need n >= 1 allocations");
+  alp_status s = check_targets(&lambda, 1);
+  if (s != ALP_OK) return s;
+  for (long long i = 0; i < (long long)n * h->M; ++i)
+    if (opts[i] < 0 || opts[i] >= h->K) return fail(ALP_EINVAL, "opts[%lld] out of range 0..K-1", i);
+  CU(cudaSetDevice(h->device));
+  CU(h->d_opts.ensure((size_t)n * h->M));
+  CU(h->d_plat.ensure(n));
+  CU(h->d_pthr.ensure(n));
+  CU(h->d_punits.ensure(n));
+  CU(h->d_pfeas.ensure(n));
+  CU(cudaMemcpyAsync(h->d_opts.p, opts, (size_t)n * h->M * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  PredictArgs a;
+  a.prof = h->dprof();
+  a.opts = h->d_opts.p;
+  a.n = n;
+  a.lambda = lambda;
+  a.budget = budget;
+  a.latency = h->d_plat.p;
+  a.throughput = h->d_pthr.p;
+  a.units = h->d_punits.p;
+  a.feasible = h->d_pfeas.p;
+  CU(launch_predict(a, h->stream));
+  if (latency) CU(cudaMemcpyAsync(latency, a.latency, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (throughput) CU(cudaMemcpyAsync(throughput, a.throughput, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (units) CU(cudaMemcpyAsync(units, a.units, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  if (feasible) CU(cudaMemcpyAsync(feasible, a.feasible, n * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return ALP_OK;
+}
+
+uint64_t alp_num_items(const alp_t *h, int64_t budget_units) {
+  (void)budget_units;
+  return h ? (uint64_t)h->n_chunks * h->n_groups * h->nQ : 0;
+}
+
+alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, int32_t world, uint64_t *lo,
+                           uint64_t *hi) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ALP_EINVAL, "need 0 <= rank < world");
+  if (!lo || !hi) return fail(ALP_EINVAL, "lo/hi is NULL");
+  const uint64_t n = alp_num_items(h, budget_units);
+  // contiguous, balanced to +-1 item; computed without overflow for n < 2^63
+  const uint64_t q = n / (uint64_t)world, r = n % (uint64_t)world;
+  *lo = q * (uint64_t)rank + std::min<uint64_t>((uint64_t)rank, r);
+  *hi = *lo + q + ((uint64_t)rank < r ? 1 : 0);
+  return ALP_OK;
+}
+
+alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
+                            uint64_t hi, void *stream, int64_t *d_keys, int64_t *d_counts) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
+  return search_shard_impl(h, targets, n, budget_units, lo, hi, stream ? (cudaStream_t)stream : h->stream,
+                           reinterpret_cast<unsigned long long *>(d_keys),
+                           reinterpret_cast<unsigned long long *>(d_counts));
+}
+
+alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budget_units, const int64_t *d_keys,
+                        const int64_t *d_counts, void *stream, alp_result *out) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
+  alp_status s = check_targets(targets, n);
+  if (s != ALP_OK) return s;
+  return finalize_impl(h, targets, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
+                       reinterpret_cast<const unsigned long long *>(d_counts),
+                       stream ? (cudaStream_t)stream : h->stream, out);
+}
+
+alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t budget_units, alp_result *out) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  alp_status s = check_targets(targets, n);
+  if (s != ALP_OK) return s;
+  CU(cudaSetDevice(h->device));
+  s = ensure_scratch(h, n);
+  if (s != ALP_OK) return s;
+  const uint64_t items = alp_num_items(h, budget_units);
+  s = search_shard_impl(h, targets, n, budget_units, 0, items, h->stream, h->d_keys.p, h->d_counts.p);
+  if (s != ALP_OK) return s;
+  return finalize_impl(h, targets, n, budget_units, h->d_keys.p, h->d_counts.p, h->stream, out);
+}
+
+alp_status alp_search(alp_t *h, double target, int64_t budget_units, alp_result *out) {
+  return alp_search_batch(h, &target, 1, budget_units, out);
+}
+
+float alp_last_kernel_ms(const alp_t *h) {
+  if (!h) return 0.f;
+  alp_s *m = const_cast<alp_s *>(h);
+  if (m->ev_pending && cudaEventSynchronize(m->ev1) == cudaSuccess) {
+    cudaEventElapsedTime(&m->last_ms, m->ev0, m->ev1);
+    m->ev_pending = false;
+  }
+  return m->last_ms;
+}
+
+int32_t alp_last_launches(const alp_t *h) { return h ? h->last_launches : 0; }
+
+}  // extern "C"

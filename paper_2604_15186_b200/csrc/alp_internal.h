@@ -1,0 +1,105 @@
+// Internal declarations shared by the host library (alp_api.cu) and the kernels (alp_kernels.cu).
+// Not part of the C ABI (include/alp.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/alp.h"
+
+namespace alp {
+
+constexpr int kRowsPerLane = 8;          // T: rows (sort-list entries) per lane tile
+constexpr int kWarpTiles = 32;           // lane tiles per warp group
+constexpr int kThreads = 256;            // threads per search block
+constexpr uint32_t kDummy = 0xFFFFFFFFu; // padded row marker in the tile list
+constexpr unsigned long long kKeyNone = 0x7FFFFFFFFFFFFFFFull;  // INT64_MAX: nothing feasible
+
+// Device-resident profile description (uploaded by alp_build).
+struct DevProfiles {
+  int M, F, nS, nT, nR, K;
+  const double *n, *p;
+  const int *S, *T, *R;
+  const int *prof_off;
+  const double *rate, *lat, *tmax;
+  const int *min_units;  // nullptr = no floor
+};
+
+// Option-term kernel (K1) arguments.
+struct OptionArgs {
+  DevProfiles prof;
+  const double *targets;
+  int n_targets;
+  float *tau;      // [n_t][M][K]
+  double *term;    // [n_t][M][K]
+  double *b;       // [n_t][M][K]
+  int *u;          // [M][K]
+  unsigned long long *keys;    // [n_t] initialised to kKeyNone (may be null)
+  unsigned long long *counts;  // [n_t] initialised to 0 (may be null)
+};
+
+// Search kernel (K2) arguments: the static plan + per-search values.
+struct SearchArgs {
+  int M, K;
+  int g0, g1;            // prefix LLMs [0,g0), sort-group LLMs [g0,g1)
+  int a_llm, b_llm;      // a = LLM M-2 (or -1: virtual single zero option), b = LLM M-1
+  int Ka, Kb;
+  int ng, dig_bits;      // sort group size, bits per packed digit
+  uint32_t L;            // sort-list length K^ng
+  uint32_t n_chunks;     // K^g0
+  uint32_t n_groups;     // warp groups of 32 lane tiles
+  uint32_t nQ, A;        // a-ranges: a in [q*A, min((q+1)*A, Ka))
+  uint64_t item_lo, item_hi;
+  int budget;            // R (capped at the total max units; <= kMaxBudget)
+  int Rc;                // count-table upper clamp min(R, Umax_a + Umax_b)
+  int n_targets;
+  int n_bchunks, bchunk_w, bchunk_wpad;  // b columns (u-sorted) split in chunks
+  int row_stride;        // floats per masked row (== 4 mod 8)
+  int rows_max;          // max distinct masked rows per chunk
+  // device tables
+  const float *tau;      // [n_t][M][K]
+  const int *u;          // [M][K]
+  const int *tile_s;     // [n_tiles] units of the lane tile's sort-group options
+  const uint32_t *tile_e;// [n_tiles][T] packed sort-group digits (kDummy = padding)
+  const int *bperm;      // [Kb] canonical option of u-sorted column j
+  const int *dv;         // [Dall] distinct b unit values, ascending
+  const int *dcnt;       // [Dall+1] dcnt[i] = #u-sorted columns with u <= dv[i-1] (dcnt[0] = 0)
+  int D;                 // #distinct b unit values <= budget (masked rows = D + 1)
+  uint32_t pw[ALP_MAX_M];// pw[m] = K^(g0-1-m): prefix digit m of a chunk index
+  unsigned long long *keys;
+  unsigned long long *counts;
+  // shared memory layout (byte offsets)
+  int off_tau, off_u, off_a, off_lut, off_cnt, off_btab, off_tmp, smem_bytes;
+};
+
+struct FinalizeArgs {
+  SearchArgs s;
+  const double *term;    // [n_t][M][K]
+  const double *b;       // [n_t][M][K]
+  const int *S, *T, *R;  // grids (for the winner's (share, tp, replicas))
+  int nS, nT, nR;
+  uint64_t N;
+  const unsigned long long *keys;
+  const unsigned long long *counts;
+  alp_result *out;       // [n_t] device
+};
+
+struct PredictArgs {
+  DevProfiles prof;
+  const int *opts;       // [n][M]
+  int n;
+  double lambda;
+  long long budget;
+  double *latency, *throughput;
+  long long *units;
+  int *feasible;
+};
+
+// Launchers (alp_kernels.cu). Return cudaError_t of the launch.
+cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st);
+cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, cudaStream_t st);
+cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
+cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
+cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
+int search_max_blocks_per_sm(const SearchArgs &a);
+
+}  // namespace alp

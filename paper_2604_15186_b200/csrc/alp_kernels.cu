@@ -1,0 +1,632 @@
+// sm_100a kernels of the exhaustive ALP allocation search (Scepsy, arXiv 2604.15186).
+//
+//   K1 k_option_table  per (target, LLM, option): FP64 option terms of PAPER.md:355-359
+//                      (Eq. 1 term, Eq. 2 term, feasibility) -> binary32 tau (reading R7).
+//   K2 k_search        exhaustive evaluation of every candidate: canonical binary32 Eq. 1 sum,
+//                      budget + target feasibility, argmin (lowest index on ties) and count.
+//   K3 k_finalize      decodes the reduced 64-bit key into the lowest canonical index and the
+//                      FP64 Eq. 1 / Eq. 2 prediction of the winner.
+//   k_predict          FP64 prediction of given allocations (alp_predict).
+//
+// K2 is the hot path.  Its design:
+//  * the candidate digits are split into  prefix LLMs [0,g0) | sort-group LLMs [g0,g1) |
+//    a = LLM M-2 | b = LLM M-1.  A "row" is (prefix, sort-group) digits; its canonical partial
+//    sum Q_row = ((0 + tau_0) + tau_1) + ... is computed once and reused for Ka*Kb candidates.
+//  * the b options are sorted by units; for a remaining budget r the feasible b options are a
+//    prefix of that order, so a shared-memory "masked row" (tau_b, or +inf when u_b > r) folds
+//    the budget test into the value.  Sort-group entries are pre-sorted (static, at build) by
+//    their unit sum so the 8 rows of a lane share one remaining budget -> one masked row.
+//  * per candidate the SASS is half an FADD2 (add.rn.f32x2, binary32 RNE, scalar broadcast of
+//    Q_a) and half an FMNMX3 (3-input min): 1 issue slot per candidate, with the b values
+//    streamed by LDS.128 (4 columns x 8 rows = 32 candidates per load).
+//  * argmin: per-row min over the item's (a,b) block, folded into the thread's (value, segment)
+//    best with a lowest-segment tie-break; keys = bits(value)<<32 | segment; warp shuffle ->
+//    block -> atomicMin.  K3 re-scans the single winning segment for the lowest index.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "alp_internal.h"
+
+namespace alp {
+
+__device__ __forceinline__ float finf() { return __int_as_float(0x7f800000); }
+
+// ------------------------------------------------------------------ option terms (FP64, no FMA)
+// SURVEY.md §8(c) / DESIGN.md §3: every operation is an explicit IEEE RNE intrinsic, in the
+// order written, so the result is bit-identical to the oracle's -ffp-contract=off C code.
+__device__ double lookup_latency(const double *r, const double *l, int P, double x) {
+  // R3: clamp below r_0; i = max{i : r_i <= x}; hold L_last at/after the last point.
+  if (x <= r[0]) return l[0];
+  int i = 0;
+  for (int j = 0; j < P; ++j)
+    if (r[j] <= x) i = j;
+  if (i == P - 1) return l[P - 1];
+  double dl = __dsub_rn(l[i + 1], l[i]);
+  double dx = __dsub_rn(x, r[i]);
+  double dr = __dsub_rn(r[i + 1], r[i]);
+  double w = __ddiv_rn(dx, dr);
+  return __dadd_rn(l[i], __dmul_rn(dl, w));
+}
+
+__device__ int option_terms(const DevProfiles &P, double lambda, int m, int k, float *tau, double *term,
+                            double *b, int *u) {
+  const int r_i = k % P.nR;
+  const int t_i = (k / P.nR) % P.nT;
+  const int s_i = k / (P.nR * P.nT);
+  const int s_units = P.S[s_i], t = P.T[t_i], d = P.R[r_i];
+  const int c = m * P.nT + t_i;
+  const double T = P.tmax[c];
+  const double lam_m = __dmul_rn(lambda, P.n[m]);              // lambda_m = lambda_W n_m
+  const double rate = __ddiv_rn(lam_m, (double)d);            // per replica
+  const double f = __ddiv_rn((double)s_units, (double)P.F);   // per-shard share
+  const double x = __ddiv_rn(rate, f);                        // L'(l) = L(l/f)/f
+  const double cap = __dmul_rn(f, T);
+  const double bb = __ddiv_rn(__dmul_rn((double)d, cap), P.n[m]);  // Eq. 2 term
+  int ok = (x <= T) && (bb >= lambda);                        // R4
+  if (P.min_units && s_units < P.min_units[c]) ok = 0;        // memory floor
+  *b = bb;
+  *u = s_units * t * d;
+  if (ok) {
+    const int o = P.prof_off[c];
+    const double L = lookup_latency(P.rate + o, P.lat + o, P.prof_off[c + 1] - o, x);
+    const double tt = __dmul_rn(__ddiv_rn(L, f), __ddiv_rn(P.n[m], P.p[m]));  // Eq. 1 term
+    *term = tt;
+    *tau = __double2float_rn(tt);
+  } else {
+    *term = CUDART_INF;
+    *tau = finf();
+  }
+  return ok;
+}
+
+__global__ void k_option_table(const OptionArgs A) {
+  const int MK = A.prof.M * A.prof.K;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < A.n_targets) {
+    if (A.keys) A.keys[i] = kKeyNone;
+    if (A.counts) A.counts[i] = 0ull;
+  }
+  if (i >= A.n_targets * MK) return;
+  const int t = i / MK, mk = i % MK, m = mk / A.prof.K, k = mk % A.prof.K;
+  float tau;
+  double term, b;
+  int u;
+  option_terms(A.prof, A.targets[t], m, k, &tau, &term, &b, &u);
+  A.tau[i] = tau;
+  A.term[i] = term;
+  A.b[i] = b;
+  if (t == 0) A.u[mk] = u;
+}
+
+__global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    keys[i] = kKeyNone;
+    counts[i] = 0ull;
+  }
+}
+
+// ------------------------------------------------------------------ search kernel (K2)
+// add.rn.f32x2 {v0,v1} = {q,q} + {b0,b1}  (SASS: FADD2 with scalar-broadcast operand)
+__device__ __forceinline__ void add2(float &v0, float &v1, float q, float b0, float b1) {
+  asm("{.reg .b64 x,y,z;\n\tmov.b64 x,{%2,%2};\n\tmov.b64 y,{%3,%4};\n\tadd.rn.f32x2 z,x,y;\n\tmov.b64 {%0,%1},z;}"
+      : "=f"(v0), "=f"(v1)
+      : "f"(q), "f"(b0), "f"(b1));
+}
+// add.rn.f32x2 {v0,v1} = {q0,q1} + {b,b}
+__device__ __forceinline__ void add2b(float &v0, float &v1, float q0, float q1, float b) {
+  asm("{.reg .b64 x,y,z;\n\tmov.b64 x,{%2,%3};\n\tmov.b64 y,{%4,%4};\n\tadd.rn.f32x2 z,x,y;\n\tmov.b64 {%0,%1},z;}"
+      : "=f"(v0), "=f"(v1)
+      : "f"(q0), "f"(q1), "f"(b));
+}
+// 3-input min (SASS: FMNMX3)
+__device__ __forceinline__ float min3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+struct Smem {
+  float *tau;      // [g1*K] tau of prefix + sort-group LLMs (current target)
+  int *u;          // [g0*K] units of prefix LLMs
+  float2 *a;       // [Ka] {tau_a, bits(-u_a)}
+  int *lut;        // [R+2] byte offset (from smem base) of the masked row for r = -1..R
+  int *rowidx;     // [R+2] masked-row index for r = -1..R
+  unsigned *cnt;   // [nQ][Rc+2] feasible (a,b) pairs per a-range and remaining budget
+  int *dv;         // [D] distinct b unit values (ascending)  (temp)
+  int *dcnt;       // [D+1] #sorted columns with u <= dv[i-1] (temp)
+  unsigned *rowfin;// [rows] finite columns per masked row (temp)
+  float *btab;     // [rows][row_stride] masked rows
+};
+
+__device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
+  Smem s;
+  s.tau = reinterpret_cast<float *>(base + P.off_tau);
+  s.u = reinterpret_cast<int *>(base + P.off_u);
+  s.a = reinterpret_cast<float2 *>(base + P.off_a);
+  s.lut = reinterpret_cast<int *>(base + P.off_lut);
+  s.rowidx = s.lut + (P.budget + 2);
+  s.cnt = reinterpret_cast<unsigned *>(base + P.off_cnt);
+  s.dv = reinterpret_cast<int *>(base + P.off_tmp);
+  s.dcnt = s.dv + (P.Kb + 1);
+  s.rowfin = reinterpret_cast<unsigned *>(s.dcnt + (P.Kb + 2));
+  s.btab = reinterpret_cast<float *>(base + P.off_btab);
+  return s;
+}
+
+// Build the per-(target, b-chunk) tables in shared memory.  All threads participate.
+__device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
+  const int D = P.D;
+  const int *g_dv = P.dv, *g_dcnt = P.dcnt;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int K = P.K, R = P.budget;
+  const float *tau_t = P.tau + (size_t)t * P.M * K;
+  const int c0 = c * P.bchunk_w;
+  const int c1 = min(c0 + P.bchunk_w, P.Kb);
+  for (int i = tid; i < P.g1 * K; i += nt) s.tau[i] = tau_t[i];
+  for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
+  for (int a = tid; a < P.Ka; a += nt) {
+    float2 v = make_float2(0.f, __int_as_float(0));
+    if (P.a_llm >= 0) v = make_float2(tau_t[P.a_llm * K + a], __int_as_float(-P.u[P.a_llm * K + a]));
+    s.a[a] = v;
+  }
+  for (int i = tid; i < D; i += nt) s.dv[i] = g_dv[i];
+  for (int i = tid; i <= D; i += nt) s.dcnt[i] = g_dcnt[i];
+  __syncthreads();
+  // masked row of r: index = #{distinct b unit values <= r}; row i holds the u-sorted columns
+  // [c0, c1) that satisfy u <= dv[i-1] (row 0: none).
+  const int rows = D + 1;
+  for (int r = tid - 1; r <= R; r += nt) {
+    int lo = 0, hi = D;  // upper_bound(dv, r)
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (s.dv[mid] <= r) lo = mid + 1; else hi = mid;
+    }
+    s.rowidx[r + 1] = lo;
+    s.lut[r + 1] = P.off_btab + lo * P.row_stride * 4;
+  }
+  const float *tau_b = tau_t + P.b_llm * K;
+  for (int i = tid; i < rows * P.bchunk_wpad; i += nt) {
+    const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
+    const int len = min(max(s.dcnt[row], c0), c1) - c0;
+    s.btab[row * P.row_stride + j] = (j < len) ? tau_b[P.bperm[c0 + j]] : finf();
+  }
+  __syncthreads();
+  // finite entries per masked row (for the feasible count)
+  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+  for (int row = warp; row < rows; row += nwarp) {
+    unsigned n = 0;
+    for (int j = lane; j < P.bchunk_wpad; j += 32) n += (s.btab[row * P.row_stride + j] < finf()) ? 1u : 0u;
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0) s.rowfin[row] = n;
+  }
+  __syncthreads();
+  // cnt[q][r'+1] = sum over finite a in range q of rowfin[row(r' - u_a)], r' in [-1, Rc]
+  const int W = P.Rc + 2;
+  for (int i = tid; i < (int)P.nQ * W; i += nt) {
+    const int q = i / W, rr = i % W - 1;
+    const int a0 = q * P.A, a1 = min(a0 + (int)P.A, P.Ka);
+    unsigned n = 0;
+    for (int a = a0; a < a1; ++a) {
+      const float2 av = s.a[a];
+      if (!(av.x < finf())) continue;
+      const int ra = rr + __float_as_int(av.y);
+      if (ra < 0) continue;
+      n += s.rowfin[s.rowidx[min(ra, R) + 1]];
+    }
+    s.cnt[i] = n;
+  }
+  __syncthreads();
+}
+
+template <int NB4, bool TAIL2>
+__device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&Qa)[kRowsPerLane],
+                                         float (&acc)[kRowsPerLane], int ng4) {
+  constexpr int T = kRowsPerLane;
+  if constexpr (NB4 > 0) {
+#pragma unroll
+    for (int g = 0; g < NB4; ++g) {
+      const float4 bv = *reinterpret_cast<const float4 *>(rp + 16 * g);
+#pragma unroll
+      for (int i = 0; i < T; ++i) {
+        float v0, v1, v2, v3;
+        add2(v0, v1, Qa[i], bv.x, bv.y);
+        add2(v2, v3, Qa[i], bv.z, bv.w);
+        acc[i] = min3(acc[i], v0, v1);
+        acc[i] = min3(acc[i], v2, v3);
+      }
+    }
+  } else {
+#pragma unroll 2
+    for (int g = 0; g < ng4; ++g) {
+      const float4 bv = *reinterpret_cast<const float4 *>(rp + 16 * g);
+#pragma unroll
+      for (int i = 0; i < T; ++i) {
+        float v0, v1, v2, v3;
+        add2(v0, v1, Qa[i], bv.x, bv.y);
+        add2(v2, v3, Qa[i], bv.z, bv.w);
+        acc[i] = min3(acc[i], v0, v1);
+        acc[i] = min3(acc[i], v2, v3);
+      }
+    }
+  }
+  if constexpr (TAIL2) {
+    const int tail = (NB4 > 0 ? NB4 : ng4) * 16;
+    const float2 bv = *reinterpret_cast<const float2 *>(rp + tail);
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      float v0, v1;
+      add2(v0, v1, Qa[i], bv.x, bv.y);
+      acc[i] = min3(acc[i], v0, v1);
+    }
+  }
+}
+
+template <int NB4, bool TAIL2>
+__device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
+                              uint32_t &best_seg, unsigned long long &cnt) {
+  const uint32_t *pw = P.pw;
+  constexpr int T = kRowsPerLane;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nW = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint64_t n = P.item_hi - P.item_lo;
+  uint64_t it = P.item_lo + n * w / nW;
+  const uint64_t end = P.item_lo + n * (w + 1) / nW;
+  if (it >= end) return;
+  const int K = P.K;
+  const int ng4 = P.bchunk_wpad >> 2;
+  const uint32_t dmask = (1u << P.dig_bits) - 1u;
+  uint32_t q = (uint32_t)(it % P.nQ);
+  uint64_t tq = it / P.nQ;
+  uint32_t grp = (uint32_t)(tq % P.n_groups);
+  uint32_t chunk = (uint32_t)(tq / P.n_groups);
+  float Pfx = 0.f;
+  int Upfx = 0;
+  auto prefix = [&](uint32_t ch) {
+    // canonical partial sum over LLMs 0..g0-1 (LLM 0 most significant): ((0 + tau_0) + tau_1) + ...
+    float acc = 0.f;
+    int U = 0;
+    for (int m = 0; m < P.g0; ++m) {
+      const uint32_t d = (ch / pw[m]) % (uint32_t)K;
+      acc = __fadd_rn(acc, s.tau[m * K + d]);
+      U += s.u[m * K + d];
+    }
+    Pfx = acc;
+    Upfx = U;
+  };
+  prefix(chunk);
+  const int Rc = P.Rc;
+  for (; it < end; ++it) {
+    const uint32_t tile = grp * kWarpTiles + lane;
+    const int stile = __ldg(P.tile_s + tile);
+    uint32_t e[T];
+    {
+      const uint4 *ep = reinterpret_cast<const uint4 *>(P.tile_e) + (size_t)tile * (T / 4);
+#pragma unroll
+      for (int v = 0; v < T / 4; ++v) {
+        const uint4 x = __ldg(ep + v);
+        e[4 * v] = x.x; e[4 * v + 1] = x.y; e[4 * v + 2] = x.z; e[4 * v + 3] = x.w;
+      }
+    }
+    float Qr[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const uint32_t ei = (e[i] == kDummy) ? 0u : e[i];
+      float qv = Pfx;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < P.ng) {
+          const uint32_t d = (ei >> (j * P.dig_bits)) & dmask;
+          qv = __fadd_rn(qv, s.tau[(P.g0 + j) * K + d]);
+        }
+      }
+      Qr[i] = (e[i] == kDummy) ? finf() : qv;
+    }
+    const int r_tile = P.budget - Upfx - stile;
+    float acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = finf();
+    const int a0 = (int)(q * P.A);
+    const int a1 = min(a0 + (int)P.A, P.Ka);
+    for (int a = a0; a < a1; ++a) {
+      const float2 av = s.a[a];
+      const int ra = max(r_tile + __float_as_int(av.y), -1);
+      const int rowoff = s.lut[ra + 1];
+      float Qa[T];
+#pragma unroll
+      for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+      eval_row<NB4, TAIL2>(base + rowoff, Qa, acc, ng4);
+    }
+    // fold rows into the thread's best (lowest segment on equal value)
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      if (acc[i] <= best && acc[i] < finf()) {
+        uint32_t ec = 0;
+        for (int j = P.ng - 1; j >= 0; --j) ec = ec * (uint32_t)K + ((e[i] >> (j * P.dig_bits)) & dmask);
+        const uint32_t seg = ((chunk * P.L + ec) * P.nQ) + q;
+        if (acc[i] < best || seg < best_seg) {
+          best = acc[i];
+          best_seg = seg;
+        }
+      }
+    }
+    // feasible count: rows with a finite partial sum x feasible (a,b) pairs at this budget
+    {
+      const int rc = min(max(r_tile, -1), Rc);
+      const unsigned cab = s.cnt[q * (Rc + 2) + rc + 1];
+      unsigned c32 = 0;
+#pragma unroll
+      for (int i = 0; i < T; ++i) c32 += (Qr[i] < finf()) ? cab : 0u;
+      cnt += c32;
+    }
+    if (++q == P.nQ) {
+      q = 0;
+      if (++grp == P.n_groups) {
+        grp = 0;
+        ++chunk;
+        if (chunk < P.n_chunks) prefix(chunk);
+      }
+    }
+  }
+}
+
+template <int NB4, bool TAIL2>
+__global__ void __launch_bounds__(kThreads, 3)
+    k_search(const __grid_constant__ SearchArgs P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
+  const Smem s = smem_layout(P, smem);
+  for (int t = 0; t < P.n_targets; ++t) {
+    float best = finf();
+    uint32_t best_seg = 0xffffffffu;
+    unsigned long long cnt = 0ull;
+    for (int c = 0; c < P.n_bchunks; ++c) {
+      __syncthreads();
+      build_tables(P, s, t, c);
+      process_items<NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
+    }
+    unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+      const unsigned long long oc = __shfl_xor_sync(0xffffffffu, cnt, o);
+      key = ok < key ? ok : key;
+      cnt += oc;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+      red_key[warp] = key;
+      red_cnt[warp] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long k = red_key[0], n = red_cnt[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        k = red_key[w] < k ? red_key[w] : k;
+        n += red_cnt[w];
+      }
+      if (k != kKeyNone) atomicMin(P.keys + t, k);
+      if (n) atomicAdd(P.counts + t, n);
+    }
+  }
+}
+
+// Host-side dispatch over the b-chunk width specialisations.
+template <int NB4, bool TAIL2>
+static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
+  auto fn = k_search<NB4, TAIL2>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NB4, bool TAIL2>
+static int occ_one(const SearchArgs &a) {
+  auto fn = k_search<NB4, TAIL2>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, a.smem_bytes) != cudaSuccess) return 0;
+  return n;
+}
+
+// Specialised (fully unrolled) b loop for chunk widths <= 34 columns: NB4 LDS.128 groups plus an
+// optional LDS.64 tail; wider chunks use the runtime loop (NB4 = 0).
+#define ALP_DISPATCH(CALL)                                                   \
+  do {                                                                       \
+    const int w = a.bchunk_wpad;                                             \
+    const bool t2 = (w % 4) == 2;                                            \
+    if (w > 34) {                                                            \
+      if (t2) return CALL(0, true);                                          \
+      return CALL(0, false);                                                 \
+    }                                                                        \
+    switch (w) {                                                             \
+      case 2: return CALL(0, true);                                          \
+      case 4: return CALL(1, false); case 6: return CALL(1, true);           \
+      case 8: return CALL(2, false); case 10: return CALL(2, true);          \
+      case 12: return CALL(3, false); case 14: return CALL(3, true);         \
+      case 16: return CALL(4, false); case 18: return CALL(4, true);         \
+      case 20: return CALL(5, false); case 22: return CALL(5, true);         \
+      case 24: return CALL(6, false); case 26: return CALL(6, true);         \
+      case 28: return CALL(7, false); case 30: return CALL(7, true);         \
+      case 32: return CALL(8, false); case 34: return CALL(8, true);         \
+      default: if (t2) return CALL(0, true); return CALL(0, false);          \
+    }                                                                        \
+  } while (0)
+
+cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st) {
+#define CALL(N, T2) launch_one<N, T2>(a, grid, st)
+  ALP_DISPATCH(CALL);
+#undef CALL
+}
+
+int search_max_blocks_per_sm(const SearchArgs &a) {
+#define CALL(N, T2) occ_one<N, T2>(a)
+  ALP_DISPATCH(CALL);
+#undef CALL
+}
+
+// ------------------------------------------------------------------ finalize (K3)
+__global__ void k_finalize(const FinalizeArgs F) {
+  const SearchArgs &P = F.s;
+  const int t = blockIdx.x;
+  const unsigned long long key = F.keys[t];
+  const unsigned long long count = F.counts[t];
+  __shared__ unsigned long long s_best;
+  __shared__ int s_found;
+  const int K = P.K;
+  const float *tau_t = P.tau + (size_t)t * P.M * K;
+  const uint32_t seg = (uint32_t)(key & 0xffffffffull);
+  const float val = __uint_as_float((uint32_t)(key >> 32));
+  const bool found = key != kKeyNone && val < finf();
+  uint32_t q = 0, chunk = 0, e = 0;
+  float Qrow = 0.f;
+  int Urow = 0;
+  if (found) {
+    q = seg % P.nQ;
+    const uint32_t row = seg / P.nQ;
+    chunk = row / P.L;
+    e = row % P.L;
+    // canonical partial sum over LLMs 0..g1-1 (digits of chunk then e, most significant first)
+    int kd[ALP_MAX_M];
+    uint32_t rem = chunk;
+    for (int m = P.g0 - 1; m >= 0; --m) { kd[m] = (int)(rem % (uint32_t)K); rem /= (uint32_t)K; }
+    rem = e;
+    for (int j = P.ng - 1; j >= 0; --j) { kd[P.g0 + j] = (int)(rem % (uint32_t)K); rem /= (uint32_t)K; }
+    for (int m = 0; m < P.g1; ++m) {
+      Qrow = __fadd_rn(Qrow, tau_t[m * K + kd[m]]);
+      Urow += P.u[m * K + kd[m]];
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_best = ~0ull;
+    s_found = found;
+  }
+  __syncthreads();
+  if (found) {
+    const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
+    const unsigned long long n = (unsigned long long)(a1 - a0) * P.Kb;
+    unsigned long long mine = ~0ull;
+    for (unsigned long long li = threadIdx.x; li < n; li += blockDim.x) {
+      const int a = a0 + (int)(li / P.Kb), b = (int)(li % P.Kb);
+      float ta = 0.f;
+      int ua = 0;
+      if (P.a_llm >= 0) {
+        ta = tau_t[P.a_llm * K + a];
+        ua = P.u[P.a_llm * K + a];
+      }
+      const float v = __fadd_rn(__fadd_rn(Qrow, ta), tau_t[P.b_llm * K + b]);
+      const int units = Urow + ua + P.u[P.b_llm * K + b];
+      if (v == val && units <= P.budget) {
+        mine = li;
+        break;
+      }
+    }
+    atomicMin(&s_best, mine);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  alp_result r;
+  memset(&r, 0, sizeof(r));
+  r.M = P.M;
+  r.feasible_count = count;
+  r.candidates = F.N;
+  r.index = ~0ull;
+  r.latency_key = finf();
+  if (found && s_best != ~0ull) {
+    const int a0 = (int)(q * P.A);
+    const int a = a0 + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
+    int k[ALP_MAX_M];
+    uint32_t rem = chunk;
+    for (int m = P.g0 - 1; m >= 0; --m) {
+      k[m] = (int)(rem % (uint32_t)K);
+      rem /= (uint32_t)K;
+    }
+    rem = e;
+    for (int j = P.ng - 1; j >= 0; --j) {
+      k[P.g0 + j] = (int)(rem % (uint32_t)K);
+      rem /= (uint32_t)K;
+    }
+    if (P.a_llm >= 0) k[P.a_llm] = a;
+    k[P.b_llm] = b;
+    unsigned long long idx = 0;
+    double L = 0.0, Tw = CUDART_INF;
+    long long U = 0;
+    const double *term_t = F.term + (size_t)t * P.M * K;
+    const double *b_t = F.b + (size_t)t * P.M * K;
+    for (int m = 0; m < P.M; ++m) {
+      idx = idx * (unsigned long long)K + (unsigned long long)k[m];
+      const double tm = term_t[m * K + k[m]];
+      L = (m == 0) ? tm : __dadd_rn(L, tm);  // Eq. 1 in canonical order (FP64)
+      const double bm = b_t[m * K + k[m]];
+      Tw = bm < Tw ? bm : Tw;                // Eq. 2
+      U += P.u[m * K + k[m]];
+      if (F.S) {
+        const int s_i = k[m] / (F.nR * F.nT), t_i = (k[m] / F.nR) % F.nT, r_i = k[m] % F.nR;
+        r.share_units[m] = F.S[s_i];
+        r.tp[m] = F.T[t_i];
+        r.replicas[m] = F.R[r_i];
+      }
+    }
+    r.found = 1;
+    r.index = idx;
+    r.latency_key = val;
+    r.latency = L;
+    r.throughput = Tw;
+    r.units = U;
+  } else {
+    r.latency = CUDART_INF;
+    r.throughput = 0.0;
+  }
+  F.out[t] = r;
+}
+
+// ------------------------------------------------------------------ predict
+__global__ void k_predict(const PredictArgs A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  double L = 0.0, Tw = CUDART_INF;
+  long long U = 0;
+  int all_ok = 1;
+  for (int m = 0; m < A.prof.M; ++m) {
+    float tau;
+    double term, b;
+    int u;
+    all_ok &= option_terms(A.prof, A.lambda, m, A.opts[i * A.prof.M + m], &tau, &term, &b, &u);
+    L = (m == 0) ? term : __dadd_rn(L, term);
+    Tw = b < Tw ? b : Tw;
+    U += u;
+  }
+  const int feas = all_ok && U <= A.budget;
+  A.latency[i] = all_ok ? L : CUDART_INF;
+  A.throughput[i] = Tw;
+  A.units[i] = U;
+  A.feasible[i] = feas;
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st) {
+  const int total = a.n_targets * a.prof.M * a.prof.K;
+  const int n = total > a.n_targets ? total : a.n_targets;
+  k_option_table<<<(n + 255) / 256, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, cudaStream_t st) {
+  k_init_keys<<<(n + 255) / 256, 256, 0, st>>>(keys, counts, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st) {
+  k_finalize<<<a.s.n_targets, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st) {
+  k_predict<<<(a.n + 127) / 128, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace alp

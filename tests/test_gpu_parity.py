@@ -1,0 +1,291 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.  Needs a B200 (-m gpu).
+
+Bar (BASELINE.json north star): chosen index and feasible count bit-exact; latency_key (the
+canonical binary32 objective) bit-exact; FP64 latency / throughput within 1e-6 relative (they are
+expected to be bit-identical: same IEEE operations in the same order).
+"""
+from __future__ import annotations
+
+import itertools
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import dp
+from workloads import generate
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2604_15186_b200 as P
+    return P
+
+
+def _same(g, o_found, o_key, o_idx, o_cnt, tag=""):
+    assert g.found == o_found, tag
+    assert g.feasible_count == o_cnt, tag
+    if o_found:
+        assert g.index == o_idx, tag
+        assert np.float32(g.latency_key).view(np.uint32) == np.float32(o_key).view(np.uint32), tag
+
+
+def _check_winner(P, alp, I, lam, B, g):
+    """FP64 Eq. 1 / Eq. 2 of the winner vs the oracle's prediction (rel 1e-6; expected exact)."""
+    if not g.found:
+        return
+    ks = oracle.decode(I, g.index)
+    p = oracle.predict(I, lam, ks, B)
+    assert p["feasible"] and p["units"] == g.units
+    assert g.latency == pytest.approx(p["latency"], rel=1e-6)
+    assert g.throughput == pytest.approx(p["throughput"], rel=1e-6)
+    assert p["latency_key"] == g.latency_key
+    grid = [oracle.option_grid(I, k) for k in ks]
+    assert [x[0] for x in grid] == g.share_units and [x[1] for x in grid] == g.tp and [x[2] for x in grid] == g.replicas
+
+
+# ----------------------------------------------------------------------------- option table
+@pytest.mark.parametrize("name", ["hand", "C1", "C2", "C3", "C4"])
+def test_option_table_bitexact(P, name):
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in d["targets"] + [d["targets"][0] * 3.7, d["targets"][0] * 0.01]:
+        g = alp.option_table(lam, I.K)
+        o = oracle.option_table(I, lam)
+        assert np.array_equal(g["tau"].view(np.uint32), o["tau"].view(np.uint32))
+        assert np.array_equal(g["b"].view(np.uint64), o["b"].view(np.uint64))
+        assert np.array_equal(g["u"], o["u"])
+        fin = o["ok"]
+        assert np.array_equal(g["term"][fin].view(np.uint64), o["term"][fin].view(np.uint64))
+
+
+def test_option_table_edge_cases(P):
+    # x exactly at r_0, at an interior r_i and at T; x below r_0; b exactly lambda; f = 1/F; d = 3.
+    d = {"M": 2, "F": 4, "share_units": [1, 2, 4], "tp": [1, 2], "replicas": [1, 2, 3], "n": [2.0, 3.0],
+         "p": [1.0, 1.5], "min_units": None, "budget_units": 40, "percentile": "mean",
+         "profiles": [[{"rate": [0.5, 1.0, 2.0, 4.0], "lat": {k: [0.1, 0.2, 0.5, 1.1] for k in oracle.PCT_KEYS},
+                        "tmax": 4.0},
+                       {"rate": [0.25, 3.0], "lat": {k: [0.05, 0.3] for k in oracle.PCT_KEYS}, "tmax": 5.0}]] * 2}
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in [0.0625, 0.125, 0.25, 0.5, 1.0 / 3.0, 0.7, 1.5, 2.0]:
+        g = alp.option_table(lam, I.K)
+        o = oracle.option_table(I, lam)
+        assert np.array_equal(g["tau"].view(np.uint32), o["tau"].view(np.uint32)), lam
+        assert np.array_equal(g["b"].view(np.uint64), o["b"].view(np.uint64)), lam
+
+
+# ----------------------------------------------------------------------------- hand case
+def test_hand_case_all_rows(P):
+    with open("tests/golden/hand_case.json") as f:
+        g = json.load(f)["searches"]
+    from fractions import Fraction
+    d = generate.load("hand")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam_s, B, found, idx, _kg, _kv, Lw, Tw, units, feas in g["rows"]:
+        lam = float(Fraction(lam_s))
+        r = alp.search(lam, B)
+        assert r.found == found and r.feasible_count == feas
+        if found:
+            assert r.index == idx and r.units == units
+            assert r.latency == pytest.approx(float(Fraction(Lw)), rel=1e-12)
+            assert r.throughput == float(Fraction(Tw))
+            _check_winner(P, alp, I, lam, B, r)
+
+
+# ----------------------------------------------------------------------------- configs
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_full_bruteforce_small(P, name):
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (d["targets"][0], d["targets"][0] * 2, d["lambda_star"]):
+        for B in (I.budget, I.budget // 2, I.budget * 4):
+            r = alp.search(lam, B)
+            o = oracle.search(I, lam, B)
+            _same(r, o.found, o.latency_key, o.index, o.count, (name, lam, B))
+            _check_winner(P, alp, I, lam, B, r)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_vs_dp(P, name):
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = d["targets"][0]
+    for B in (I.budget, I.budget // 2 + 3):
+        r = alp.search(lam, B)
+        tab = oracle.option_table(I, lam)
+        f, v, idx, cnt = dp.search(tab["tau"], tab["u"], B)
+        _same(r, f, v, idx, cnt, (name, B))
+        assert r.candidates == I.N
+        _check_winner(P, alp, I, lam, B, r)
+        # the winner, recomputed one by one from the profiles
+        ok, l32, _ = oracle.candidate(I, lam, r.index, B)
+        assert ok and l32 == r.latency_key
+
+
+def test_c4_window_bruteforce(P):
+    # exhaustive O1 around the optimum: no candidate in a 2e7-wide canonical window beats it
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = d["targets"][0]
+    r = alp.search(lam, I.budget)
+    lo = max(0, r.index - 10_000_000)
+    o = oracle.search(I, lam, I.budget, lo=lo, hi=min(I.N, r.index + 10_000_000), threads=8)
+    assert o.found and o.index == r.index and o.latency_key == r.latency_key
+
+
+def test_c5_target_batch(P):
+    d = generate.load("C5")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    targets = d["targets"]
+    res = alp.search_batch(targets, I.budget)
+    assert len(res) == 256
+    prev_cnt = None
+    for j in list(range(0, 256, 17)) + [255]:
+        tab = oracle.option_table(I, targets[j])
+        f, v, idx, cnt = dp.search(tab["tau"], tab["u"], I.budget)
+        _same(res[j], f, v, idx, cnt, j)
+    for j in range(256):  # Pareto invariants over the sweep (exact count monotonicity)
+        if prev_cnt is not None:
+            assert res[j].feasible_count <= prev_cnt
+        prev_cnt = res[j].feasible_count
+    assert res[255].found and res[255].feasible_count >= 1
+
+
+# ----------------------------------------------------------------------------- fuzzing
+@pytest.mark.parametrize("seed", range(24))
+def test_random_instances_vs_bruteforce(P, seed):
+    rng = np.random.default_rng(7000 + seed)
+    M = int(rng.integers(1, 6))
+    S = sorted(set(int(x) for x in rng.integers(1, 5, size=int(rng.integers(1, 4)))))
+    T = [1, 2, 4, 8][: int(rng.integers(1, 5))]
+    R = list(range(1, int(rng.integers(2, 6))))
+    K = len(S) * len(T) * len(R)
+    while K ** M > 3_000_000:
+        M -= 1
+    budget = int(rng.integers(0, 40))
+    d = generate.random_instance(seed, M=M, F=4, S=S, T=T, R=R, budget=budget, min_units=bool(seed % 4 == 1))
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (0.02, 0.2, 1.1):
+        r = alp.search(lam, budget)
+        o = oracle.search(I, lam, budget, threads=4)
+        _same(r, o.found, o.latency_key, o.index, o.count, (seed, lam))
+        _check_winner(P, alp, I, lam, budget, r)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_injected_terms_ties_and_exact_sums(P, seed):
+    # dyadic terms (multiples of 2^-10, sums < 2^14): every binary32 sum is exact; heavy ties.
+    rng = np.random.default_rng(seed)
+    M = int(rng.integers(2, 5))
+    K = int(rng.integers(2, 12))
+    tau = (rng.integers(1, 9, size=(M, K)) * 128 / 1024.0).astype(np.float32)
+    tau[rng.random((M, K)) < 0.15] = np.inf
+    u = rng.integers(0, 6, size=(M, K)).astype(np.int32)
+    B = int(rng.integers(0, 6 * M))
+    alp = P.Alp.from_terms(tau, u)
+    r = alp.search(1.0, B)
+    best, bidx, cnt = None, None, 0
+    for i, ks in enumerate(itertools.product(range(K), repeat=M)):
+        if sum(u[m, k] for m, k in enumerate(ks)) > B or not all(np.isfinite(tau[m, k]) for m, k in enumerate(ks)):
+            continue
+        cnt += 1
+        v = sum(int(tau[m, k] * 1024) for m, k in enumerate(ks))
+        if best is None or v < best:
+            best, bidx = v, i
+    assert r.feasible_count == cnt
+    assert r.found == (cnt > 0)
+    if cnt:
+        assert r.index == bidx and r.latency_key == best / 1024.0
+
+
+def test_subulp_terms_match_dp(P):
+    rng = np.random.default_rng(3)
+    M, K = 4, 20
+    tau = (np.float32(1.0) + rng.integers(0, 4, size=(M, K)).astype(np.float32) * np.float32(2.0 ** -23))
+    tau = tau.astype(np.float32)
+    u = rng.integers(1, 5, size=(M, K)).astype(np.int32)
+    for B in (4, 7, 11, 16, 80):
+        alp = P.Alp.from_terms(tau, u)
+        r = alp.search(1.0, B)
+        f, v, idx, cnt = dp.search(tau, u, B)
+        _same(r, f, v, idx, cnt, B)
+
+
+# ----------------------------------------------------------------------------- sharding / edges
+def test_partition_independence(P):
+    import torch
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = [d["targets"][0]]
+    ref = alp.search(lam[0], I.budget)
+    for world in (2, 3, 8):
+        keys = torch.empty((world, 1), dtype=torch.int64, device="cuda")
+        counts = torch.empty((world, 1), dtype=torch.int64, device="cuda")
+        for rank in range(world):
+            lo, hi = alp.shard_range(I.budget, rank, world)
+            alp.search_shard(lam, I.budget, lo, hi, keys[rank].data_ptr(), counts[rank].data_ptr())
+            torch.cuda.synchronize()
+        k = keys.min(dim=0).values.contiguous()
+        c = counts.sum(dim=0).contiguous()
+        r = alp.finalize(lam, I.budget, k.data_ptr(), c.data_ptr())[0]
+        assert (r.index, r.feasible_count, r.latency_key) == (ref.index, ref.feasible_count, ref.latency_key)
+
+
+def test_infeasible_and_zero_budget(P):
+    d = generate.load("C1")
+    alp = P.Alp.from_instance(d)
+    r = alp.search(1e6, 16)
+    assert not r.found and r.feasible_count == 0 and r.index == -1
+    r = alp.search(d["targets"][0], 0)
+    assert not r.found and r.feasible_count == 0
+
+
+def test_validation_errors(P):
+    d = generate.load("C1")
+    bad = json.loads(json.dumps(d))
+    bad["n"][1] = -1.0
+    with pytest.raises(P.AlpError, match="n\\[1\\]"):
+        P.Alp.from_instance(bad)
+    bad = json.loads(json.dumps(d))
+    bad["profiles"][0][1]["rate"][3] = bad["profiles"][0][1]["rate"][2]
+    with pytest.raises(P.AlpError, match="strictly increasing"):
+        P.Alp.from_instance(bad)
+    alp = P.Alp.from_instance(d)
+    with pytest.raises(P.AlpError, match="targets"):
+        alp.search(-1.0, 16)
+
+
+def test_predict_matches_oracle(P):
+    d = generate.load("C3")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    rng = np.random.default_rng(0)
+    opts = rng.integers(0, I.K, size=(500, I.M))
+    lam = d["targets"][0]
+    g = alp.predict(opts, lam, I.budget)
+    for i in range(len(opts)):
+        o = oracle.predict(I, lam, list(opts[i]), I.budget)
+        assert g["feasible"][i] == o["feasible"] and g["units"][i] == o["units"]
+        assert g["throughput"][i] == o["throughput"]
+        if np.isfinite(o["latency"]):
+            assert g["latency"][i] == o["latency"]
+
+
+def test_decode_roundtrip(P):
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for idx in [0, 1, I.N - 1, 123456789, 9725594165]:
+        assert alp.decode(idx) == [oracle.option_grid(I, k) for k in oracle.decode(I, idx)]
