@@ -247,8 +247,9 @@ alp_status make_plan(alp_s *h) {
     for (int k = 0; k < K; ++k) mx = std::max(mx, U(m, k));
     h->umax_total += mx;
   }
-  // a-ranges: enough equal-cost work items to balance ~8 items per resident warp.
-  const uint64_t want = (uint64_t)h->sm_count * 24 * 8;
+  // a-ranges: enough equal-cost work items for ~48 items per resident warp (load balance); a warp
+  // keeps its lane tile across consecutive a-ranges, so small ranges cost little.
+  const uint64_t want = (uint64_t)h->sm_count * 24 * 48;
   uint32_t nQ = 1;
   while ((uint64_t)h->n_chunks * h->n_groups * nQ < want && nQ < (uint32_t)h->Ka) ++nQ;
   h->A = (uint32_t)((h->Ka + nQ - 1) / nQ);
@@ -314,7 +315,6 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.Ka = h->Ka; a.Kb = h->Kb; a.ng = h->ng; a.dig_bits = h->dig_bits; a.L = h->L; a.n_chunks = h->n_chunks;
   a.n_groups = h->n_groups; a.nQ = h->nQ; a.A = h->A; a.item_lo = lo; a.item_hi = hi;
   a.budget = (int)Reff;
-  a.Rc = (int)std::min<long long>(Reff, (long long)h->umax_a + h->umax_b);
   a.n_targets = n_targets;
   a.D = (int)(std::upper_bound(h->dv.begin(), h->dv.end(), (int)Reff) - h->dv.begin());
   for (int m = 0; m < ALP_MAX_M; ++m) a.pw[m] = h->pw[m];
@@ -325,15 +325,14 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
     a.bchunk_w = W;
     a.n_bchunks = (h->Kb + W - 1) / W;
     a.bchunk_wpad = W <= 34 ? (W + 1) / 2 * 2 : (W + 3) / 4 * 4;
-    a.row_stride = a.bchunk_wpad;
+    a.row_stride = a.bchunk_wpad + 1;  // >= 1 padding column (holds the row's finite count)
     while (a.row_stride % 8 != 4) ++a.row_stride;
     int off = 0;
     a.off_tau = off; off = align16(off + h->g1 * h->K * 4);
     a.off_u = off; off = align16(off + h->g0 * h->K * 4);
     a.off_a = off; off = align16(off + h->Ka * 8);
-    a.off_lut = off; off = align16(off + 2 * (a.budget + 2) * 4);
-    a.off_cnt = off; off = align16(off + (int)h->nQ * (a.Rc + 2) * 4);
-    a.off_tmp = off; off = align16(off + (2 * h->Kb + 3 + rows) * 4);
+    a.off_lut = off; off = align16(off + (a.budget + 2) * 8);
+    a.off_tmp = off; off = align16(off + (2 * h->Kb + 3) * 4);
     a.off_btab = off; off = align16(off + rows * a.row_stride * 4);
     a.smem_bytes = off;
     return off;

@@ -50,7 +50,6 @@ struct SearchArgs {
   uint32_t nQ, A;        // a-ranges: a in [q*A, min((q+1)*A, Ka))
   uint64_t item_lo, item_hi;
   int budget;            // R (capped at the total max units; <= kMaxBudget)
-  int Rc;                // count-table upper clamp min(R, Umax_a + Umax_b)
   int n_targets;
   int n_bchunks, bchunk_w, bchunk_wpad;  // b columns (u-sorted) split in chunks
   int row_stride;        // floats per masked row (== 4 mod 8)
@@ -68,7 +67,7 @@ struct SearchArgs {
   unsigned long long *keys;
   unsigned long long *counts;
   // shared memory layout (byte offsets)
-  int off_tau, off_u, off_a, off_lut, off_cnt, off_btab, off_tmp, smem_bytes;
+  int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
 };
 
 struct FinalizeArgs {

@@ -128,39 +128,33 @@ __device__ __forceinline__ float min3(float a, float b, float c) {
 }
 
 struct Smem {
-  float *tau;      // [g1*K] tau of prefix + sort-group LLMs (current target)
+  float *tau;      // [g1*K] tau of prefix + sort-group LLMs (current target); at smem offset 0
   int *u;          // [g0*K] units of prefix LLMs
-  float2 *a;       // [Ka] {tau_a, bits(-u_a)}
-  int *lut;        // [R+2] byte offset (from smem base) of the masked row for r = -1..R
-  int *rowidx;     // [R+2] masked-row index for r = -1..R
-  unsigned *cnt;   // [nQ][Rc+2] feasible (a,b) pairs per a-range and remaining budget
-  int *dv;         // [D] distinct b unit values (ascending)  (temp)
-  int *dcnt;       // [D+1] #sorted columns with u <= dv[i-1] (temp)
-  unsigned *rowfin;// [rows] finite columns per masked row (temp)
+  float2 *a;       // [Ka] {tau_a, bits(-u_a)}; u_a := kBigUnits when tau_a is +inf
+  int2 *lut;       // [R+2] {byte offset of the masked row, #finite entries in it} for r = -1..R
+  int *dv;         // [D] distinct b unit values <= R, ascending
+  int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
   float *btab;     // [rows][row_stride] masked rows
 };
+
+constexpr int kBigUnits = 1 << 28;
 
 __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
   Smem s;
   s.tau = reinterpret_cast<float *>(base + P.off_tau);
   s.u = reinterpret_cast<int *>(base + P.off_u);
   s.a = reinterpret_cast<float2 *>(base + P.off_a);
-  s.lut = reinterpret_cast<int *>(base + P.off_lut);
-  s.rowidx = s.lut + (P.budget + 2);
-  s.cnt = reinterpret_cast<unsigned *>(base + P.off_cnt);
+  s.lut = reinterpret_cast<int2 *>(base + P.off_lut);
   s.dv = reinterpret_cast<int *>(base + P.off_tmp);
   s.dcnt = s.dv + (P.Kb + 1);
-  s.rowfin = reinterpret_cast<unsigned *>(s.dcnt + (P.Kb + 2));
   s.btab = reinterpret_cast<float *>(base + P.off_btab);
   return s;
 }
 
 // Build the per-(target, b-chunk) tables in shared memory.  All threads participate.
 __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
-  const int D = P.D;
-  const int *g_dv = P.dv, *g_dcnt = P.dcnt;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int K = P.K, R = P.budget;
+  const int K = P.K, R = P.budget, D = P.D;
   const float *tau_t = P.tau + (size_t)t * P.M * K;
   const int c0 = c * P.bchunk_w;
   const int c1 = min(c0 + P.bchunk_w, P.Kb);
@@ -168,24 +162,17 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
   for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
   for (int a = tid; a < P.Ka; a += nt) {
     float2 v = make_float2(0.f, __int_as_float(0));
-    if (P.a_llm >= 0) v = make_float2(tau_t[P.a_llm * K + a], __int_as_float(-P.u[P.a_llm * K + a]));
+    if (P.a_llm >= 0) {
+      const float ta = tau_t[P.a_llm * K + a];
+      v = make_float2(ta, __int_as_float(ta < finf() ? -P.u[P.a_llm * K + a] : -kBigUnits));
+    }
     s.a[a] = v;
   }
-  for (int i = tid; i < D; i += nt) s.dv[i] = g_dv[i];
-  for (int i = tid; i <= D; i += nt) s.dcnt[i] = g_dcnt[i];
+  for (int i = tid; i < D; i += nt) s.dv[i] = P.dv[i];
+  for (int i = tid; i <= D; i += nt) s.dcnt[i] = P.dcnt[i];
   __syncthreads();
-  // masked row of r: index = #{distinct b unit values <= r}; row i holds the u-sorted columns
-  // [c0, c1) that satisfy u <= dv[i-1] (row 0: none).
+  // masked row i holds the u-sorted columns [c0, c1) with u <= dv[i-1] (row 0: none), +inf elsewhere
   const int rows = D + 1;
-  for (int r = tid - 1; r <= R; r += nt) {
-    int lo = 0, hi = D;  // upper_bound(dv, r)
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (s.dv[mid] <= r) lo = mid + 1; else hi = mid;
-    }
-    s.rowidx[r + 1] = lo;
-    s.lut[r + 1] = P.off_btab + lo * P.row_stride * 4;
-  }
   const float *tau_b = tau_t + P.b_llm * K;
   for (int i = tid; i < rows * P.bchunk_wpad; i += nt) {
     const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
@@ -193,29 +180,24 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
     s.btab[row * P.row_stride + j] = (j < len) ? tau_b[P.bperm[c0 + j]] : finf();
   }
   __syncthreads();
-  // finite entries per masked row (for the feasible count)
+  // finite entries per masked row (feasible b count), kept in the row's padding column
   const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
   for (int row = warp; row < rows; row += nwarp) {
     unsigned n = 0;
     for (int j = lane; j < P.bchunk_wpad; j += 32) n += (s.btab[row * P.row_stride + j] < finf()) ? 1u : 0u;
     n = __reduce_add_sync(0xffffffffu, n);
-    if (lane == 0) s.rowfin[row] = n;
+    if (lane == 0) s.btab[row * P.row_stride + P.bchunk_wpad] = __int_as_float((int)n);
   }
   __syncthreads();
-  // cnt[q][r'+1] = sum over finite a in range q of rowfin[row(r' - u_a)], r' in [-1, Rc]
-  const int W = P.Rc + 2;
-  for (int i = tid; i < (int)P.nQ * W; i += nt) {
-    const int q = i / W, rr = i % W - 1;
-    const int a0 = q * P.A, a1 = min(a0 + (int)P.A, P.Ka);
-    unsigned n = 0;
-    for (int a = a0; a < a1; ++a) {
-      const float2 av = s.a[a];
-      if (!(av.x < finf())) continue;
-      const int ra = rr + __float_as_int(av.y);
-      if (ra < 0) continue;
-      n += s.rowfin[s.rowidx[min(ra, R) + 1]];
+  // r -> masked row: index = #{distinct b unit values <= r}
+  for (int r = tid - 1; r <= R; r += nt) {
+    int lo = 0, hi = D;  // upper_bound(dv, r)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s.dv[mid] <= r) lo = mid + 1; else hi = mid;
     }
-    s.cnt[i] = n;
+    s.lut[r + 1] = make_int2(P.off_btab + lo * P.row_stride * 4,
+                             __float_as_int(s.btab[lo * P.row_stride + P.bchunk_wpad]));
   }
   __syncthreads();
 }
@@ -263,10 +245,29 @@ __device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&
   }
 }
 
+// Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
+// row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
+__device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[kRowsPerLane],
+                                          const uint32_t (&e)[kRowsPerLane], uint32_t chunk, uint32_t q0,
+                                          float &best, uint32_t &best_seg) {
+  const uint32_t dmask = (1u << P.dig_bits) - 1u;
+#pragma unroll
+  for (int i = 0; i < kRowsPerLane; ++i) {
+    if (acc[i] <= best && acc[i] < finf()) {  // rare after the first items
+      uint32_t ec = 0;  // canonical within-group index: LLM g0 most significant
+      for (int j = 0; j < P.ng; ++j) ec = ec * (uint32_t)P.K + ((e[i] >> (j * P.dig_bits)) & dmask);
+      const uint32_t seg = (chunk * P.L + ec) * P.nQ + q0;
+      if (acc[i] < best || seg < best_seg) {
+        best = acc[i];
+        best_seg = seg;
+      }
+    }
+  }
+}
+
 template <int NB4, bool TAIL2>
 __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
                               uint32_t &best_seg, unsigned long long &cnt) {
-  const uint32_t *pw = P.pw;
   constexpr int T = kRowsPerLane;
   const int lane = threadIdx.x & 31;
   const uint64_t nW = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -279,97 +280,86 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   const int ng4 = P.bchunk_wpad >> 2;
   const uint32_t dmask = (1u << P.dig_bits) - 1u;
   uint32_t q = (uint32_t)(it % P.nQ);
-  uint64_t tq = it / P.nQ;
+  const uint64_t tq = it / P.nQ;
   uint32_t grp = (uint32_t)(tq % P.n_groups);
   uint32_t chunk = (uint32_t)(tq / P.n_groups);
+  // state of the lane tile currently loaded
+  float Qr[T], acc[T];
+  uint32_t e[T];
+  int r_tile = 0;
+  unsigned nfin = 0;
+  uint32_t q0 = q, tchunk = chunk;
+  bool loaded = false;
   float Pfx = 0.f;
   int Upfx = 0;
-  auto prefix = [&](uint32_t ch) {
-    // canonical partial sum over LLMs 0..g0-1 (LLM 0 most significant): ((0 + tau_0) + tau_1) + ...
-    float acc = 0.f;
-    int U = 0;
-    for (int m = 0; m < P.g0; ++m) {
-      const uint32_t d = (ch / pw[m]) % (uint32_t)K;
-      acc = __fadd_rn(acc, s.tau[m * K + d]);
-      U += s.u[m * K + d];
-    }
-    Pfx = acc;
-    Upfx = U;
-  };
-  prefix(chunk);
-  const int Rc = P.Rc;
+  uint32_t pchunk = 0xffffffffu;
   for (; it < end; ++it) {
-    const uint32_t tile = grp * kWarpTiles + lane;
-    const int stile = __ldg(P.tile_s + tile);
-    uint32_t e[T];
-    {
+    if (!loaded) {
+      if (chunk != pchunk) {
+        // canonical partial sum over LLMs 0..g0-1 (LLM 0 most significant): ((0 + tau_0) + tau_1) + ...
+        float pa = 0.f;
+        int U = 0;
+        for (int m = 0; m < P.g0; ++m) {
+          const uint32_t d = (chunk / P.pw[m]) % (uint32_t)K;
+          pa = __fadd_rn(pa, s.tau[m * K + d]);
+          U += s.u[m * K + d];
+        }
+        Pfx = pa;
+        Upfx = U;
+        pchunk = chunk;
+      }
+      const uint32_t tile = grp * kWarpTiles + lane;
+      const int stile = __ldg(P.tile_s + tile);
       const uint4 *ep = reinterpret_cast<const uint4 *>(P.tile_e) + (size_t)tile * (T / 4);
 #pragma unroll
       for (int v = 0; v < T / 4; ++v) {
         const uint4 x = __ldg(ep + v);
         e[4 * v] = x.x; e[4 * v + 1] = x.y; e[4 * v + 2] = x.z; e[4 * v + 3] = x.w;
       }
-    }
-    float Qr[T];
+      nfin = 0;
 #pragma unroll
-    for (int i = 0; i < T; ++i) {
-      const uint32_t ei = (e[i] == kDummy) ? 0u : e[i];
-      float qv = Pfx;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j < P.ng) {
+      for (int i = 0; i < T; ++i) {
+        const uint32_t ei = (e[i] == kDummy) ? 0u : e[i];
+        float qv = Pfx;
+        for (int j = 0; j < P.ng; ++j) {
           const uint32_t d = (ei >> (j * P.dig_bits)) & dmask;
           qv = __fadd_rn(qv, s.tau[(P.g0 + j) * K + d]);
         }
+        Qr[i] = (e[i] == kDummy) ? finf() : qv;
+        nfin += (Qr[i] < finf()) ? 1u : 0u;
+        acc[i] = finf();
       }
-      Qr[i] = (e[i] == kDummy) ? finf() : qv;
+      r_tile = P.budget - Upfx - stile;
+      q0 = q;
+      tchunk = chunk;
+      loaded = true;
     }
-    const int r_tile = P.budget - Upfx - stile;
-    float acc[T];
-#pragma unroll
-    for (int i = 0; i < T; ++i) acc[i] = finf();
+    unsigned c32 = 0;
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
     for (int a = a0; a < a1; ++a) {
       const float2 av = s.a[a];
       const int ra = max(r_tile + __float_as_int(av.y), -1);
-      const int rowoff = s.lut[ra + 1];
+      const int2 lu = s.lut[ra + 1];
+      c32 += (unsigned)lu.y;
       float Qa[T];
 #pragma unroll
       for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-      eval_row<NB4, TAIL2>(base + rowoff, Qa, acc, ng4);
+      eval_row<NB4, TAIL2>(base + lu.x, Qa, acc, ng4);
     }
-    // fold rows into the thread's best (lowest segment on equal value)
-#pragma unroll
-    for (int i = 0; i < T; ++i) {
-      if (acc[i] <= best && acc[i] < finf()) {
-        uint32_t ec = 0;
-        for (int j = P.ng - 1; j >= 0; --j) ec = ec * (uint32_t)K + ((e[i] >> (j * P.dig_bits)) & dmask);
-        const uint32_t seg = ((chunk * P.L + ec) * P.nQ) + q;
-        if (acc[i] < best || seg < best_seg) {
-          best = acc[i];
-          best_seg = seg;
-        }
-      }
-    }
-    // feasible count: rows with a finite partial sum x feasible (a,b) pairs at this budget
-    {
-      const int rc = min(max(r_tile, -1), Rc);
-      const unsigned cab = s.cnt[q * (Rc + 2) + rc + 1];
-      unsigned c32 = 0;
-#pragma unroll
-      for (int i = 0; i < T; ++i) c32 += (Qr[i] < finf()) ? cab : 0u;
-      cnt += c32;
-    }
+    cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
+    // advance to the next item (q fastest); fold when the lane tile changes
     if (++q == P.nQ) {
       q = 0;
+      fold_rows(P, acc, e, tchunk, q0, best, best_seg);
+      loaded = false;
       if (++grp == P.n_groups) {
         grp = 0;
         ++chunk;
-        if (chunk < P.n_chunks) prefix(chunk);
       }
     }
   }
+  if (loaded) fold_rows(P, acc, e, tchunk, q0, best, best_seg);
 }
 
 template <int NB4, bool TAIL2>
@@ -475,7 +465,6 @@ __global__ void k_finalize(const FinalizeArgs F) {
   const unsigned long long key = F.keys[t];
   const unsigned long long count = F.counts[t];
   __shared__ unsigned long long s_best;
-  __shared__ int s_found;
   const int K = P.K;
   const float *tau_t = P.tau + (size_t)t * P.M * K;
   const uint32_t seg = (uint32_t)(key & 0xffffffffull);
@@ -502,11 +491,11 @@ __global__ void k_finalize(const FinalizeArgs F) {
   }
   if (threadIdx.x == 0) {
     s_best = ~0ull;
-    s_found = found;
   }
   __syncthreads();
   if (found) {
-    const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
+    // the segment starts at a-range q and runs to the end of the row (see fold_rows)
+    const int a0 = (int)(q * P.A), a1 = P.Ka;
     const unsigned long long n = (unsigned long long)(a1 - a0) * P.Kb;
     unsigned long long mine = ~0ull;
     for (unsigned long long li = threadIdx.x; li < n; li += blockDim.x) {
