@@ -221,27 +221,20 @@ def candidate(I: Instance, lam: float, idx: int, budget: int | None = None):
 
 def lambda_star(I: Instance, budget: int | None = None) -> float:
     """Budget-aware maximum workflow throughput: the largest v among all Eq. 2 terms
-    b_m[k] such that sum_m min{u_m[k] : b_m[k] >= v and k passes the memory floor} <= B."""
+    b_m[k] such that some candidate is feasible at target lambda = v, i.e.
+    sum_m min{u_m[k] : option k of LLM m is feasible at lambda = v} <= B.  Feasibility is the full R4
+    test (x <= T and b >= lambda, both in FP64, plus the memory floor), so lambda* itself is feasible."""
     B = I.budget if budget is None else budget
-    tab = option_table(I, 1.0)
-    b, u = tab["b"], tab["u"]
-    floor_ok = np.ones_like(b, dtype=bool)
-    if I.min_units is not None:
-        for m in range(I.M):
-            for k in range(I.K):
-                s_units, _t, _d = option_grid(I, k)
-                t_i = (k // len(I.R)) % len(I.T)
-                floor_ok[m, k] = s_units >= I.min_units[m * len(I.T) + t_i]
-    best = 0.0
-    for v in np.unique(b[floor_ok])[::-1]:
+    b = option_table(I, 1.0)["b"]  # Eq. 2 terms do not depend on lambda (PAPER.md:350)
+    for v in np.unique(b)[::-1]:
+        tab = option_table(I, float(v))
         tot = 0
         for m in range(I.M):
-            sel = u[m][(b[m] >= v) & floor_ok[m]]
+            sel = tab["u"][m][tab["ok"][m]]
             if sel.size == 0:
                 tot = None
                 break
             tot += int(sel.min())
         if tot is not None and tot <= B:
-            best = float(v)
-            break
-    return best
+            return float(v)
+    return 0.0

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "alp_internal.h"
 
@@ -138,6 +139,7 @@ struct Smem {
 };
 
 constexpr int kBigUnits = 1 << 28;
+constexpr int kDefaultVariant = 0;
 
 __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
   Smem s;
@@ -202,60 +204,90 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
   __syncthreads();
 }
 
-template <int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&Qa)[kRowsPerLane],
-                                         float (&acc)[kRowsPerLane], int ng4) {
+// Inner-loop encodings of "candidate = Q_a + tau_b; acc = min(acc, candidate)" (V selects; all
+// are the same IEEE binary32 RNE additions and exact mins, so results are identical):
+//   V0: FADD2 {Q,Q}+{b0,b1}, FADD2 {Q,Q}+{b2,b3}, FMNMX3 acc,v0,v1, FMNMX3 acc,v2,v3   (per row)
+//   V1: 4x scalar FADD + 2x FMNMX3                                                     (per row)
+//   V2: FADD2 {Qi,Qj}+{b,b} per (row pair, b) + FMNMX3 per (row, b pair)
+//   V3: V0 with a min tree: t = min(v0,v1,v2); acc = min(acc,t,v3)
+template <int V>
+__device__ __forceinline__ void eval4(const float4 bv, const float (&Qa)[kRowsPerLane], float (&acc)[kRowsPerLane]) {
   constexpr int T = kRowsPerLane;
-  if constexpr (NB4 > 0) {
-#pragma unroll
-    for (int g = 0; g < NB4; ++g) {
-      const float4 bv = *reinterpret_cast<const float4 *>(rp + 16 * g);
-#pragma unroll
-      for (int i = 0; i < T; ++i) {
-        float v0, v1, v2, v3;
-        add2(v0, v1, Qa[i], bv.x, bv.y);
-        add2(v2, v3, Qa[i], bv.z, bv.w);
-        acc[i] = min3(acc[i], v0, v1);
-        acc[i] = min3(acc[i], v2, v3);
-      }
-    }
-  } else {
-#pragma unroll 2
-    for (int g = 0; g < ng4; ++g) {
-      const float4 bv = *reinterpret_cast<const float4 *>(rp + 16 * g);
-#pragma unroll
-      for (int i = 0; i < T; ++i) {
-        float v0, v1, v2, v3;
-        add2(v0, v1, Qa[i], bv.x, bv.y);
-        add2(v2, v3, Qa[i], bv.z, bv.w);
-        acc[i] = min3(acc[i], v0, v1);
-        acc[i] = min3(acc[i], v2, v3);
-      }
-    }
-  }
-  if constexpr (TAIL2) {
-    const int tail = (NB4 > 0 ? NB4 : ng4) * 16;
-    const float2 bv = *reinterpret_cast<const float2 *>(rp + tail);
+  if constexpr (V == 0 || V == 3) {
 #pragma unroll
     for (int i = 0; i < T; ++i) {
-      float v0, v1;
+      float v0, v1, v2, v3;
       add2(v0, v1, Qa[i], bv.x, bv.y);
+      add2(v2, v3, Qa[i], bv.z, bv.w);
+      if constexpr (V == 0) {
+        acc[i] = min3(acc[i], v0, v1);
+        acc[i] = min3(acc[i], v2, v3);
+      } else {
+        acc[i] = min3(acc[i], min3(v0, v1, v2), v3);
+      }
+    }
+  } else if constexpr (V == 1) {
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const float v0 = __fadd_rn(Qa[i], bv.x), v1 = __fadd_rn(Qa[i], bv.y);
+      const float v2 = __fadd_rn(Qa[i], bv.z), v3 = __fadd_rn(Qa[i], bv.w);
       acc[i] = min3(acc[i], v0, v1);
+      acc[i] = min3(acc[i], v2, v3);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < T; i += 2) {
+      float a0, b0, a1, b1, a2, b2, a3, b3;
+      add2b(a0, b0, Qa[i], Qa[i + 1], bv.x);
+      add2b(a1, b1, Qa[i], Qa[i + 1], bv.y);
+      add2b(a2, b2, Qa[i], Qa[i + 1], bv.z);
+      add2b(a3, b3, Qa[i], Qa[i + 1], bv.w);
+      acc[i] = min3(acc[i], a0, a1);
+      acc[i + 1] = min3(acc[i + 1], b0, b1);
+      acc[i] = min3(acc[i], a2, a3);
+      acc[i + 1] = min3(acc[i + 1], b2, b3);
     }
   }
 }
 
-// Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
-// row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
-__device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[kRowsPerLane],
-                                          const uint32_t (&e)[kRowsPerLane], uint32_t chunk, uint32_t q0,
-                                          float &best, uint32_t &best_seg) {
-  const uint32_t dmask = (1u << P.dig_bits) - 1u;
+template <int V>
+__device__ __forceinline__ void eval2(const float2 bv, const float (&Qa)[kRowsPerLane], float (&acc)[kRowsPerLane]) {
 #pragma unroll
   for (int i = 0; i < kRowsPerLane; ++i) {
-    if (acc[i] <= best && acc[i] < finf()) {  // rare after the first items
+    float v0, v1;
+    add2(v0, v1, Qa[i], bv.x, bv.y);
+    acc[i] = min3(acc[i], v0, v1);
+  }
+}
+
+template <int V, int NB4, bool TAIL2>
+__device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&Qa)[kRowsPerLane],
+                                         float (&acc)[kRowsPerLane], int ng4) {
+  if constexpr (NB4 > 0) {
+#pragma unroll
+    for (int g = 0; g < NB4; ++g) eval4<V>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
+  } else {
+#pragma unroll 2
+    for (int g = 0; g < ng4; ++g) eval4<V>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
+  }
+  if constexpr (TAIL2) eval2<V>(*reinterpret_cast<const float2 *>(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
+}
+
+// Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
+// row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
+// The tile's packed digits are re-read only when a row can improve the best (rare).
+__device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[kRowsPerLane], uint32_t tile,
+                                          uint32_t chunk, uint32_t q0, float &best, uint32_t &best_seg) {
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < kRowsPerLane; ++i) any |= (acc[i] <= best) && (acc[i] < finf());
+  if (!any) return;
+  const uint32_t dmask = (1u << P.dig_bits) - 1u;
+  for (int i = 0; i < kRowsPerLane; ++i) {
+    if (acc[i] <= best && acc[i] < finf()) {
+      const uint32_t e = __ldg(P.tile_e + (size_t)tile * kRowsPerLane + i);
       uint32_t ec = 0;  // canonical within-group index: LLM g0 most significant
-      for (int j = 0; j < P.ng; ++j) ec = ec * (uint32_t)P.K + ((e[i] >> (j * P.dig_bits)) & dmask);
+      for (int j = 0; j < P.ng; ++j) ec = ec * (uint32_t)P.K + ((e >> (j * P.dig_bits)) & dmask);
       const uint32_t seg = (chunk * P.L + ec) * P.nQ + q0;
       if (acc[i] < best || seg < best_seg) {
         best = acc[i];
@@ -265,7 +297,7 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
   }
 }
 
-template <int NB4, bool TAIL2>
+template <int V, int NB4, bool TAIL2>
 __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
                               uint32_t &best_seg, unsigned long long &cnt) {
   constexpr int T = kRowsPerLane;
@@ -285,10 +317,9 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   uint32_t chunk = (uint32_t)(tq / P.n_groups);
   // state of the lane tile currently loaded
   float Qr[T], acc[T];
-  uint32_t e[T];
   int r_tile = 0;
   unsigned nfin = 0;
-  uint32_t q0 = q, tchunk = chunk;
+  uint32_t q0 = q, tchunk = chunk, ttile = 0;
   bool loaded = false;
   float Pfx = 0.f;
   int Upfx = 0;
@@ -310,6 +341,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
       const uint32_t tile = grp * kWarpTiles + lane;
       const int stile = __ldg(P.tile_s + tile);
+      uint32_t e[T];
       const uint4 *ep = reinterpret_cast<const uint4 *>(P.tile_e) + (size_t)tile * (T / 4);
 #pragma unroll
       for (int v = 0; v < T / 4; ++v) {
@@ -332,11 +364,13 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       r_tile = P.budget - Upfx - stile;
       q0 = q;
       tchunk = chunk;
+      ttile = tile;
       loaded = true;
     }
     unsigned c32 = 0;
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
+#pragma unroll 1
     for (int a = a0; a < a1; ++a) {
       const float2 av = s.a[a];
       const int ra = max(r_tile + __float_as_int(av.y), -1);
@@ -345,13 +379,13 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       float Qa[T];
 #pragma unroll
       for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-      eval_row<NB4, TAIL2>(base + lu.x, Qa, acc, ng4);
+      eval_row<V, NB4, TAIL2>(base + lu.x, Qa, acc, ng4);
     }
     cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
     // advance to the next item (q fastest); fold when the lane tile changes
     if (++q == P.nQ) {
       q = 0;
-      fold_rows(P, acc, e, tchunk, q0, best, best_seg);
+      fold_rows(P, acc, ttile, tchunk, q0, best, best_seg);
       loaded = false;
       if (++grp == P.n_groups) {
         grp = 0;
@@ -359,10 +393,10 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
     }
   }
-  if (loaded) fold_rows(P, acc, e, tchunk, q0, best, best_seg);
+  if (loaded) fold_rows(P, acc, ttile, tchunk, q0, best, best_seg);
 }
 
-template <int NB4, bool TAIL2>
+template <int V, int NB4, bool TAIL2>
 __global__ void __launch_bounds__(kThreads, 3)
     k_search(const __grid_constant__ SearchArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -375,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     for (int c = 0; c < P.n_bchunks; ++c) {
       __syncthreads();
       build_tables(P, s, t, c);
-      process_items<NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
+      process_items<V, NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
     }
     unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
 #pragma unroll
@@ -404,9 +438,25 @@ __global__ void __launch_bounds__(kThreads, 3)
 }
 
 // Host-side dispatch over the b-chunk width specialisations.
+static int g_variant = -1;
+static int variant() {  // inner-loop encoding (tuning knob; all variants give identical results)
+  if (g_variant < 0) {
+    const char *v = getenv("ALP_KERNEL_VARIANT");
+    g_variant = v ? atoi(v) : kDefaultVariant;
+    if (g_variant < 0 || g_variant > 3) g_variant = kDefaultVariant;
+  }
+  return g_variant;
+}
+
 template <int NB4, bool TAIL2>
 static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
-  auto fn = k_search<NB4, TAIL2>;
+  auto fn = k_search<0, NB4, TAIL2>;
+  switch (variant()) {
+    case 1: fn = k_search<1, NB4, TAIL2>; break;
+    case 2: fn = k_search<2, NB4, TAIL2>; break;
+    case 3: fn = k_search<3, NB4, TAIL2>; break;
+    default: break;
+  }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
   if (e != cudaSuccess) return e;
   fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
@@ -415,7 +465,7 @@ static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
 
 template <int NB4, bool TAIL2>
 static int occ_one(const SearchArgs &a) {
-  auto fn = k_search<NB4, TAIL2>;
+  auto fn = k_search<0, NB4, TAIL2>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, a.smem_bytes) != cudaSuccess) return 0;
