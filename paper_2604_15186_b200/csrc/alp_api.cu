@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -54,16 +55,37 @@ struct DBuf {
   }
 };
 
-template <class T>
-cudaError_t upload(DBuf<T> &d, const std::vector<T> &h, uint64_t &bytes) {
-  cudaError_t e = d.ensure(h.size());
-  if (e != cudaSuccess) return e;
-  if (!h.empty()) {
-    e = cudaMemcpy(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
-    bytes += h.size() * sizeof(T);
+// One device allocation for every table a handle owns: the host stages the copied sections into
+// one buffer (one cudaMalloc + one cudaMemcpy per alp_build); scratch sections follow, uncopied.
+struct Arena {
+  std::vector<unsigned char> host;
+  size_t copied = 0, total = 0;
+  std::vector<std::pair<size_t, void **>> fix;
+  static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
+  template <class T>
+  void add(const std::vector<T> &v, T **dptr) {
+    const size_t off = align(total);
+    total = off + v.size() * sizeof(T);
+    host.resize(total);
+    if (!v.empty()) memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+    copied = total;
+    fix.push_back({off, reinterpret_cast<void **>(dptr)});
   }
-  return e;
-}
+  template <class T>
+  void scratch(size_t count, T **dptr) {
+    const size_t off = align(total);
+    total = off + count * sizeof(T);
+    fix.push_back({off, reinterpret_cast<void **>(dptr)});
+  }
+  cudaError_t commit(void **base, uint64_t &h2d) {
+    cudaError_t e = cudaMalloc(base, total ? total : 1);
+    if (e != cudaSuccess) return e;
+    if (copied) e = cudaMemcpy(*base, host.data(), copied, cudaMemcpyHostToDevice);
+    h2d += copied;
+    for (auto &f : fix) *f.second = static_cast<unsigned char *>(*base) + f.first;
+    return e;
+  }
+};
 
 int ceil_log2(int k) {
   int b = 0;
@@ -88,21 +110,32 @@ struct alp_s {
   uint32_t L = 1, n_chunks = 1, n_groups = 1, nQ = 1, A = 1;
   uint32_t pw[ALP_MAX_M] = {0};
   std::vector<int> tile_s, bperm, bu, dv, dcnt;
-  std::vector<uint32_t> tile_e;
+  std::vector<uint32_t> tile_e, tile_off;
+  int rows_per_lane = 16;
   int umax_a = 0, umax_b = 0;
   long long umax_total = 0;
   // device
   int device = 0, sm_count = 148;
-  DBuf<double> d_n, d_p, d_rate, d_lat, d_tmax;
-  DBuf<int> d_S, d_T, d_R, d_off, d_minu, d_u, d_tile_s, d_bperm, d_dv, d_dcnt;
-  DBuf<uint32_t> d_tile_e;
-  DBuf<float> d_tau_fixed;
-  DBuf<double> d_term_fixed, d_b_fixed;
-  // per-search scratch
-  DBuf<double> d_targets, d_term, d_b;
-  DBuf<float> d_tau;
-  DBuf<alp_result> d_res;
-  DBuf<unsigned long long> d_keys, d_counts;
+  void *d_arena = nullptr;  // every static table + single-target scratch (one allocation)
+  double *d_n = nullptr, *d_p = nullptr, *d_rate = nullptr, *d_lat = nullptr, *d_tmax = nullptr;
+  int *d_S = nullptr, *d_T = nullptr, *d_R = nullptr, *d_off = nullptr, *d_minu = nullptr, *d_u = nullptr;
+  int *d_tile_s = nullptr, *d_bperm = nullptr, *d_dv = nullptr, *d_dcnt = nullptr;
+  uint32_t *d_tile_e = nullptr, *d_tile_off = nullptr;
+  float *d_tau_fixed = nullptr;
+  double *d_term_fixed = nullptr, *d_b_fixed = nullptr;
+  // per-search scratch: arena (1 target) or grown buffers (n > 1)
+  double *a_targets = nullptr, *a_term = nullptr, *a_b = nullptr;
+  float *a_tau = nullptr;
+  alp_result *a_res = nullptr;
+  unsigned long long *a_keys = nullptr, *a_counts = nullptr;
+  DBuf<double> g_targets, g_term, g_b;
+  DBuf<float> g_tau;
+  DBuf<alp_result> g_res;
+  DBuf<unsigned long long> g_keys, g_counts;
+  double *s_targets = nullptr, *s_term = nullptr, *s_b = nullptr;
+  float *s_tau = nullptr;
+  alp_result *s_res = nullptr;
+  unsigned long long *s_keys = nullptr, *s_counts = nullptr;
   DBuf<int> d_opts, d_pfeas;
   DBuf<double> d_plat, d_pthr;
   DBuf<long long> d_punits;
@@ -117,25 +150,21 @@ struct alp_s {
   DevProfiles dprof() const {
     DevProfiles d;
     d.M = M; d.F = F; d.nS = nS; d.nT = nT; d.nR = nR; d.K = K;
-    d.n = d_n.p; d.p = d_p.p; d.S = d_S.p; d.T = d_T.p; d.R = d_R.p; d.prof_off = d_off.p;
-    d.rate = d_rate.p; d.lat = d_lat.p; d.tmax = d_tmax.p;
-    d.min_units = min_units.empty() ? nullptr : d_minu.p;
+    d.n = d_n; d.p = d_p; d.S = d_S; d.T = d_T; d.R = d_R; d.prof_off = d_off;
+    d.rate = d_rate; d.lat = d_lat; d.tmax = d_tmax;
+    d.min_units = min_units.empty() ? nullptr : d_minu;
     return d;
   }
 
   ~alp_s() {
-    for (auto *b : {&d_n, &d_p, &d_rate, &d_lat, &d_tmax, &d_term_fixed, &d_b_fixed, &d_targets, &d_term, &d_b,
-                    &d_plat, &d_pthr})
-      b->release();
-    for (auto *b : {&d_S, &d_T, &d_R, &d_off, &d_minu, &d_u, &d_tile_s, &d_bperm, &d_dv, &d_dcnt, &d_opts, &d_pfeas})
-      b->release();
-    d_tile_e.release();
-    d_tau_fixed.release();
-    d_tau.release();
-    d_res.release();
-    d_keys.release();
-    d_counts.release();
+    for (auto *b : {&g_targets, &g_term, &g_b, &d_plat, &d_pthr}) b->release();
+    for (auto *b : {&d_opts, &d_pfeas}) b->release();
+    g_tau.release();
+    g_res.release();
+    g_keys.release();
+    g_counts.release();
     d_punits.release();
+    if (d_arena) cudaFree(d_arena);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -181,25 +210,24 @@ alp_status make_plan(alp_s *h) {
   }
   auto U = [&](int m, int k) { return h->u[(size_t)m * K + k]; };
   // sort list: entries of the sort group ordered by unit sum (stable in canonical order), padded
-  // so every lane tile holds kRowsPerLane entries of one unit sum.
-  std::vector<int> sum(L);
-  int smax = 0;
-  for (uint32_t e = 0; e < L; ++e) {
-    uint32_t rem = e;
-    int s = 0;
-    for (int j = ng - 1; j >= 0; --j) {
-      s += U(h->g0 + j, (int)(rem % (uint32_t)K));
-      rem /= (uint32_t)K;
-    }
-    sum[e] = s;
-    smax = std::max(smax, s);
+  // so every lane tile holds T entries of one unit sum.
+  // unit sum of every entry, built digit by digit (entry e = sum_j d_j K^(ng-1-j))
+  std::vector<int> sum(L, 0);
+  for (int j = 0; j < ng; ++j) {
+    uint32_t stride = 1;
+    for (int q = j + 1; q < ng; ++q) stride *= (uint32_t)K;
+    for (uint32_t e = 0; e < L; ++e) sum[e] += U(h->g0 + j, (int)((e / stride) % (uint32_t)K));
   }
-  std::vector<uint32_t> order(L);
-  std::iota(order.begin(), order.end(), 0u);
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return sum[a] < sum[b]; });
+  int smax = 0;
+  for (uint32_t e = 0; e < L; ++e) smax = std::max(smax, sum[e]);
+  // stable counting sort by unit sum
+  std::vector<uint32_t> start(smax + 2, 0), order(L);
+  for (uint32_t e = 0; e < L; ++e) ++start[sum[e] + 1];
+  for (int s = 0; s <= smax; ++s) start[s + 1] += start[s];
+  for (uint32_t e = 0; e < L; ++e) order[start[sum[e]]++] = e;
   h->tile_s.clear();
   h->tile_e.clear();
-  const int T = kRowsPerLane;
+  const int T = h->rows_per_lane;
   auto pack = [&](uint32_t e) {
     uint32_t rem = e, v = 0;
     for (int j = ng - 1; j >= 0; --j) {
@@ -225,6 +253,21 @@ alp_status make_plan(alp_s *h) {
     for (int r = 0; r < T; ++r) h->tile_e.push_back(kDummy);
   }
   h->n_groups = (uint32_t)(h->tile_s.size() / kWarpTiles);
+  // smem byte offsets of each row's sort-group terms (tau of LLM g0+j lives at ((g0+j)*K + d)*4;
+  // slot g1*K holds 0.0f for unused digits, slot g1*K+1 holds +inf for padded rows)
+  const uint32_t zero_off = (uint32_t)(h->g1 * K) * 4u, inf_off = zero_off + 4u;
+  h->tile_off.assign(h->tile_e.size() * 2, 0u);
+  const uint32_t dm = (1u << h->dig_bits) - 1u;
+  for (size_t i = 0; i < h->tile_e.size(); ++i) {
+    uint32_t off[4] = {zero_off, zero_off, zero_off, zero_off};
+    if (h->tile_e[i] == kDummy) {
+      off[0] = inf_off;
+    } else {
+      for (int j = 0; j < ng; ++j) off[j] = (uint32_t)((h->g0 + j) * K + ((h->tile_e[i] >> (j * h->dig_bits)) & dm)) * 4u;
+    }
+    h->tile_off[2 * i] = off[0] | (off[1] << 16);
+    h->tile_off[2 * i + 1] = off[2] | (off[3] << 16);
+  }
   // b columns sorted by units (stable): the feasible set for a remaining budget is a prefix.
   h->bperm.resize(K);
   std::iota(h->bperm.begin(), h->bperm.end(), 0);
@@ -262,18 +305,46 @@ alp_status make_plan(alp_s *h) {
   return ALP_OK;
 }
 
-alp_status upload_plan(alp_s *h) {
-  uint64_t &B = h->h2d;
-  CU(upload(h->d_tile_s, h->tile_s, B));
-  CU(upload(h->d_tile_e, h->tile_e, B));
-  CU(upload(h->d_bperm, h->bperm, B));
-  CU(upload(h->d_dv, h->dv, B));
-  CU(upload(h->d_dcnt, h->dcnt, B));
-  CU(upload(h->d_u, h->u, B));
+// Stage every static table of the handle (+ single-target scratch) into one device allocation.
+alp_status upload_all(alp_s *h) {
+  Arena A;
+  const size_t MK = (size_t)h->M * h->K;
+  if (h->from_terms) {
+    A.add(h->tau_fixed, &h->d_tau_fixed);
+    A.add(h->term_fixed, &h->d_term_fixed);
+    A.add(h->b_fixed, &h->d_b_fixed);
+  } else {
+    A.add(h->n, &h->d_n);
+    A.add(h->p, &h->d_p);
+    A.add(h->S, &h->d_S);
+    A.add(h->prof_off, &h->d_off);
+    A.add(h->rate, &h->d_rate);
+    A.add(h->lat, &h->d_lat);
+    A.add(h->tmax, &h->d_tmax);
+    if (!h->min_units.empty()) A.add(h->min_units, &h->d_minu);
+  }
+  A.add(h->T, &h->d_T);
+  A.add(h->R, &h->d_R);
+  A.add(h->u, &h->d_u);
+  A.add(h->tile_s, &h->d_tile_s);
+  A.add(h->tile_e, &h->d_tile_e);
+  A.add(h->tile_off, &h->d_tile_off);
+  A.add(h->bperm, &h->d_bperm);
+  A.add(h->dv, &h->d_dv);
+  A.add(h->dcnt, &h->d_dcnt);
+  A.scratch(1, &h->a_targets);
+  A.scratch(MK, &h->a_tau);
+  A.scratch(MK, &h->a_term);
+  A.scratch(MK, &h->a_b);
+  A.scratch(1, &h->a_res);
+  A.scratch(1, &h->a_keys);
+  A.scratch(1, &h->a_counts);
+  CU(A.commit(&h->d_arena, h->h2d));
   return ALP_OK;
 }
 
 alp_status init_device(alp_s *h) {
+  if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 8) ? 8 : 16;
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -328,7 +399,7 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
     a.row_stride = a.bchunk_wpad + 1;  // >= 1 padding column (holds the row's finite count)
     while (a.row_stride % 8 != 4) ++a.row_stride;
     int off = 0;
-    a.off_tau = off; off = align16(off + h->g1 * h->K * 4);
+    a.off_tau = off; off = align16(off + (h->g1 * h->K + 2) * 4);  // must stay at offset 0
     a.off_u = off; off = align16(off + h->g0 * h->K * 4);
     a.off_a = off; off = align16(off + h->Ka * 8);
     a.off_lut = off; off = align16(off + (a.budget + 2) * 8);
@@ -341,8 +412,9 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   while (layout(W) > 72 * 1024 && W > 64) W = (W + 1) / 2;
   if (a.smem_bytes > 220 * 1024) return fail(ALP_EINVAL, "shared-memory tables too large (%d B)", a.smem_bytes);
   a.tau = nullptr;  // set by caller
-  a.u = h->d_u.p; a.tile_s = h->d_tile_s.p; a.tile_e = h->d_tile_e.p; a.bperm = h->d_bperm.p;
-  a.dv = h->d_dv.p; a.dcnt = h->d_dcnt.p;
+  a.u = h->d_u; a.tile_s = h->d_tile_s; a.tile_e = h->d_tile_e; a.tile_off = h->d_tile_off; a.bperm = h->d_bperm;
+  a.rows_per_lane = h->rows_per_lane;
+  a.dv = h->d_dv; a.dcnt = h->d_dcnt;
   int bps = search_max_blocks_per_sm(a);
   if (bps < 1) return fail(ALP_ECUDA, "search kernel cannot be resident (smem %d B)", a.smem_bytes);
   g.grid = h->sm_count * bps;
@@ -351,13 +423,20 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
 
 alp_status ensure_scratch(alp_s *h, int n) {
   const size_t MK = (size_t)h->M * h->K;
-  CU(h->d_targets.ensure(n));
-  CU(h->d_tau.ensure(n * MK));
-  CU(h->d_term.ensure(n * MK));
-  CU(h->d_b.ensure(n * MK));
-  CU(h->d_res.ensure(n));
-  CU(h->d_keys.ensure(n));
-  CU(h->d_counts.ensure(n));
+  if (n <= 1) {
+    h->s_targets = h->a_targets; h->s_tau = h->a_tau; h->s_term = h->a_term; h->s_b = h->a_b;
+    h->s_res = h->a_res; h->s_keys = h->a_keys; h->s_counts = h->a_counts;
+    return ALP_OK;
+  }
+  CU(h->g_targets.ensure(n));
+  CU(h->g_tau.ensure(n * MK));
+  CU(h->g_term.ensure(n * MK));
+  CU(h->g_b.ensure(n * MK));
+  CU(h->g_res.ensure(n));
+  CU(h->g_keys.ensure(n));
+  CU(h->g_counts.ensure(n));
+  h->s_targets = h->g_targets.p; h->s_tau = h->g_tau.p; h->s_term = h->g_term.p; h->s_b = h->g_b.p;
+  h->s_res = h->g_res.p; h->s_keys = h->g_keys.p; h->s_counts = h->g_counts.p;
   return ALP_OK;
 }
 
@@ -365,24 +444,24 @@ alp_status ensure_scratch(alp_s *h, int n) {
 alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st, unsigned long long *keys,
                          unsigned long long *counts) {
   const size_t MK = (size_t)h->M * h->K;
-  CU(cudaMemcpyAsync(h->d_targets.p, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->s_targets, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
   if (h->from_terms) {
     for (int t = 0; t < n; ++t) {
-      CU(cudaMemcpyAsync(h->d_tau.p + t * MK, h->d_tau_fixed.p, MK * sizeof(float), cudaMemcpyDeviceToDevice, st));
-      CU(cudaMemcpyAsync(h->d_term.p + t * MK, h->d_term_fixed.p, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      CU(cudaMemcpyAsync(h->d_b.p + t * MK, h->d_b_fixed.p, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->s_tau + t * MK, h->d_tau_fixed, MK * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->s_term + t * MK, h->d_term_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->s_b + t * MK, h->d_b_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
     if (keys) CU(launch_init_keys(keys, counts, n, st));
     return ALP_OK;
   }
   OptionArgs o;
   o.prof = h->dprof();
-  o.targets = h->d_targets.p;
+  o.targets = h->s_targets;
   o.n_targets = n;
-  o.tau = h->d_tau.p;
-  o.term = h->d_term.p;
-  o.b = h->d_b.p;
-  o.u = h->d_u.p;
+  o.tau = h->s_tau;
+  o.term = h->s_term;
+  o.b = h->s_b;
+  o.u = h->d_u;
   o.keys = keys;
   o.counts = counts;
   CU(launch_option_table(o, st));
@@ -413,7 +492,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, int n, int64_t bud
   if (s != ALP_OK) return s;
   g.a.item_lo = lo;
   g.a.item_hi = hi;
-  g.a.tau = h->d_tau.p;
+  g.a.tau = h->s_tau;
   g.a.keys = keys;
   g.a.counts = counts;
   CU(cudaEventRecord(h->ev0, st));
@@ -438,19 +517,19 @@ alp_status finalize_impl(alp_s *h, const double *targets, int n, int64_t budget,
   (void)targets;
   FinalizeArgs f;
   f.s = g.a;
-  f.s.tau = h->d_tau.p;
-  f.term = h->d_term.p;
-  f.b = h->d_b.p;
-  f.S = h->from_terms ? nullptr : h->d_S.p;
-  f.T = h->d_T.p;
-  f.R = h->d_R.p;
+  f.s.tau = h->s_tau;
+  f.term = h->s_term;
+  f.b = h->s_b;
+  f.S = h->from_terms ? nullptr : h->d_S;
+  f.T = h->d_T;
+  f.R = h->d_R;
   f.nS = h->nS; f.nT = h->nT; f.nR = h->nR;
   f.N = h->N;
   f.keys = keys;
   f.counts = counts;
-  f.out = h->d_res.p;
+  f.out = h->s_res;
   CU(launch_finalize(f, st));
-  CU(cudaMemcpyAsync(out, h->d_res.p, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   h->last_launches += 1;
   if (h->ev_pending) {
@@ -534,22 +613,7 @@ alp_status alp_build(const alp_desc *d, alp_t **out) {
   compute_units(h);
   alp_status s = init_device(h);
   if (s == ALP_OK) s = make_plan(h);
-  if (s == ALP_OK) s = upload_plan(h);
-  if (s == ALP_OK) {
-    uint64_t &B = h->h2d;
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = upload(h->d_n, h->n, B);
-    if (e == cudaSuccess) e = upload(h->d_p, h->p, B);
-    if (e == cudaSuccess) e = upload(h->d_S, h->S, B);
-    if (e == cudaSuccess) e = upload(h->d_T, h->T, B);
-    if (e == cudaSuccess) e = upload(h->d_R, h->R, B);
-    if (e == cudaSuccess) e = upload(h->d_off, h->prof_off, B);
-    if (e == cudaSuccess) e = upload(h->d_rate, h->rate, B);
-    if (e == cudaSuccess) e = upload(h->d_lat, h->lat, B);
-    if (e == cudaSuccess) e = upload(h->d_tmax, h->tmax, B);
-    if (e == cudaSuccess && !h->min_units.empty()) e = upload(h->d_minu, h->min_units, B);
-    if (e != cudaSuccess) s = fail(ALP_ECUDA, "upload: %s", cudaGetErrorString(e));
-  }
+  if (s == ALP_OK) s = upload_all(h);
   if (s != ALP_OK) {
     delete h;
     return s;
@@ -590,15 +654,7 @@ alp_status alp_build_from_terms(int32_t M, int32_t K, const float *tau, const in
   std::iota(h->R.begin(), h->R.end(), 1);
   alp_status s = init_device(h);
   if (s == ALP_OK) s = make_plan(h);
-  if (s == ALP_OK) s = upload_plan(h);
-  if (s == ALP_OK) {
-    cudaError_t e = upload(h->d_tau_fixed, h->tau_fixed, h->h2d);
-    if (e == cudaSuccess) e = upload(h->d_term_fixed, h->term_fixed, h->h2d);
-    if (e == cudaSuccess) e = upload(h->d_b_fixed, h->b_fixed, h->h2d);
-    if (e == cudaSuccess) e = upload(h->d_T, h->T, h->h2d);
-    if (e == cudaSuccess) e = upload(h->d_R, h->R, h->h2d);
-    if (e != cudaSuccess) s = fail(ALP_ECUDA, "upload: %s", cudaGetErrorString(e));
-  }
+  if (s == ALP_OK) s = upload_all(h);
   if (s != ALP_OK) {
     delete h;
     return s;
@@ -637,9 +693,9 @@ alp_status alp_option_table(alp_t *h, double lambda, float *tau, double *term, d
   s = option_tables(h, &lambda, 1, h->stream, nullptr, nullptr);
   if (s != ALP_OK) return s;
   const size_t MK = (size_t)h->M * h->K;
-  if (tau) CU(cudaMemcpyAsync(tau, h->d_tau.p, MK * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
-  if (term) CU(cudaMemcpyAsync(term, h->d_term.p, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if (b) CU(cudaMemcpyAsync(b, h->d_b.p, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (tau) CU(cudaMemcpyAsync(tau, h->s_tau, MK * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (term) CU(cudaMemcpyAsync(term, h->s_term, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (b) CU(cudaMemcpyAsync(b, h->s_b, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   if (u) memcpy(u, h->u.data(), MK * sizeof(int32_t));
   return ALP_OK;
@@ -726,9 +782,9 @@ alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t 
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   const uint64_t items = alp_num_items(h, budget_units);
-  s = search_shard_impl(h, targets, n, budget_units, 0, items, h->stream, h->d_keys.p, h->d_counts.p);
+  s = search_shard_impl(h, targets, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts);
   if (s != ALP_OK) return s;
-  return finalize_impl(h, targets, n, budget_units, h->d_keys.p, h->d_counts.p, h->stream, out);
+  return finalize_impl(h, targets, n, budget_units, h->s_keys, h->s_counts, h->stream, out);
 }
 
 alp_status alp_search(alp_t *h, double target, int64_t budget_units, alp_result *out) {

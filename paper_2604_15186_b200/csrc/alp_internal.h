@@ -8,7 +8,6 @@
 
 namespace alp {
 
-constexpr int kRowsPerLane = 8;          // T: rows (sort-list entries) per lane tile
 constexpr int kWarpTiles = 32;           // lane tiles per warp group
 constexpr int kThreads = 256;            // threads per search block
 constexpr uint32_t kDummy = 0xFFFFFFFFu; // padded row marker in the tile list
@@ -59,6 +58,8 @@ struct SearchArgs {
   const int *u;          // [M][K]
   const int *tile_s;     // [n_tiles] units of the lane tile's sort-group options
   const uint32_t *tile_e;// [n_tiles][T] packed sort-group digits (kDummy = padding)
+  const uint32_t *tile_off;// [n_tiles][T][2] smem byte offsets of the row's sort-group terms (4 x 16 bit)
+  int rows_per_lane;     // T (8 or 16)
   const int *bperm;      // [Kb] canonical option of u-sorted column j
   const int *dv;         // [Dall] distinct b unit values, ascending
   const int *dcnt;       // [Dall+1] dcnt[i] = #u-sorted columns with u <= dv[i-1] (dcnt[0] = 0)

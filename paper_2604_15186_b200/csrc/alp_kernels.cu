@@ -25,7 +25,6 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "alp_internal.h"
 
@@ -129,7 +128,7 @@ __device__ __forceinline__ float min3(float a, float b, float c) {
 }
 
 struct Smem {
-  float *tau;      // [g1*K] tau of prefix + sort-group LLMs (current target); at smem offset 0
+  float *tau;      // [g1*K + 2] tau of prefix + sort-group LLMs (current target), then {0, +inf}; offset 0
   int *u;          // [g0*K] units of prefix LLMs
   float2 *a;       // [Ka] {tau_a, bits(-u_a)}; u_a := kBigUnits when tau_a is +inf
   int2 *lut;       // [R+2] {byte offset of the masked row, #finite entries in it} for r = -1..R
@@ -139,7 +138,6 @@ struct Smem {
 };
 
 constexpr int kBigUnits = 1 << 28;
-constexpr int kDefaultVariant = 0;
 
 __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
   Smem s;
@@ -161,6 +159,10 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
   const int c0 = c * P.bchunk_w;
   const int c1 = min(c0 + P.bchunk_w, P.Kb);
   for (int i = tid; i < P.g1 * K; i += nt) s.tau[i] = tau_t[i];
+  if (tid == 0) {
+    s.tau[P.g1 * K] = 0.f;         // unused sort-group digit slot: x + 0 = x exactly
+    s.tau[P.g1 * K + 1] = finf();  // padded (dummy) row
+  }
   for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
   for (int a = tid; a < P.Ka; a += nt) {
     float2 v = make_float2(0.f, __int_as_float(0));
@@ -204,88 +206,65 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
   __syncthreads();
 }
 
-// Inner-loop encodings of "candidate = Q_a + tau_b; acc = min(acc, candidate)" (V selects; all
-// are the same IEEE binary32 RNE additions and exact mins, so results are identical):
-//   V0: FADD2 {Q,Q}+{b0,b1}, FADD2 {Q,Q}+{b2,b3}, FMNMX3 acc,v0,v1, FMNMX3 acc,v2,v3   (per row)
-//   V1: 4x scalar FADD + 2x FMNMX3                                                     (per row)
-//   V2: FADD2 {Qi,Qj}+{b,b} per (row pair, b) + FMNMX3 per (row, b pair)
-//   V3: V0 with a min tree: t = min(v0,v1,v2); acc = min(acc,t,v3)
-template <int V>
-__device__ __forceinline__ void eval4(const float4 bv, const float (&Qa)[kRowsPerLane], float (&acc)[kRowsPerLane]) {
-  constexpr int T = kRowsPerLane;
-  if constexpr (V == 0 || V == 3) {
+// "candidate = Q_a + tau_b; acc = min(acc, candidate)" for 4 b values and T rows:
+//   FADD2 {Q_i, Q_i+1} + {b, b} per (row pair, b)   (add.rn.f32x2; the b operand is a scalar broadcast)
+//   FMNMX3 acc_i = min(acc_i, v_b0, v_b1)           (3-input min)
+// = one issue slot per candidate.  The row-pair form lets the Q pair sit in the operand-reuse cache
+// across the 4 b values (tools/microbench/pipes3: fastest of the encodings tried).
+template <int T>
+__device__ __forceinline__ void eval4(const float4 bv, const float (&Qa)[T], float (&acc)[T]) {
 #pragma unroll
-    for (int i = 0; i < T; ++i) {
-      float v0, v1, v2, v3;
-      add2(v0, v1, Qa[i], bv.x, bv.y);
-      add2(v2, v3, Qa[i], bv.z, bv.w);
-      if constexpr (V == 0) {
-        acc[i] = min3(acc[i], v0, v1);
-        acc[i] = min3(acc[i], v2, v3);
-      } else {
-        acc[i] = min3(acc[i], min3(v0, v1, v2), v3);
-      }
-    }
-  } else if constexpr (V == 1) {
-#pragma unroll
-    for (int i = 0; i < T; ++i) {
-      const float v0 = __fadd_rn(Qa[i], bv.x), v1 = __fadd_rn(Qa[i], bv.y);
-      const float v2 = __fadd_rn(Qa[i], bv.z), v3 = __fadd_rn(Qa[i], bv.w);
-      acc[i] = min3(acc[i], v0, v1);
-      acc[i] = min3(acc[i], v2, v3);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < T; i += 2) {
-      float a0, b0, a1, b1, a2, b2, a3, b3;
-      add2b(a0, b0, Qa[i], Qa[i + 1], bv.x);
-      add2b(a1, b1, Qa[i], Qa[i + 1], bv.y);
-      add2b(a2, b2, Qa[i], Qa[i + 1], bv.z);
-      add2b(a3, b3, Qa[i], Qa[i + 1], bv.w);
-      acc[i] = min3(acc[i], a0, a1);
-      acc[i + 1] = min3(acc[i + 1], b0, b1);
-      acc[i] = min3(acc[i], a2, a3);
-      acc[i + 1] = min3(acc[i + 1], b2, b3);
-    }
+  for (int i = 0; i < T; i += 2) {
+    float a0, b0, a1, b1, a2, b2, a3, b3;
+    add2b(a0, b0, Qa[i], Qa[i + 1], bv.x);
+    add2b(a1, b1, Qa[i], Qa[i + 1], bv.y);
+    add2b(a2, b2, Qa[i], Qa[i + 1], bv.z);
+    add2b(a3, b3, Qa[i], Qa[i + 1], bv.w);
+    acc[i] = min3(acc[i], a0, a1);
+    acc[i + 1] = min3(acc[i + 1], b0, b1);
+    acc[i] = min3(acc[i], a2, a3);
+    acc[i + 1] = min3(acc[i + 1], b2, b3);
   }
 }
 
-template <int V>
-__device__ __forceinline__ void eval2(const float2 bv, const float (&Qa)[kRowsPerLane], float (&acc)[kRowsPerLane]) {
+template <int T>
+__device__ __forceinline__ void eval2(const float2 bv, const float (&Qa)[T], float (&acc)[T]) {
 #pragma unroll
-  for (int i = 0; i < kRowsPerLane; ++i) {
-    float v0, v1;
-    add2(v0, v1, Qa[i], bv.x, bv.y);
-    acc[i] = min3(acc[i], v0, v1);
+  for (int i = 0; i < T; i += 2) {
+    float a0, b0, a1, b1;
+    add2b(a0, b0, Qa[i], Qa[i + 1], bv.x);
+    add2b(a1, b1, Qa[i], Qa[i + 1], bv.y);
+    acc[i] = min3(acc[i], a0, a1);
+    acc[i + 1] = min3(acc[i + 1], b0, b1);
   }
 }
 
-template <int V, int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&Qa)[kRowsPerLane],
-                                         float (&acc)[kRowsPerLane], int ng4) {
+template <int T, int NB4, bool TAIL2>
+__device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&Qa)[T], float (&acc)[T], int ng4) {
   if constexpr (NB4 > 0) {
 #pragma unroll
-    for (int g = 0; g < NB4; ++g) eval4<V>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
+    for (int g = 0; g < NB4; ++g) eval4<T>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
   } else {
 #pragma unroll 2
-    for (int g = 0; g < ng4; ++g) eval4<V>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
+    for (int g = 0; g < ng4; ++g) eval4<T>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
   }
-  if constexpr (TAIL2) eval2<V>(*reinterpret_cast<const float2 *>(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
+  if constexpr (TAIL2) eval2<T>(*reinterpret_cast<const float2 *>(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
 }
 
 // Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
 // row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
-// The tile's packed digits are re-read only when a row can improve the best (rare).
-__device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[kRowsPerLane], uint32_t tile,
-                                          uint32_t chunk, uint32_t q0, float &best, uint32_t &best_seg) {
+// The tile's packed digits are read only when a row can improve the best (rare).
+template <int T>
+__device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[T], uint32_t tile, uint32_t chunk,
+                                          uint32_t q0, float &best, uint32_t &best_seg) {
   bool any = false;
 #pragma unroll
-  for (int i = 0; i < kRowsPerLane; ++i) any |= (acc[i] <= best) && (acc[i] < finf());
+  for (int i = 0; i < T; ++i) any |= (acc[i] <= best) && (acc[i] < finf());
   if (!any) return;
   const uint32_t dmask = (1u << P.dig_bits) - 1u;
-  for (int i = 0; i < kRowsPerLane; ++i) {
+  for (int i = 0; i < T; ++i) {
     if (acc[i] <= best && acc[i] < finf()) {
-      const uint32_t e = __ldg(P.tile_e + (size_t)tile * kRowsPerLane + i);
+      const uint32_t e = __ldg(P.tile_e + (size_t)tile * T + i);
       uint32_t ec = 0;  // canonical within-group index: LLM g0 most significant
       for (int j = 0; j < P.ng; ++j) ec = ec * (uint32_t)P.K + ((e >> (j * P.dig_bits)) & dmask);
       const uint32_t seg = (chunk * P.L + ec) * P.nQ + q0;
@@ -297,10 +276,9 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
   }
 }
 
-template <int V, int NB4, bool TAIL2>
+template <int T, int NB4, bool TAIL2>
 __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
                               uint32_t &best_seg, unsigned long long &cnt) {
-  constexpr int T = kRowsPerLane;
   const int lane = threadIdx.x & 31;
   const uint64_t nW = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -310,7 +288,6 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   if (it >= end) return;
   const int K = P.K;
   const int ng4 = P.bchunk_wpad >> 2;
-  const uint32_t dmask = (1u << P.dig_bits) - 1u;
   uint32_t q = (uint32_t)(it % P.nQ);
   const uint64_t tq = it / P.nQ;
   uint32_t grp = (uint32_t)(tq % P.n_groups);
@@ -324,6 +301,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   float Pfx = 0.f;
   int Upfx = 0;
   uint32_t pchunk = 0xffffffffu;
+  const unsigned char *tau_b = reinterpret_cast<const unsigned char *>(s.tau);
   for (; it < end; ++it) {
     if (!loaded) {
       if (chunk != pchunk) {
@@ -341,25 +319,25 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
       const uint32_t tile = grp * kWarpTiles + lane;
       const int stile = __ldg(P.tile_s + tile);
-      uint32_t e[T];
-      const uint4 *ep = reinterpret_cast<const uint4 *>(P.tile_e) + (size_t)tile * (T / 4);
-#pragma unroll
-      for (int v = 0; v < T / 4; ++v) {
-        const uint4 x = __ldg(ep + v);
-        e[4 * v] = x.x; e[4 * v + 1] = x.y; e[4 * v + 2] = x.z; e[4 * v + 3] = x.w;
-      }
+      // per row: 4 smem byte offsets (16 bits each) of the sort-group terms, in LLM order;
+      // unused digits point at 0.0f, padded rows at +inf
+      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * (T / 2);
       nfin = 0;
 #pragma unroll
-      for (int i = 0; i < T; ++i) {
-        const uint32_t ei = (e[i] == kDummy) ? 0u : e[i];
-        float qv = Pfx;
-        for (int j = 0; j < P.ng; ++j) {
-          const uint32_t d = (ei >> (j * P.dig_bits)) & dmask;
-          qv = __fadd_rn(qv, s.tau[(P.g0 + j) * K + d]);
+      for (int v = 0; v < T / 2; ++v) {
+        const uint4 o = __ldg(op + v);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t w0 = h ? o.z : o.x, w1 = h ? o.w : o.y;
+          float qv = Pfx;
+          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w0 & 0xffffu)));
+          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w0 >> 16)));
+          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w1 & 0xffffu)));
+          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w1 >> 16)));
+          Qr[2 * v + h] = qv;
+          nfin += (qv < finf()) ? 1u : 0u;
+          acc[2 * v + h] = finf();
         }
-        Qr[i] = (e[i] == kDummy) ? finf() : qv;
-        nfin += (Qr[i] < finf()) ? 1u : 0u;
-        acc[i] = finf();
       }
       r_tile = P.budget - Upfx - stile;
       q0 = q;
@@ -379,13 +357,13 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       float Qa[T];
 #pragma unroll
       for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-      eval_row<V, NB4, TAIL2>(base + lu.x, Qa, acc, ng4);
+      eval_row<T, NB4, TAIL2>(base + lu.x, Qa, acc, ng4);
     }
     cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
     // advance to the next item (q fastest); fold when the lane tile changes
     if (++q == P.nQ) {
       q = 0;
-      fold_rows(P, acc, ttile, tchunk, q0, best, best_seg);
+      fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
       loaded = false;
       if (++grp == P.n_groups) {
         grp = 0;
@@ -393,11 +371,11 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
     }
   }
-  if (loaded) fold_rows(P, acc, ttile, tchunk, q0, best, best_seg);
+  if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
 }
 
-template <int V, int NB4, bool TAIL2>
-__global__ void __launch_bounds__(kThreads, 3)
+template <int T, int NB4, bool TAIL2>
+__global__ void __launch_bounds__(kThreads, T >= 16 ? 2 : 3)
     k_search(const __grid_constant__ SearchArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
@@ -409,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     for (int c = 0; c < P.n_bchunks; ++c) {
       __syncthreads();
       build_tables(P, s, t, c);
-      process_items<V, NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
+      process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
     }
     unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
 #pragma unroll
@@ -437,73 +415,63 @@ __global__ void __launch_bounds__(kThreads, 3)
   }
 }
 
-// Host-side dispatch over the b-chunk width specialisations.
-static int g_variant = -1;
-static int variant() {  // inner-loop encoding (tuning knob; all variants give identical results)
-  if (g_variant < 0) {
-    const char *v = getenv("ALP_KERNEL_VARIANT");
-    g_variant = v ? atoi(v) : kDefaultVariant;
-    if (g_variant < 0 || g_variant > 3) g_variant = kDefaultVariant;
-  }
-  return g_variant;
-}
-
-template <int NB4, bool TAIL2>
+// Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
+template <int T, int NB4, bool TAIL2>
 static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
-  auto fn = k_search<0, NB4, TAIL2>;
-  switch (variant()) {
-    case 1: fn = k_search<1, NB4, TAIL2>; break;
-    case 2: fn = k_search<2, NB4, TAIL2>; break;
-    case 3: fn = k_search<3, NB4, TAIL2>; break;
-    default: break;
-  }
+  auto fn = k_search<T, NB4, TAIL2>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
   if (e != cudaSuccess) return e;
   fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int NB4, bool TAIL2>
+template <int T, int NB4, bool TAIL2>
 static int occ_one(const SearchArgs &a) {
-  auto fn = k_search<0, NB4, TAIL2>;
+  auto fn = k_search<T, NB4, TAIL2>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, a.smem_bytes) != cudaSuccess) return 0;
   return n;
 }
 
-// Specialised (fully unrolled) b loop for chunk widths <= 34 columns: NB4 LDS.128 groups plus an
-// optional LDS.64 tail; wider chunks use the runtime loop (NB4 = 0).
-#define ALP_DISPATCH(CALL)                                                   \
+// Fully unrolled b loop for chunk widths <= 34 columns: NB4 LDS.128 groups plus an optional LDS.64
+// tail; wider chunks use the runtime loop (NB4 = 0).
+#define ALP_DISPATCH_W(CALL, T)                                              \
   do {                                                                       \
     const int w = a.bchunk_wpad;                                             \
     const bool t2 = (w % 4) == 2;                                            \
     if (w > 34) {                                                            \
-      if (t2) return CALL(0, true);                                          \
-      return CALL(0, false);                                                 \
+      if (t2) return CALL(T, 0, true);                                       \
+      return CALL(T, 0, false);                                              \
     }                                                                        \
     switch (w) {                                                             \
-      case 2: return CALL(0, true);                                          \
-      case 4: return CALL(1, false); case 6: return CALL(1, true);           \
-      case 8: return CALL(2, false); case 10: return CALL(2, true);          \
-      case 12: return CALL(3, false); case 14: return CALL(3, true);         \
-      case 16: return CALL(4, false); case 18: return CALL(4, true);         \
-      case 20: return CALL(5, false); case 22: return CALL(5, true);         \
-      case 24: return CALL(6, false); case 26: return CALL(6, true);         \
-      case 28: return CALL(7, false); case 30: return CALL(7, true);         \
-      case 32: return CALL(8, false); case 34: return CALL(8, true);         \
-      default: if (t2) return CALL(0, true); return CALL(0, false);          \
+      case 2: return CALL(T, 0, true);                                       \
+      case 4: return CALL(T, 1, false); case 6: return CALL(T, 1, true);     \
+      case 8: return CALL(T, 2, false); case 10: return CALL(T, 2, true);    \
+      case 12: return CALL(T, 3, false); case 14: return CALL(T, 3, true);   \
+      case 16: return CALL(T, 4, false); case 18: return CALL(T, 4, true);   \
+      case 20: return CALL(T, 5, false); case 22: return CALL(T, 5, true);   \
+      case 24: return CALL(T, 6, false); case 26: return CALL(T, 6, true);   \
+      case 28: return CALL(T, 7, false); case 30: return CALL(T, 7, true);   \
+      case 32: return CALL(T, 8, false); case 34: return CALL(T, 8, true);   \
+      default: if (t2) return CALL(T, 0, true); return CALL(T, 0, false);    \
     }                                                                        \
   } while (0)
 
+#define ALP_DISPATCH(CALL)                  \
+  do {                                      \
+    if (a.rows_per_lane == 16) ALP_DISPATCH_W(CALL, 16); \
+    ALP_DISPATCH_W(CALL, 8);                \
+  } while (0)
+
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st) {
-#define CALL(N, T2) launch_one<N, T2>(a, grid, st)
+#define CALL(T, N, T2) launch_one<T, N, T2>(a, grid, st)
   ALP_DISPATCH(CALL);
 #undef CALL
 }
 
 int search_max_blocks_per_sm(const SearchArgs &a) {
-#define CALL(N, T2) occ_one<N, T2>(a)
+#define CALL(T, N, T2) occ_one<T, N, T2>(a)
   ALP_DISPATCH(CALL);
 #undef CALL
 }
