@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdlib>
@@ -87,6 +88,18 @@ struct Arena {
   }
 };
 
+// ALP_TRACE=1 prints host-side phase times of alp_build (tracing aid for the e2e path).
+struct Trace {
+  bool on = getenv("ALP_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char *what) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[alp] %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 int ceil_log2(int k) {
   int b = 0;
   while ((1 << b) < k) ++b;
@@ -111,7 +124,8 @@ struct alp_s {
   uint32_t pw[ALP_MAX_M] = {0};
   std::vector<int> tile_s, bperm, bu, dv, dcnt;
   std::vector<uint32_t> tile_e, tile_off;
-  int rows_per_lane = 16;
+  int rows_per_lane = 8;
+  int min_blocks = 3;
   int umax_a = 0, umax_b = 0;
   long long umax_total = 0;
   // device
@@ -344,7 +358,8 @@ alp_status upload_all(alp_s *h) {
 }
 
 alp_status init_device(alp_s *h) {
-  if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 8) ? 8 : 16;
+  if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 16) ? 16 : 8;
+  if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = (atoi(v) == 4) ? 4 : 3;
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -414,6 +429,7 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.tau = nullptr;  // set by caller
   a.u = h->d_u; a.tile_s = h->d_tile_s; a.tile_e = h->d_tile_e; a.tile_off = h->d_tile_off; a.bperm = h->d_bperm;
   a.rows_per_lane = h->rows_per_lane;
+  a.min_blocks = h->min_blocks;
   a.dv = h->d_dv; a.dcnt = h->d_dcnt;
   int bps = search_max_blocks_per_sm(a);
   if (bps < 1) return fail(ALP_ECUDA, "search kernel cannot be resident (smem %d B)", a.smem_bytes);
@@ -611,9 +627,14 @@ alp_status alp_build(const alp_desc *d, alp_t **out) {
   for (int c = 0; c < C; ++c) h->tmax[c] = d->tmax ? d->tmax[c] : d->rate[d->prof_off[c + 1] - 1];
   if (d->min_units) h->min_units.assign(d->min_units, d->min_units + C);
   compute_units(h);
+  Trace tr;
+  tr.mark("validate");
   alp_status s = init_device(h);
+  tr.mark("init_device");
   if (s == ALP_OK) s = make_plan(h);
+  tr.mark("make_plan");
   if (s == ALP_OK) s = upload_all(h);
+  tr.mark("upload");
   if (s != ALP_OK) {
     delete h;
     return s;

@@ -60,6 +60,7 @@ struct SearchArgs {
   const uint32_t *tile_e;// [n_tiles][T] packed sort-group digits (kDummy = padding)
   const uint32_t *tile_off;// [n_tiles][T][2] smem byte offsets of the row's sort-group terms (4 x 16 bit)
   int rows_per_lane;     // T (8 or 16)
+  int min_blocks;        // launch-bounds variant for T = 8 (3 or 4 blocks/SM)
   const int *bperm;      // [Kb] canonical option of u-sorted column j
   const int *dv;         // [Dall] distinct b unit values, ascending
   const int *dcnt;       // [Dall+1] dcnt[i] = #u-sorted columns with u <= dv[i-1] (dcnt[0] = 0)

@@ -374,8 +374,9 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
 }
 
-template <int T, int NB4, bool TAIL2>
-__global__ void __launch_bounds__(kThreads, T >= 16 ? 2 : 3)
+// T = rows per lane; MB = minimum resident blocks per SM (register budget 65536 / (256 * MB)).
+template <int T, int NB4, bool TAIL2, int MB>
+__global__ void __launch_bounds__(kThreads, MB)
     k_search(const __grid_constant__ SearchArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
@@ -417,8 +418,17 @@ __global__ void __launch_bounds__(kThreads, T >= 16 ? 2 : 3)
 
 // Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
 template <int T, int NB4, bool TAIL2>
+static auto pick(const SearchArgs &a) {
+  auto fn = k_search<T, NB4, TAIL2, T >= 16 ? 2 : 3>;
+  if constexpr (T == 8) {
+    if (a.min_blocks == 4) fn = k_search<T, NB4, TAIL2, 4>;
+  }
+  return fn;
+}
+
+template <int T, int NB4, bool TAIL2>
 static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
-  auto fn = k_search<T, NB4, TAIL2>;
+  auto fn = pick<T, NB4, TAIL2>(a);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
   if (e != cudaSuccess) return e;
   fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
@@ -427,7 +437,7 @@ static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
 
 template <int T, int NB4, bool TAIL2>
 static int occ_one(const SearchArgs &a) {
-  auto fn = k_search<T, NB4, TAIL2>;
+  auto fn = pick<T, NB4, TAIL2>(a);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, a.smem_bytes) != cudaSuccess) return 0;
