@@ -146,6 +146,11 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
 float alp_last_kernel_ms(const alp_t *h);
 int32_t alp_last_launches(const alp_t *h);
 
+/* Static search plans (sort-list tiles, u-sorted columns; they depend only on the grids) are cached
+ * process-wide and shared by handles built on the same device with the same grids.  This drops the
+ * cache (plans still referenced by live handles stay alive until those handles are destroyed). */
+void alp_plan_cache_clear(void);
+
 /* Thread-local message for the last error (never NULL). */
 const char *alp_last_error(void);
 

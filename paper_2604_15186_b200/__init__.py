@@ -50,7 +50,8 @@ class _Result(ctypes.Structure):
 
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
-           "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_error"]
+           "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_error",
+           "alp_plan_cache_clear"]
 
 _lib = None
 
@@ -74,7 +75,7 @@ def lib():
             "alp_search_shard": (i32, [vp, vp, i32, i64, u64, u64, vp, vp, vp]),
             "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp]),
             "alp_last_kernel_ms": (ctypes.c_float, [vp]), "alp_last_launches": (i32, [vp]),
-            "alp_last_error": (ctypes.c_char_p, []),
+            "alp_last_error": (ctypes.c_char_p, []), "alp_plan_cache_clear": (None, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -82,6 +83,11 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def plan_cache_clear() -> None:
+    """alp_plan_cache_clear: drop the process-wide cache of static search plans."""
+    lib().alp_plan_cache_clear()
 
 
 def _check(st: int, ok=(ALP_OK,)) -> int:

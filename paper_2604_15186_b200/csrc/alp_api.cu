@@ -11,6 +11,9 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -78,10 +81,29 @@ struct Arena {
     total = off + count * sizeof(T);
     fix.push_back({off, reinterpret_cast<void **>(dptr)});
   }
-  cudaError_t commit(void **base, uint64_t &h2d) {
+  // H2D through a process-wide pinned staging buffer (one cudaMemcpyAsync; synchronises `st`).
+  cudaError_t commit(void **base, uint64_t &h2d, cudaStream_t st) {
+    static std::mutex mu;
+    static void *pinned = nullptr;
+    static size_t pinned_bytes = 0;
     cudaError_t e = cudaMalloc(base, total ? total : 1);
     if (e != cudaSuccess) return e;
-    if (copied) e = cudaMemcpy(*base, host.data(), copied, cudaMemcpyHostToDevice);
+    if (copied) {
+      std::lock_guard<std::mutex> lock(mu);
+      if (pinned_bytes < copied) {
+        if (pinned) cudaFreeHost(pinned);
+        pinned_bytes = std::max(copied, pinned_bytes * 2);
+        e = cudaHostAlloc(&pinned, pinned_bytes, cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+          pinned = nullptr;
+          pinned_bytes = 0;
+          return e;
+        }
+      }
+      memcpy(pinned, host.data(), copied);
+      e = cudaMemcpyAsync(*base, pinned, copied, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
     h2d += copied;
     for (auto &f : fix) *f.second = static_cast<unsigned char *>(*base) + f.first;
     return e;
@@ -108,6 +130,19 @@ int ceil_log2(int k) {
 
 }  // namespace
 
+// Device copy of a static search plan (sort-list tiles, u-sorted b columns, units).  The plan depends
+// only on the grids (units table), rows per lane and the device, so handles with the same key share it.
+struct PlanDev {
+  void *mem = nullptr;
+  int device = 0;
+  ~PlanDev() {
+    if (mem) {
+      cudaSetDevice(device);
+      cudaFree(mem);
+    }
+  }
+};
+
 struct alp_s {
   // problem
   int M = 0, F = 1, nS = 0, nT = 0, nR = 0, K = 0;
@@ -130,6 +165,7 @@ struct alp_s {
   long long umax_total = 0;
   // device
   int device = 0, sm_count = 148;
+  std::shared_ptr<PlanDev> plan_dev;  // shared static plan tables
   void *d_arena = nullptr;  // every static table + single-target scratch (one allocation)
   double *d_n = nullptr, *d_p = nullptr, *d_rate = nullptr, *d_lat = nullptr, *d_tmax = nullptr;
   int *d_S = nullptr, *d_T = nullptr, *d_R = nullptr, *d_off = nullptr, *d_minu = nullptr, *d_u = nullptr;
@@ -304,9 +340,9 @@ alp_status make_plan(alp_s *h) {
     for (int k = 0; k < K; ++k) mx = std::max(mx, U(m, k));
     h->umax_total += mx;
   }
-  // a-ranges: enough equal-cost work items for ~48 items per resident warp (load balance); a warp
+  // a-ranges: enough equal-cost work items for ~24 items per resident warp (load balance); a warp
   // keeps its lane tile across consecutive a-ranges, so small ranges cost little.
-  const uint64_t want = (uint64_t)h->sm_count * 24 * 48;
+  const uint64_t want = (uint64_t)h->sm_count * 24 * 24;
   uint32_t nQ = 1;
   while ((uint64_t)h->n_chunks * h->n_groups * nQ < want && nQ < (uint32_t)h->Ka) ++nQ;
   h->A = (uint32_t)((h->Ka + nQ - 1) / nQ);
@@ -319,8 +355,81 @@ alp_status make_plan(alp_s *h) {
   return ALP_OK;
 }
 
-// Stage every static table of the handle (+ single-target scratch) into one device allocation.
+// Snapshot of a built plan (everything make_plan produces that the searches need).
+struct PlanSnap {
+  uint64_t N;
+  int a_llm, b_llm, Ka, Kb, g0, g1, ng, dig_bits, umax_a, umax_b;
+  uint32_t L, n_chunks, n_groups, nQ, A;
+  uint32_t pw[ALP_MAX_M];
+  long long umax_total;
+  std::vector<int> dv;
+  int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt;
+  uint32_t *d_tile_e, *d_tile_off;
+  std::shared_ptr<PlanDev> dev;
+};
+
+std::mutex g_plan_mu;
+std::map<std::string, std::shared_ptr<PlanSnap>> g_plans;
+
+std::string plan_key(const alp_s *h) {
+  std::string k;
+  auto put = [&](const void *p, size_t n) { k.append(static_cast<const char *>(p), n); };
+  const int hdr[5] = {h->device, h->sm_count, h->M, h->K, h->rows_per_lane};
+  put(hdr, sizeof(hdr));
+  put(h->u.data(), h->u.size() * sizeof(int));
+  return k;
+}
+
+alp_status make_plan(alp_s *h);
+
+// Build (or fetch from the process-wide cache) the static plan and its device tables.
+alp_status get_plan(alp_s *h) {
+  const std::string key = plan_key(h);
+  std::lock_guard<std::mutex> lock(g_plan_mu);
+  auto it = g_plans.find(key);
+  std::shared_ptr<PlanSnap> P;
+  if (it != g_plans.end()) {
+    P = it->second;
+  } else {
+    alp_status s = make_plan(h);
+    if (s != ALP_OK) return s;
+    P = std::make_shared<PlanSnap>();
+    P->dev = std::make_shared<PlanDev>();
+    P->dev->device = h->device;
+    Arena A;
+    A.add(h->u, &P->d_u);
+    A.add(h->tile_s, &P->d_tile_s);
+    A.add(h->tile_e, &P->d_tile_e);
+    A.add(h->tile_off, &P->d_tile_off);
+    A.add(h->bperm, &P->d_bperm);
+    A.add(h->dv, &P->d_dv);
+    A.add(h->dcnt, &P->d_dcnt);
+    CU(A.commit(&P->dev->mem, h->h2d, h->stream));
+    P->N = h->N; P->a_llm = h->a_llm; P->b_llm = h->b_llm; P->Ka = h->Ka; P->Kb = h->Kb; P->g0 = h->g0;
+    P->g1 = h->g1; P->ng = h->ng; P->dig_bits = h->dig_bits; P->umax_a = h->umax_a; P->umax_b = h->umax_b;
+    P->L = h->L; P->n_chunks = h->n_chunks; P->n_groups = h->n_groups; P->nQ = h->nQ; P->A = h->A;
+    memcpy(P->pw, h->pw, sizeof(P->pw));
+    P->umax_total = h->umax_total;
+    P->dv = h->dv;
+    g_plans[key] = P;
+    h->tile_s.clear(); h->tile_e.clear(); h->tile_off.clear(); h->bperm.clear(); h->bu.clear(); h->dcnt.clear();
+  }
+  h->N = P->N; h->a_llm = P->a_llm; h->b_llm = P->b_llm; h->Ka = P->Ka; h->Kb = P->Kb; h->g0 = P->g0;
+  h->g1 = P->g1; h->ng = P->ng; h->dig_bits = P->dig_bits; h->umax_a = P->umax_a; h->umax_b = P->umax_b;
+  h->L = P->L; h->n_chunks = P->n_chunks; h->n_groups = P->n_groups; h->nQ = P->nQ; h->A = P->A;
+  memcpy(h->pw, P->pw, sizeof(h->pw));
+  h->umax_total = P->umax_total;
+  h->dv = P->dv;
+  h->d_u = P->d_u; h->d_tile_s = P->d_tile_s; h->d_tile_e = P->d_tile_e; h->d_tile_off = P->d_tile_off;
+  h->d_bperm = P->d_bperm; h->d_dv = P->d_dv; h->d_dcnt = P->d_dcnt;
+  h->plan_dev = P->dev;
+  return ALP_OK;
+}
+
+// Stage the handle's own tables (profiles or injected terms) + single-target scratch in one allocation.
 alp_status upload_all(alp_s *h) {
+  alp_status s = get_plan(h);
+  if (s != ALP_OK) return s;
   Arena A;
   const size_t MK = (size_t)h->M * h->K;
   if (h->from_terms) {
@@ -339,13 +448,6 @@ alp_status upload_all(alp_s *h) {
   }
   A.add(h->T, &h->d_T);
   A.add(h->R, &h->d_R);
-  A.add(h->u, &h->d_u);
-  A.add(h->tile_s, &h->d_tile_s);
-  A.add(h->tile_e, &h->d_tile_e);
-  A.add(h->tile_off, &h->d_tile_off);
-  A.add(h->bperm, &h->d_bperm);
-  A.add(h->dv, &h->d_dv);
-  A.add(h->dcnt, &h->d_dcnt);
   A.scratch(1, &h->a_targets);
   A.scratch(MK, &h->a_tau);
   A.scratch(MK, &h->a_term);
@@ -353,7 +455,7 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_res);
   A.scratch(1, &h->a_keys);
   A.scratch(1, &h->a_counts);
-  CU(A.commit(&h->d_arena, h->h2d));
+  CU(A.commit(&h->d_arena, h->h2d, h->stream));
   return ALP_OK;
 }
 
@@ -631,10 +733,8 @@ alp_status alp_build(const alp_desc *d, alp_t **out) {
   tr.mark("validate");
   alp_status s = init_device(h);
   tr.mark("init_device");
-  if (s == ALP_OK) s = make_plan(h);
-  tr.mark("make_plan");
   if (s == ALP_OK) s = upload_all(h);
-  tr.mark("upload");
+  tr.mark("plan+upload");
   if (s != ALP_OK) {
     delete h;
     return s;
@@ -674,7 +774,6 @@ alp_status alp_build_from_terms(int32_t M, int32_t K, const float *tau, const in
   h->R.resize(K);
   std::iota(h->R.begin(), h->R.end(), 1);
   alp_status s = init_device(h);
-  if (s == ALP_OK) s = make_plan(h);
   if (s == ALP_OK) s = upload_all(h);
   if (s != ALP_OK) {
     delete h;
@@ -823,5 +922,10 @@ float alp_last_kernel_ms(const alp_t *h) {
 }
 
 int32_t alp_last_launches(const alp_t *h) { return h ? h->last_launches : 0; }
+
+void alp_plan_cache_clear(void) {
+  std::lock_guard<std::mutex> lock(g_plan_mu);
+  g_plans.clear();
+}
 
 }  // extern "C"

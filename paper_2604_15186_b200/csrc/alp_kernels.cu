@@ -131,7 +131,7 @@ struct Smem {
   float *tau;      // [g1*K + 2] tau of prefix + sort-group LLMs (current target), then {0, +inf}; offset 0
   int *u;          // [g0*K] units of prefix LLMs
   float2 *a;       // [Ka] {tau_a, bits(-u_a)}; u_a := kBigUnits when tau_a is +inf
-  int2 *lut;       // [R+2] {byte offset of the masked row, #finite entries in it} for r = -1..R
+  int2 *lut;       // [R+2] {shared address of the masked row, #finite entries in it} for r = -1..R
   int *dv;         // [D] distinct b unit values <= R, ascending
   int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
   float *btab;     // [rows][row_stride] masked rows
@@ -200,10 +200,21 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
       const int mid = (lo + hi) >> 1;
       if (s.dv[mid] <= r) lo = mid + 1; else hi = mid;
     }
-    s.lut[r + 1] = make_int2(P.off_btab + lo * P.row_stride * 4,
+    s.lut[r + 1] = make_int2((int)(uint32_t)__cvta_generic_to_shared(s.btab + lo * P.row_stride),
                              __float_as_int(s.btab[lo * P.row_stride + P.bchunk_wpad]));
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 lds64(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
 }
 
 // "candidate = Q_a + tau_b; acc = min(acc, candidate)" for 4 b values and T rows:
@@ -240,15 +251,15 @@ __device__ __forceinline__ void eval2(const float2 bv, const float (&Qa)[T], flo
 }
 
 template <int T, int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row(const unsigned char *rp, const float (&Qa)[T], float (&acc)[T], int ng4) {
+__device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], float (&acc)[T], int ng4) {
   if constexpr (NB4 > 0) {
 #pragma unroll
-    for (int g = 0; g < NB4; ++g) eval4<T>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
+    for (int g = 0; g < NB4; ++g) eval4<T>(lds128(rp + 16 * g), Qa, acc);
   } else {
 #pragma unroll 2
-    for (int g = 0; g < ng4; ++g) eval4<T>(*reinterpret_cast<const float4 *>(rp + 16 * g), Qa, acc);
+    for (int g = 0; g < ng4; ++g) eval4<T>(lds128(rp + 16 * g), Qa, acc);
   }
-  if constexpr (TAIL2) eval2<T>(*reinterpret_cast<const float2 *>(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
+  if constexpr (TAIL2) eval2<T>(lds64(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
 }
 
 // Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
@@ -348,16 +359,17 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     unsigned c32 = 0;
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
+    const float2 *ap = s.a + a0;
 #pragma unroll 1
-    for (int a = a0; a < a1; ++a) {
-      const float2 av = s.a[a];
+    for (int a = a0; a < a1; ++a, ++ap) {
+      const float2 av = *ap;
       const int ra = max(r_tile + __float_as_int(av.y), -1);
       const int2 lu = s.lut[ra + 1];
       c32 += (unsigned)lu.y;
       float Qa[T];
 #pragma unroll
       for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-      eval_row<T, NB4, TAIL2>(base + lu.x, Qa, acc, ng4);
+      eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
     }
     cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
     // advance to the next item (q fastest); fold when the lane tile changes

@@ -289,3 +289,20 @@ def test_decode_roundtrip(P):
     alp = P.Alp.from_instance(d)
     for idx in [0, 1, I.N - 1, 123456789, 9725594165]:
         assert alp.decode(idx) == [oracle.option_grid(I, k) for k in oracle.decode(I, idx)]
+
+
+def test_plan_cache_shared_and_cleared(P):
+    d = generate.load("C4")
+    lam = d["targets"][0]
+    a1 = P.Alp.from_instance(d)
+    r1 = a1.search(lam, d["budget_units"])
+    a2 = P.Alp.from_instance(d)  # plan cache hit: only the profile tables are uploaded
+    assert a2.h2d_bytes < a1.h2d_bytes or a1.h2d_bytes < 200_000
+    P.plan_cache_clear()
+    a3 = P.Alp.from_instance(d)  # rebuilt plan
+    for a in (a2, a3):
+        r = a.search(lam, d["budget_units"])
+        assert (r.index, r.feasible_count, r.latency_key) == (r1.index, r1.feasible_count, r1.latency_key)
+    a1.close()
+    r = a2.search(lam, d["budget_units"])  # a2 keeps its (now uncached) plan alive
+    assert r.index == r1.index
