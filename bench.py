@@ -164,10 +164,17 @@ def run_ours(args):
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
+    # one rank per GPU; ALP_DIST_BACKEND=gloo lets several ranks share one GPU (test only: NCCL
+    # rejects duplicate devices), the product path is NCCL over NVLink.
+    backend = os.environ.get("ALP_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2604_15186_b200 import build as pbuild
     if rank == 0 or world == 1:
         pbuild.build()

@@ -19,7 +19,7 @@ from typing import Any, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libscepsy_alp.so")
+LIB_PATH = os.environ.get("ALP_LIB") or os.path.join(HERE, "lib", "libscepsy_alp.so")  # ALP_LIB: tuning builds
 MAX_M = 16
 PCT = {"mean": 0, "p50": 1, "p90": 2, "p99": 3}
 

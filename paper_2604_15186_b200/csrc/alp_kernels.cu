@@ -28,7 +28,13 @@
 
 #include "alp_internal.h"
 
+#ifndef ALP_A_UNROLL
+#define ALP_A_UNROLL 1  // a-loop unroll (1 keeps the hot loop inside the L0 I-cache)
+#endif
+
 namespace alp {
+
+constexpr int kAUnroll = ALP_A_UNROLL;
 
 __device__ __forceinline__ float finf() { return __int_as_float(0x7f800000); }
 
@@ -360,7 +366,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
     const float2 *ap = s.a + a0;
-#pragma unroll 1
+#pragma unroll(kAUnroll)
     for (int a = a0; a < a1; ++a, ++ap) {
       const float2 av = *ap;
       const int ra = max(r_tile + __float_as_int(av.y), -1);
