@@ -460,6 +460,9 @@ alp_status upload_all(alp_s *h) {
 }
 
 alp_status init_device(alp_s *h) {
+  // rows per lane: 16 when the b rows are long (more candidates per lane tile), else 8 (tuned on
+  // C3 / C4, profiles/r01_variant_sweep.txt); ALP_ROWS_PER_LANE overrides.
+  h->rows_per_lane = (h->K >= 64) ? 16 : 8;
   if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 16) ? 16 : 8;
   if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = (atoi(v) == 4) ? 4 : 3;
   CU(cudaGetDevice(&h->device));

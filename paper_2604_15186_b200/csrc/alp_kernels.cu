@@ -29,7 +29,7 @@
 #include "alp_internal.h"
 
 #ifndef ALP_A_UNROLL
-#define ALP_A_UNROLL 1  // a-loop unroll (1 keeps the hot loop inside the L0 I-cache)
+#define ALP_A_UNROLL 2  // a-loop unroll (tuned: 2 beats 1 on C3 and C4, profiles/r01_variant_sweep.txt)
 #endif
 
 namespace alp {
