@@ -145,6 +145,36 @@ struct Smem {
 
 constexpr int kBigUnits = 1 << 28;
 
+// Constant-bank copy of one phase's tables for the warp-uniform path (see process_items): with all
+// 32 lanes on the same masked row, the b values are read with uniform addresses (LDCU) into uniform
+// registers, so FADD2 takes b from the uniform datapath instead of the vector register file.
+// Layout (32-bit words): [0, 2*Ka) a-table {tau_a bits, -u_a}; [cu_off_lut, +2*(R+2)) {row word
+// offset, #finite} for r = -1..R; [cu_off_btab, ...) masked rows (row_stride words each).
+constexpr int kConstWords = 16384;  // 64 KB
+__constant__ uint32_t c_mem[kConstWords];
+
+// a-table entry for option a (infeasible a gets +inf units -> maps to the all-+inf row)
+__device__ __forceinline__ float2 a_entry(const SearchArgs &P, const float *tau_t, int a) {
+  if (P.a_llm < 0) return make_float2(0.f, __int_as_float(0));
+  const float ta = tau_t[P.a_llm * P.K + a];
+  return make_float2(ta, __int_as_float(ta < __int_as_float(0x7f800000) ? -P.u[P.a_llm * P.K + a] : -kBigUnits));
+}
+// masked-row element (row, j) of b-chunk [c0, c1): tau_b of the j-th u-sorted column if it fits
+__device__ __forceinline__ float btab_entry(const SearchArgs &P, const float *tau_t, const int *dcnt, int row, int j,
+                                            int c0, int c1) {
+  const int len = min(max(dcnt[row], c0), c1) - c0;
+  return (j < len) ? tau_t[P.b_llm * P.K + P.bperm[c0 + j]] : __int_as_float(0x7f800000);
+}
+// masked-row index for remaining budget r: #{distinct b unit values <= r}
+__device__ __forceinline__ int row_of(const int *dv, int D, int r) {
+  int lo = 0, hi = D;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (dv[mid] <= r) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
   Smem s;
   s.tau = reinterpret_cast<float *>(base + P.off_tau);
@@ -170,24 +200,15 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
     s.tau[P.g1 * K + 1] = finf();  // padded (dummy) row
   }
   for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
-  for (int a = tid; a < P.Ka; a += nt) {
-    float2 v = make_float2(0.f, __int_as_float(0));
-    if (P.a_llm >= 0) {
-      const float ta = tau_t[P.a_llm * K + a];
-      v = make_float2(ta, __int_as_float(ta < finf() ? -P.u[P.a_llm * K + a] : -kBigUnits));
-    }
-    s.a[a] = v;
-  }
+  for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, a);
   for (int i = tid; i < D; i += nt) s.dv[i] = P.dv[i];
   for (int i = tid; i <= D; i += nt) s.dcnt[i] = P.dcnt[i];
   __syncthreads();
   // masked row i holds the u-sorted columns [c0, c1) with u <= dv[i-1] (row 0: none), +inf elsewhere
   const int rows = D + 1;
-  const float *tau_b = tau_t + P.b_llm * K;
   for (int i = tid; i < rows * P.bchunk_wpad; i += nt) {
     const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
-    const int len = min(max(s.dcnt[row], c0), c1) - c0;
-    s.btab[row * P.row_stride + j] = (j < len) ? tau_b[P.bperm[c0 + j]] : finf();
+    s.btab[row * P.row_stride + j] = btab_entry(P, tau_t, s.dcnt, row, j, c0, c1);
   }
   __syncthreads();
   // finite entries per masked row (feasible b count), kept in the row's padding column
@@ -201,11 +222,7 @@ __device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
   __syncthreads();
   // r -> masked row: index = #{distinct b unit values <= r}
   for (int r = tid - 1; r <= R; r += nt) {
-    int lo = 0, hi = D;  // upper_bound(dv, r)
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s.dv[mid] <= r) lo = mid + 1; else hi = mid;
-    }
+    const int lo = row_of(s.dv, D, r);
     s.lut[r + 1] = make_int2((int)(uint32_t)__cvta_generic_to_shared(s.btab + lo * P.row_stride),
                              __float_as_int(s.btab[lo * P.row_stride + P.bchunk_wpad]));
   }
@@ -266,6 +283,64 @@ __device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], floa
     for (int g = 0; g < ng4; ++g) eval4<T>(lds128(rp + 16 * g), Qa, acc);
   }
   if constexpr (TAIL2) eval2<T>(lds64(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
+}
+
+// Warp-uniform variant of eval_row: the masked row lives in the constant bank at word offset
+// `row` (uniform), so every b value is an LDCU into a uniform register.
+template <int T, int NB4, bool TAIL2>
+__device__ __forceinline__ void eval_row_c(uint32_t row, const float (&Qa)[T], float (&acc)[T], int ng4) {
+  if constexpr (NB4 > 0) {
+#pragma unroll
+    for (int g = 0; g < NB4; ++g) {
+      const uint32_t o = row + 4 * g;
+      eval4<T>(make_float4(__uint_as_float(c_mem[o]), __uint_as_float(c_mem[o + 1]), __uint_as_float(c_mem[o + 2]),
+                           __uint_as_float(c_mem[o + 3])), Qa, acc);
+    }
+  } else {
+#pragma unroll 2
+    for (int g = 0; g < ng4; ++g) {
+      const uint32_t o = row + 4 * g;
+      eval4<T>(make_float4(__uint_as_float(c_mem[o]), __uint_as_float(c_mem[o + 1]), __uint_as_float(c_mem[o + 2]),
+                           __uint_as_float(c_mem[o + 3])), Qa, acc);
+    }
+  }
+  if constexpr (TAIL2) {
+    const uint32_t o = row + (NB4 > 0 ? NB4 : ng4) * 4;
+    eval2<T>(make_float2(__uint_as_float(c_mem[o]), __uint_as_float(c_mem[o + 1])), Qa, acc);
+  }
+}
+
+// Builds one phase's constant-bank tables (layout above) into a global buffer; the host copies it
+// into c_mem (cudaMemcpyToSymbolAsync, device to device) before the phase's k_search launch.
+__global__ void k_const_tables(const __grid_constant__ SearchArgs P, int t, int c, uint32_t *out) {
+  __shared__ unsigned rowcnt[ALP_MAX_K + 1];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const float *tau_t = P.tau + (size_t)t * P.M * P.K;
+  const int c0 = c * P.bchunk_w, c1 = min(c0 + P.bchunk_w, P.Kb);
+  const int rows = P.D + 1;
+  for (int a = tid; a < P.Ka; a += nt) {
+    const float2 v = a_entry(P, tau_t, a);
+    out[2 * a] = __float_as_uint(v.x);
+    out[2 * a + 1] = __float_as_uint(v.y);
+  }
+  for (int i = tid; i < rows * P.row_stride; i += nt) {
+    const int row = i / P.row_stride, j = i % P.row_stride;
+    out[P.cu_off_btab + i] = __float_as_uint(j < P.bchunk_wpad ? btab_entry(P, tau_t, P.dcnt, row, j, c0, c1) : 0.f);
+  }
+  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+  for (int row = warp; row < rows; row += nwarp) {
+    unsigned n = 0;
+    for (int j = lane; j < P.bchunk_wpad; j += 32)
+      n += (btab_entry(P, tau_t, P.dcnt, row, j, c0, c1) < finf()) ? 1u : 0u;
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0) rowcnt[row] = n;
+  }
+  __syncthreads();
+  for (int r = tid - 1; r <= P.budget; r += nt) {
+    const int row = row_of(P.dv, P.D, r);
+    out[P.cu_off_lut + 2 * (r + 1)] = (uint32_t)(P.cu_off_btab + row * P.row_stride);
+    out[P.cu_off_lut + 2 * (r + 1) + 1] = rowcnt[row];
+  }
 }
 
 // Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
@@ -365,17 +440,35 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     unsigned c32 = 0;
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
-    const float2 *ap = s.a + a0;
+    // warp-uniform lane tiles (every lane on the same remaining budget, or all over budget) take
+    // the constant-bank path; mixed tiles read their own masked rows from shared memory.
+    const int r0 = __shfl_sync(0xffffffffu, r_tile, 0);
+    if (P.uni && __all_sync(0xffffffffu, (r_tile == r0) || (r_tile < 0 && r0 < 0))) {
+      const int a0u = __shfl_sync(0xffffffffu, a0, 0), a1u = __shfl_sync(0xffffffffu, a1, 0);
 #pragma unroll(kAUnroll)
-    for (int a = a0; a < a1; ++a, ++ap) {
-      const float2 av = *ap;
-      const int ra = max(r_tile + __float_as_int(av.y), -1);
-      const int2 lu = s.lut[ra + 1];
-      c32 += (unsigned)lu.y;
-      float Qa[T];
+      for (int a = a0u; a < a1u; ++a) {
+        const float ta = __uint_as_float(c_mem[2 * a]);
+        const int ra = max(r0 + (int)c_mem[2 * a + 1], -1);
+        const uint32_t lrow = c_mem[P.cu_off_lut + 2 * (ra + 1)];
+        c32 += c_mem[P.cu_off_lut + 2 * (ra + 1) + 1];
+        float Qa[T];
 #pragma unroll
-      for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-      eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
+        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], ta);
+        eval_row_c<T, NB4, TAIL2>(lrow, Qa, acc, ng4);
+      }
+    } else {
+      const float2 *ap = s.a + a0;
+#pragma unroll(kAUnroll)
+      for (int a = a0; a < a1; ++a, ++ap) {
+        const float2 av = *ap;
+        const int ra = max(r_tile + __float_as_int(av.y), -1);
+        const int2 lu = s.lut[ra + 1];
+        c32 += (unsigned)lu.y;
+        float Qa[T];
+#pragma unroll
+        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+        eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
+      }
     }
     cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
     // advance to the next item (q fastest); fold when the lane tile changes
@@ -392,18 +485,20 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
 }
 
-// T = rows per lane; MB = minimum resident blocks per SM (register budget 65536 / (256 * MB)).
-template <int T, int NB4, bool TAIL2, int MB>
-__global__ void __launch_bounds__(kThreads, MB)
+// T = rows per lane.  Deliberately no minimum-blocks launch bound: any register cap (launch bounds
+// min blocks, -maxrregcount) stops ptxas from using the uniform datapath, which the warp-uniform
+// path needs (FADD2 with a uniform-register b operand); the natural allocation fits 3 blocks/SM.
+template <int T, int NB4, bool TAIL2>
+__global__ void __launch_bounds__(kThreads)
     k_search(const __grid_constant__ SearchArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
   const Smem s = smem_layout(P, smem);
-  for (int t = 0; t < P.n_targets; ++t) {
+  for (int t = P.t_begin; t < P.t_end; ++t) {
     float best = finf();
     uint32_t best_seg = 0xffffffffu;
     unsigned long long cnt = 0ull;
-    for (int c = 0; c < P.n_bchunks; ++c) {
+    for (int c = P.c_begin; c < P.c_end; ++c) {
       __syncthreads();
       build_tables(P, s, t, c);
       process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
@@ -437,11 +532,8 @@ __global__ void __launch_bounds__(kThreads, MB)
 // Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
 template <int T, int NB4, bool TAIL2>
 static auto pick(const SearchArgs &a) {
-  auto fn = k_search<T, NB4, TAIL2, T >= 16 ? 2 : 3>;
-  if constexpr (T == 8) {
-    if (a.min_blocks == 4) fn = k_search<T, NB4, TAIL2, 4>;
-  }
-  return fn;
+  (void)a;
+  return k_search<T, NB4, TAIL2>;
 }
 
 template <int T, int NB4, bool TAIL2>
@@ -491,6 +583,16 @@ static int occ_one(const SearchArgs &a) {
     if (a.rows_per_lane == 16) ALP_DISPATCH_W(CALL, 16); \
     ALP_DISPATCH_W(CALL, 8);                \
   } while (0)
+
+cudaError_t launch_const_tables(const SearchArgs &a, int t, int c, uint32_t *scratch, cudaStream_t st) {
+  k_const_tables<<<1, 256, 0, st>>>(a, t, c, scratch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t words = (size_t)a.cu_off_btab + (size_t)(a.D + 1) * a.row_stride;
+  return cudaMemcpyToSymbolAsync(c_mem, scratch, words * 4, 0, cudaMemcpyDeviceToDevice, st);
+}
+
+int const_words_max() { return kConstWords; }
 
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st) {
 #define CALL(T, N, T2) launch_one<T, N, T2>(a, grid, st)
