@@ -161,7 +161,7 @@ struct alp_s {
   std::vector<uint32_t> tile_e, tile_off;
   int rows_per_lane = 8;
   int min_blocks = 3;
-  int use_uniform = 1;  // ALP_UNIFORM=0 disables the constant-bank (warp-uniform) path
+  int use_uniform = 0;  // ALP_UNIFORM=1 enables the constant-bank (warp-uniform) path (measured slower, profiles/README.md)
   uint32_t *d_cscratch = nullptr;  // const_words_max() words: one phase's constant-bank tables
   int umax_a = 0, umax_b = 0;
   long long umax_total = 0;
