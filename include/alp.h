@@ -124,6 +124,23 @@ alp_status alp_search(alp_t *h, double target, int64_t budget_units, alp_result 
 /* Batched targets (Pareto sweep): out[n]. Returns ALP_OK if at least one target is feasible. */
 alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t budget_units, alp_result *out);
 
+/* Independent (target, budget) queries in one pass, out[n] — e.g. the best allocation of one
+ * workflow for every GPU count (the budget-indexed search behind multi-workflow scheduling,
+ * PAPER.md:396-398).  budgets[i] >= 0 units.  Returns ALP_OK if at least one query is feasible. */
+alp_status alp_search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n, alp_result *out);
+
+/* Multi-workflow allocation ("egalitarian welfare"; utility per SPEC.md:383):
+ * W workflows (handles hs[w], all built on one device, same units-per-GPU F) with targets[w]; the
+ * cluster has `gpus` GPUs of `units_per_gpu` units.  For each workflow the budget-indexed search
+ * gives L_w(g), the best FP64 latency on g = 0..gpus whole GPUs; utility u_w(g) = L_w(gpus)/L_w(g)
+ * (0 if infeasible).  Chooses the split g_0..g_{W-1} (sum = gpus) maximising min_w u_w, then
+ * sum_w u_w, then the lowest split index (g_0 most significant), in a device kernel.
+ * gpus_out[W] = GPUs per workflow; results_out[W] = each workflow's best allocation on its share;
+ * min/sum utility optional.  ALP_EINFEASIBLE if some workflow is infeasible on its share. */
+alp_status alp_schedule_egalitarian(alp_t *const *hs, const double *targets, int32_t W, int32_t gpus,
+                                    int32_t units_per_gpu, int32_t *gpus_out, alp_result *results_out,
+                                    double *min_utility, double *sum_utility);
+
 /* ---- multi-GPU building blocks (PyTorch owns memory, streams and the process group) ----
  * The candidate space is cut into equal-cost work items; rank r of world w gets the contiguous
  * item range [lo, hi).  Every rank calls alp_search_shard on its range (async on `stream`),

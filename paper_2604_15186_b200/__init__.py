@@ -51,7 +51,7 @@ class _Result(ctypes.Structure):
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
            "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_error",
-           "alp_plan_cache_clear"]
+           "alp_plan_cache_clear", "alp_search_queries", "alp_schedule_egalitarian"]
 
 _lib = None
 
@@ -76,6 +76,8 @@ def lib():
             "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp]),
             "alp_last_kernel_ms": (ctypes.c_float, [vp]), "alp_last_launches": (i32, [vp]),
             "alp_last_error": (ctypes.c_char_p, []), "alp_plan_cache_clear": (None, []),
+            "alp_search_queries": (i32, [vp, vp, vp, i32, vp]),
+            "alp_schedule_egalitarian": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -88,6 +90,21 @@ def lib():
 def plan_cache_clear() -> None:
     """alp_plan_cache_clear: drop the process-wide cache of static search plans."""
     lib().alp_plan_cache_clear()
+
+
+def schedule_egalitarian(alps: Sequence["Alp"], targets: Sequence[float], gpus: int, units_per_gpu: int):
+    """alp_schedule_egalitarian: split `gpus` whole GPUs across workflows (max-min utility).
+    Returns (gpus per workflow, per-workflow Result, min utility, sum utility)."""
+    W = len(alps)
+    hs = (ctypes.c_void_p * W)(*[a._h.value for a in alps])
+    t = _arr(targets, np.float64)
+    g = np.zeros(W, np.int32)
+    out = (_Result * W)()
+    mn = ctypes.c_double()
+    sm = ctypes.c_double()
+    _check(lib().alp_schedule_egalitarian(hs, t.ctypes.data, W, gpus, units_per_gpu, g.ctypes.data, out,
+                                          ctypes.byref(mn), ctypes.byref(sm)), (ALP_OK, ALP_EINFEASIBLE))
+    return g.tolist(), [Result._from(x) for x in out], mn.value, sm.value
 
 
 def _check(st: int, ok=(ALP_OK,)) -> int:
@@ -238,6 +255,16 @@ class Alp:
         t = _arr(targets, np.float64)
         out = (_Result * len(t))()
         _check(lib().alp_search_batch(self._h, t.ctypes.data, len(t), budget, out), (ALP_OK, ALP_EINFEASIBLE))
+        return [Result._from(x) for x in out]
+
+    def search_queries(self, targets: Sequence[float], budgets: Sequence[int]) -> list[Result]:
+        """alp_search_queries: independent (target, budget) pairs in one pass."""
+        t = _arr(targets, np.float64)
+        bu = _arr(budgets, np.int64)
+        if len(t) != len(bu):
+            raise ValueError("targets and budgets differ in length")
+        out = (_Result * len(t))()
+        _check(lib().alp_search_queries(self._h, t.ctypes.data, bu.ctypes.data, len(t), out), (ALP_OK, ALP_EINFEASIBLE))
         return [Result._from(x) for x in out]
 
     def num_items(self, budget: int) -> int:

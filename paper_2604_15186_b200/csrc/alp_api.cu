@@ -184,6 +184,9 @@ struct alp_s {
   DBuf<float> g_tau;
   DBuf<alp_result> g_res;
   DBuf<unsigned long long> g_keys, g_counts;
+  int *a_qb = nullptr;
+  DBuf<int> g_qb;
+  int *s_qb = nullptr;  // per-query budgets (device) when the last search used them, else nullptr
   double *s_targets = nullptr, *s_term = nullptr, *s_b = nullptr;
   float *s_tau = nullptr;
   alp_result *s_res = nullptr;
@@ -210,7 +213,7 @@ struct alp_s {
 
   ~alp_s() {
     for (auto *b : {&g_targets, &g_term, &g_b, &d_plat, &d_pthr}) b->release();
-    for (auto *b : {&d_opts, &d_pfeas}) b->release();
+    for (auto *b : {&d_opts, &d_pfeas, &g_qb}) b->release();
     g_tau.release();
     g_res.release();
     g_keys.release();
@@ -457,6 +460,7 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_res);
   A.scratch(1, &h->a_keys);
   A.scratch(1, &h->a_counts);
+  A.scratch(1, &h->a_qb);
   A.scratch((size_t)const_words_max(), &h->d_cscratch);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
   return ALP_OK;
@@ -606,21 +610,49 @@ alp_status check_targets(const double *targets, int n) {
   return ALP_OK;
 }
 
-alp_status search_shard_impl(alp_s *h, const double *targets, int n, int64_t budget, uint64_t lo, uint64_t hi,
-                             cudaStream_t st, unsigned long long *keys, unsigned long long *counts) {
+// Per-query budgets: validated, capped at the total max units (never binding above it) and uploaded.
+// Returns the largest (capped) budget, which sizes the shared-memory tables.
+alp_status prepare_budgets(alp_s *h, const int64_t *budgets, int n, cudaStream_t st, int64_t *rmax) {
+  h->s_qb = nullptr;
+  if (!budgets) return ALP_OK;
+  std::vector<int> qb(n);
+  int64_t mx = 0;
+  for (int i = 0; i < n; ++i) {
+    if (budgets[i] < 0) return fail(ALP_EINVAL, "budgets[%d] < 0", i);
+    qb[i] = (int)std::min<int64_t>(budgets[i], h->umax_total);
+    mx = std::max<int64_t>(mx, budgets[i]);
+  }
+  if (n <= 1) {
+    h->s_qb = h->a_qb;
+  } else {
+    CU(h->g_qb.ensure(n));
+    h->s_qb = h->g_qb.p;
+  }
+  CU(cudaMemcpyAsync(h->s_qb, qb.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));  // qb is a host temporary
+  *rmax = mx;
+  return ALP_OK;
+}
+
+alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
+                             uint64_t lo, uint64_t hi, cudaStream_t st, unsigned long long *keys,
+                             unsigned long long *counts) {
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
+  s = ensure_scratch(h, n);
+  if (s != ALP_OK) return s;
+  s = prepare_budgets(h, budgets, n, st, &budget);
+  if (s != ALP_OK) return s;
   Geometry g;
   s = make_geometry(h, n, budget, 0, 0, g);
   if (s != ALP_OK) return s;
   const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
   if (lo > hi || hi > items) return fail(ALP_EINVAL, "item range [%llu, %llu) outside [0, %llu)",
                                          (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)items);
-  s = ensure_scratch(h, n);
-  if (s != ALP_OK) return s;
   s = option_tables(h, targets, n, st, keys, counts);
   if (s != ALP_OK) return s;
+  g.a.q_budget = h->s_qb;
   g.a.item_lo = lo;
   g.a.item_hi = hi;
   g.a.tau = h->s_tau;
@@ -661,19 +693,27 @@ alp_status search_shard_impl(alp_s *h, const double *targets, int n, int64_t bud
   return ALP_OK;
 }
 
-alp_status finalize_impl(alp_s *h, const double *targets, int n, int64_t budget, const unsigned long long *keys,
-                         const unsigned long long *counts, cudaStream_t st, alp_result *out) {
+alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
+                         const unsigned long long *keys, const unsigned long long *counts, cudaStream_t st,
+                         alp_result *out) {
   if (!out) return fail(ALP_EINVAL, "out is NULL");
   CU(cudaSetDevice(h->device));
-  Geometry g;
-  alp_status s = make_geometry(h, n, budget, 0, 0, g);
+  alp_status s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
-  s = ensure_scratch(h, n);
+  if (budgets) {
+    s = prepare_budgets(h, budgets, n, st, &budget);
+    if (s != ALP_OK) return s;
+  } else {
+    h->s_qb = nullptr;
+  }
+  Geometry g;
+  s = make_geometry(h, n, budget, 0, 0, g);
   if (s != ALP_OK) return s;
   // option tables must describe these targets (the shard call computed them on this handle)
   (void)targets;
   FinalizeArgs f;
   f.s = g.a;
+  f.s.q_budget = h->s_qb;
   f.s.tau = h->s_tau;
   f.term = h->s_term;
   f.b = h->s_b;
@@ -917,7 +957,7 @@ alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t 
                             uint64_t hi, void *stream, int64_t *d_keys, int64_t *d_counts) {
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
-  return search_shard_impl(h, targets, n, budget_units, lo, hi, stream ? (cudaStream_t)stream : h->stream,
+  return search_shard_impl(h, targets, nullptr, n, budget_units, lo, hi, stream ? (cudaStream_t)stream : h->stream,
                            reinterpret_cast<unsigned long long *>(d_keys),
                            reinterpret_cast<unsigned long long *>(d_counts));
 }
@@ -928,12 +968,13 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
-  return finalize_impl(h, targets, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
+  return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
                        reinterpret_cast<const unsigned long long *>(d_counts),
                        stream ? (cudaStream_t)stream : h->stream, out);
 }
 
-alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t budget_units, alp_result *out) {
+static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
+                                 int64_t budget_units, alp_result *out) {
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
@@ -941,13 +982,83 @@ alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t 
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   const uint64_t items = alp_num_items(h, budget_units);
-  s = search_shard_impl(h, targets, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts);
+  s = search_shard_impl(h, targets, budgets, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts);
   if (s != ALP_OK) return s;
-  return finalize_impl(h, targets, n, budget_units, h->s_keys, h->s_counts, h->stream, out);
+  return finalize_impl(h, targets, budgets, n, budget_units, h->s_keys, h->s_counts, h->stream, out);
+}
+
+alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t budget_units, alp_result *out) {
+  return search_queries(h, targets, nullptr, n, budget_units, out);
+}
+
+alp_status alp_search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n, alp_result *out) {
+  if (!budgets) return fail(ALP_EINVAL, "budgets is NULL");
+  return search_queries(h, targets, budgets, n, 0, out);
 }
 
 alp_status alp_search(alp_t *h, double target, int64_t budget_units, alp_result *out) {
   return alp_search_batch(h, &target, 1, budget_units, out);
+}
+
+alp_status alp_schedule_egalitarian(alp_t *const *hs, const double *targets, int32_t W, int32_t gpus,
+                                    int32_t units_per_gpu, int32_t *gpus_out, alp_result *results_out,
+                                    double *min_utility, double *sum_utility) {
+  if (!hs || !targets || !gpus_out || !results_out) return fail(ALP_EINVAL, "NULL argument");
+  if (W < 1 || W > ALP_MAX_M) return fail(ALP_EINVAL, "W must be in 1..%d", ALP_MAX_M);
+  if (gpus < 0 || gpus > 4096) return fail(ALP_EINVAL, "gpus must be in 0..4096");
+  if (units_per_gpu < 1) return fail(ALP_EINVAL, "units_per_gpu must be >= 1");
+  double splits = 1;
+  for (int w = 0; w + 1 < W; ++w) splits *= (gpus + 1);
+  if (splits > 1e8) return fail(ALP_EINVAL, "too many GPU splits (%.3g)", splits);
+  for (int w = 0; w < W; ++w) {
+    if (!hs[w]) return fail(ALP_EINVAL, "hs[%d] is NULL", w);
+    if (hs[w]->device != hs[0]->device) return fail(ALP_EINVAL, "all handles must live on one device");
+  }
+  // budget-indexed search per workflow: the best allocation on g = 0..G GPUs
+  const int G = gpus;
+  std::vector<int64_t> budgets(G + 1);
+  for (int g = 0; g <= G; ++g) budgets[g] = (int64_t)g * units_per_gpu;
+  std::vector<double> lat((size_t)W * (G + 1));
+  std::vector<std::vector<alp_result>> per(W, std::vector<alp_result>(G + 1));
+  for (int w = 0; w < W; ++w) {
+    std::vector<double> tg(G + 1, targets[w]);
+    alp_status s = search_queries(hs[w], tg.data(), budgets.data(), G + 1, 0, per[w].data());
+    if (s != ALP_OK && s != ALP_EINFEASIBLE) return s;
+    for (int g = 0; g <= G; ++g) lat[(size_t)w * (G + 1) + g] = per[w][g].found ? per[w][g].latency : INFINITY;
+  }
+  alp_s *h0 = hs[0];
+  CU(cudaSetDevice(h0->device));
+  DBuf<double> d_lat, d_out;
+  DBuf<long long> d_idx;
+  CU(d_lat.ensure(lat.size()));
+  CU(d_out.ensure(2));
+  CU(d_idx.ensure(1));
+  CU(cudaMemcpyAsync(d_lat.p, lat.data(), lat.size() * sizeof(double), cudaMemcpyHostToDevice, h0->stream));
+  CU(launch_egalitarian(d_lat.p, W, G, d_idx.p, d_out.p, d_out.p + 1, h0->stream));
+  long long idx = -1;
+  double mm[2] = {0, 0};
+  CU(cudaMemcpyAsync(&idx, d_idx.p, sizeof(idx), cudaMemcpyDeviceToHost, h0->stream));
+  CU(cudaMemcpyAsync(mm, d_out.p, sizeof(mm), cudaMemcpyDeviceToHost, h0->stream));
+  CU(cudaStreamSynchronize(h0->stream));
+  d_lat.release();
+  d_out.release();
+  d_idx.release();
+  if (idx < 0) return fail(ALP_EINTERNAL, "no split evaluated");
+  int used = 0;
+  for (int w = W - 2; w >= 0; --w) {
+    gpus_out[w] = (int32_t)(idx % (G + 1));
+    idx /= (G + 1);
+    used += gpus_out[w];
+  }
+  gpus_out[W - 1] = G - used;
+  bool all = true;
+  for (int w = 0; w < W; ++w) {
+    results_out[w] = per[w][gpus_out[w]];
+    all &= results_out[w].found != 0;
+  }
+  if (min_utility) *min_utility = mm[0];
+  if (sum_utility) *sum_utility = mm[1];
+  return all ? ALP_OK : ALP_EINFEASIBLE;
 }
 
 float alp_last_kernel_ms(const alp_t *h) {

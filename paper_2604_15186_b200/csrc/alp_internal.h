@@ -48,7 +48,8 @@ struct SearchArgs {
   uint32_t n_groups;     // warp groups of 32 lane tiles
   uint32_t nQ, A;        // a-ranges: a in [q*A, min((q+1)*A, Ka))
   uint64_t item_lo, item_hi;
-  int budget;            // R (capped at the total max units; <= kMaxBudget)
+  int budget;            // R (capped at the total max units); max over queries when q_budget is set
+  const int *q_budget;   // [n_targets] per-query budgets (capped) or nullptr (all = budget)
   int n_targets;
   int n_bchunks, bchunk_w, bchunk_wpad;  // b columns (u-sorted) split in chunks
   int row_stride;        // floats per masked row (== 4 mod 8)
@@ -109,5 +110,7 @@ int const_words_max();
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
 int search_max_blocks_per_sm(const SearchArgs &a);
+cudaError_t launch_egalitarian(const double *lat, int W, int G, long long *best_idx, double *best_min,
+                               double *best_sum, cudaStream_t st);
 
 }  // namespace alp

@@ -165,6 +165,9 @@ __device__ __forceinline__ float btab_entry(const SearchArgs &P, const float *ta
   const int len = min(max(dcnt[row], c0), c1) - c0;
   return (j < len) ? tau_t[P.b_llm * P.K + P.bperm[c0 + j]] : __int_as_float(0x7f800000);
 }
+// budget of query t (per-query budgets for budget sweeps, else the common budget)
+__device__ __forceinline__ int qbudget(const SearchArgs &P, int t) { return P.q_budget ? P.q_budget[t] : P.budget; }
+
 // masked-row index for remaining budget r: #{distinct b unit values <= r}
 __device__ __forceinline__ int row_of(const int *dv, int D, int r) {
   int lo = 0, hi = D;
@@ -188,9 +191,9 @@ __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *
 }
 
 // Build the per-(target, b-chunk) tables in shared memory.  All threads participate.
-__device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c) {
+__device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c, int R) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int K = P.K, R = P.budget, D = P.D;
+  const int K = P.K, D = row_of(P.dv, P.D, R);
   const float *tau_t = P.tau + (size_t)t * P.M * K;
   const int c0 = c * P.bchunk_w;
   const int c1 = min(c0 + P.bchunk_w, P.Kb);
@@ -317,7 +320,8 @@ __global__ void k_const_tables(const __grid_constant__ SearchArgs P, int t, int 
   const int tid = threadIdx.x, nt = blockDim.x;
   const float *tau_t = P.tau + (size_t)t * P.M * P.K;
   const int c0 = c * P.bchunk_w, c1 = min(c0 + P.bchunk_w, P.Kb);
-  const int rows = P.D + 1;
+  const int R = qbudget(P, t), D = row_of(P.dv, P.D, R);
+  const int rows = D + 1;
   for (int a = tid; a < P.Ka; a += nt) {
     const float2 v = a_entry(P, tau_t, a);
     out[2 * a] = __float_as_uint(v.x);
@@ -336,8 +340,8 @@ __global__ void k_const_tables(const __grid_constant__ SearchArgs P, int t, int 
     if (lane == 0) rowcnt[row] = n;
   }
   __syncthreads();
-  for (int r = tid - 1; r <= P.budget; r += nt) {
-    const int row = row_of(P.dv, P.D, r);
+  for (int r = tid - 1; r <= R; r += nt) {
+    const int row = row_of(P.dv, D, r);
     out[P.cu_off_lut + 2 * (r + 1)] = (uint32_t)(P.cu_off_btab + row * P.row_stride);
     out[P.cu_off_lut + 2 * (r + 1) + 1] = rowcnt[row];
   }
@@ -370,7 +374,7 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
 
 template <int T, int NB4, bool TAIL2>
 __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
-                              uint32_t &best_seg, unsigned long long &cnt) {
+                              uint32_t &best_seg, unsigned long long &cnt, int R) {
   const int lane = threadIdx.x & 31;
   const uint64_t nW = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -431,7 +435,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
           acc[2 * v + h] = finf();
         }
       }
-      r_tile = P.budget - Upfx - stile;
+      r_tile = R - Upfx - stile;
       q0 = q;
       tchunk = chunk;
       ttile = tile;
@@ -500,8 +504,9 @@ __global__ void __launch_bounds__(kThreads)
     unsigned long long cnt = 0ull;
     for (int c = P.c_begin; c < P.c_end; ++c) {
       __syncthreads();
-      build_tables(P, s, t, c);
-      process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt);
+      const int R = qbudget(P, t);
+      build_tables(P, s, t, c, R);
+      process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt, R);
     }
     unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
 #pragma unroll
@@ -656,7 +661,7 @@ __global__ void k_finalize(const FinalizeArgs F) {
       }
       const float v = __fadd_rn(__fadd_rn(Qrow, ta), tau_t[P.b_llm * K + b]);
       const int units = Urow + ua + P.u[P.b_llm * K + b];
-      if (v == val && units <= P.budget) {
+      if (v == val && units <= qbudget(P, t)) {
         mine = li;
         break;
       }
@@ -718,6 +723,67 @@ __global__ void k_finalize(const FinalizeArgs F) {
     r.throughput = 0.0;
   }
   F.out[t] = r;
+}
+
+// ------------------------------------------------------------------ multi-workflow split (NEXT-1)
+// Egalitarian welfare over whole-GPU splits: lat[w*(G+1)+g] = best FP64 latency
+// of workflow w on g GPUs (+inf if infeasible).  u_w(g) = lat_w(G) / lat_w(g) (0 if infeasible);
+// splits (g_0..g_{W-2}, g_{W-1} = G - sum) maximise min_w u_w, then sum_w u_w, then the lowest
+// split index (g_0 most significant).  One block; out: best split index, min and sum utility.
+__global__ void k_egalitarian(const double *lat, int W, int G, long long *best_idx, double *best_min, double *best_sum) {
+  __shared__ double s_min[256], s_sum[256];
+  __shared__ long long s_idx[256];
+  long long total = 1;
+  for (int w = 0; w + 1 < W; ++w) total *= (G + 1);
+  double bmin = -1.0, bsum = -1.0;
+  long long bidx = -1;
+  for (long long i = threadIdx.x; i < total; i += blockDim.x) {
+    long long rem = i;
+    int g[ALP_MAX_M];
+    int used = 0;
+    for (int w = W - 2; w >= 0; --w) {
+      g[w] = (int)(rem % (G + 1));
+      rem /= (G + 1);
+      used += g[w];
+    }
+    if (used > G) continue;
+    g[W - 1] = G - used;
+    double mn = CUDART_INF, sm = 0.0;
+    for (int w = 0; w < W; ++w) {
+      const double solo = lat[w * (G + 1) + G], l = lat[w * (G + 1) + g[w]];
+      const double u = (l < CUDART_INF && solo < CUDART_INF) ? __ddiv_rn(solo, l) : 0.0;
+      mn = u < mn ? u : mn;
+      sm = __dadd_rn(sm, u);
+    }
+    if (mn > bmin || (mn == bmin && (sm > bsum || (sm == bsum && i < bidx)))) {
+      bmin = mn;
+      bsum = sm;
+      bidx = i;
+    }
+  }
+  s_min[threadIdx.x] = bmin;
+  s_sum[threadIdx.x] = bsum;
+  s_idx[threadIdx.x] = bidx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < (int)blockDim.x; ++j) {
+      if (s_idx[j] < 0) continue;
+      if (bidx < 0 || s_min[j] > bmin || (s_min[j] == bmin && (s_sum[j] > bsum || (s_sum[j] == bsum && s_idx[j] < bidx)))) {
+        bmin = s_min[j];
+        bsum = s_sum[j];
+        bidx = s_idx[j];
+      }
+    }
+    *best_idx = bidx;
+    *best_min = bmin;
+    *best_sum = bsum;
+  }
+}
+
+cudaError_t launch_egalitarian(const double *lat, int W, int G, long long *best_idx, double *best_min,
+                               double *best_sum, cudaStream_t st) {
+  k_egalitarian<<<1, 256, 0, st>>>(lat, W, G, best_idx, best_min, best_sum);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ predict

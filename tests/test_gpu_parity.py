@@ -306,3 +306,41 @@ def test_plan_cache_shared_and_cleared(P):
     a1.close()
     r = a2.search(lam, d["budget_units"])  # a2 keeps its (now uncached) plan alive
     assert r.index == r1.index
+
+
+# ----------------------------------------------------------------------------- budget queries / NEXT-1
+def test_search_queries_budget_sweep(P):
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = d["targets"][0]
+    budgets = [0, 7, 16, 33, 64, 96, 128, 200, 10**6]
+    res = alp.search_queries([lam] * len(budgets), budgets)
+    tab = oracle.option_table(I, lam)
+    for B, r in zip(budgets, res):
+        f, v, idx, cnt = dp.search(tab["tau"], tab["u"], min(B, 10**4))
+        _same(r, f, v, idx, cnt, B)
+    # mixed targets and budgets in one pass
+    qs = [(lam, 128), (lam * 2, 64), (lam * 0.5, 100), (d["lambda_star"], 128)]
+    res = alp.search_queries([q[0] for q in qs], [q[1] for q in qs])
+    for (l, B), r in zip(qs, res):
+        t2 = oracle.option_table(I, l)
+        f, v, idx, cnt = dp.search(t2["tau"], t2["u"], B)
+        _same(r, f, v, idx, cnt, (l, B))
+
+
+@pytest.mark.parametrize("names,gpus,F", [(("C1", "C1"), 8, 4), (("hand", "C4"), 16, 2), (("C2", "C3"), 16, 8)])
+def test_egalitarian_vs_oracle(P, names, gpus, F):
+    from oracle import multi
+    ds = [generate.load(n) for n in names]
+    alps = [P.Alp.from_instance(d) for d in ds]
+    targets = [d["targets"][0] for d in ds]
+    split, res, mn, sm = P.schedule_egalitarian(alps, targets, gpus, F)
+    lat = [multi.best_latencies(oracle.from_json(d), t, gpus, F) for d, t in zip(ds, targets)]
+    osplit, omn, osm = multi.egalitarian(lat, gpus)
+    assert split == osplit and mn == omn and sm == osm
+    for d, t, g, r in zip(ds, targets, split, res):
+        I = oracle.from_json(d)
+        tab = oracle.option_table(I, t)
+        f, v, idx, cnt = dp.search(tab["tau"], tab["u"], g * F)
+        _same(r, f, v, idx, cnt, (d["name"], g))

@@ -387,3 +387,30 @@ def test_c1_full_bruteforce_vs_literal_candidates():
             if best is None or l32 < best[0]:
                 best = (l32, idx)
     assert (r.count, r.latency_key, r.index) == (cnt, best[0], best[1])
+
+
+# ----------------------------------------------------------------------------- multi-workflow (NEXT-1)
+def test_egalitarian_single_workflow_degenerates_to_search():
+    # search_multi with one workflow degenerates exactly to search (all GPUs, u = 1)
+    from oracle import multi
+    d = generate.load("C1")
+    I = oracle.from_json(d)
+    lat = multi.best_latencies(I, d["targets"][0], 4, 4)
+    split, mn, sm = multi.egalitarian([lat], 4)
+    assert split == [4] and mn == 1.0 and sm == 1.0
+    r = oracle.search(I, d["targets"][0], 16)
+    assert lat[4] == oracle.predict(I, d["targets"][0], oracle.decode(I, r.index), 16)["latency"]
+
+
+def test_egalitarian_identical_workflows_split_evenly():
+    # two identical workflows with identical rates on an even cluster -> symmetric
+    # split, equal utilities
+    from oracle import multi
+    d = generate.load("C1")
+    I = oracle.from_json(d)
+    lat = multi.best_latencies(I, d["targets"][0], 8, 4)
+    split, mn, sm = multi.egalitarian([lat, lat], 8)
+    assert split == [4, 4]
+    u = lat[8] / lat[4]
+    assert mn == u and sm == u + u
+    assert all(a >= b for a, b in zip(lat, lat[1:]))  # more GPUs never hurt (budget monotone)
