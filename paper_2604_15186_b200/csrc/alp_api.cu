@@ -161,8 +161,6 @@ struct alp_s {
   std::vector<uint32_t> tile_e, tile_off;
   int rows_per_lane = 8;
   int min_blocks = 3;
-  int use_uniform = 0;  // ALP_UNIFORM=1 enables the constant-bank (warp-uniform) path (measured slower, profiles/README.md)
-  uint32_t *d_cscratch = nullptr;  // const_words_max() words: one phase's constant-bank tables
   int umax_a = 0, umax_b = 0;
   long long umax_total = 0;
   // device
@@ -461,7 +459,6 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_keys);
   A.scratch(1, &h->a_counts);
   A.scratch(1, &h->a_qb);
-  A.scratch((size_t)const_words_max(), &h->d_cscratch);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
   return ALP_OK;
 }
@@ -471,8 +468,7 @@ alp_status init_device(alp_s *h) {
   // C3 / C4, profiles/r01_variant_sweep.txt); ALP_ROWS_PER_LANE overrides.
   h->rows_per_lane = (h->K >= 64) ? 16 : 8;
   if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 16) ? 16 : 8;
-  if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = (atoi(v) == 4) ? 4 : 3;
-  if (const char *v = getenv("ALP_UNIFORM")) h->use_uniform = atoi(v) != 0;
+  if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = std::min(4, std::max(2, atoi(v)));
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -544,11 +540,6 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.rows_per_lane = h->rows_per_lane;
   a.min_blocks = h->min_blocks;
   a.dv = h->d_dv; a.dcnt = h->d_dcnt;
-  // constant-bank layout for the warp-uniform path (one phase): a-table, lut, masked rows
-  a.cu_off_lut = (2 * h->Ka + 3) & ~3;
-  a.cu_off_btab = (a.cu_off_lut + 2 * (a.budget + 2) + 3) & ~3;
-  const long long cwords = (long long)a.cu_off_btab + (long long)rows * a.row_stride;
-  a.uni = (cwords <= const_words_max() && h->use_uniform) ? 1 : 0;
   a.t_begin = 0; a.t_end = n_targets; a.c_begin = 0; a.c_end = a.n_bchunks;
   int bps = search_max_blocks_per_sm(a);
   if (bps < 1) return fail(ALP_ECUDA, "search kernel cannot be resident (smem %d B)", a.smem_bytes);
@@ -661,30 +652,9 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   CU(cudaEventRecord(h->ev0, st));
   int launches = 1;  // K1
   if (hi > lo) {
-    if (!g.a.uni) {
-      g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
-      CU(launch_search(g.a, g.grid, st));
-      launches += 1;
-    } else {
-      // one launch per phase (target, b-chunk): the constant bank holds one phase's tables.  The
-      // constant bank is per device and per process, so phases from different streams are
-      // serialised through g_cmem_mu + g_cmem_ev.
-      static std::mutex g_cmem_mu;
-      static cudaEvent_t g_cmem_ev[64] = {nullptr};
-      std::lock_guard<std::mutex> lock(g_cmem_mu);
-      cudaEvent_t &ev = g_cmem_ev[h->device & 63];
-      if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      CU(cudaStreamWaitEvent(st, ev, 0));
-      for (int t = 0; t < n; ++t)
-        for (int c = 0; c < g.a.n_bchunks; ++c) {
-          CU(launch_const_tables(g.a, t, c, h->d_cscratch, st));
-          SearchArgs a = g.a;
-          a.t_begin = t; a.t_end = t + 1; a.c_begin = c; a.c_end = c + 1;
-          CU(launch_search(a, g.grid, st));
-          launches += 2;
-        }
-      CU(cudaEventRecord(ev, st));
-    }
+    g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
+    CU(launch_search(g.a, g.grid, st));
+    launches += 1;
   }
   CU(cudaEventRecord(h->ev1, st));
   h->ev_pending = true;

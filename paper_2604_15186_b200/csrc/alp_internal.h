@@ -63,8 +63,6 @@ struct SearchArgs {
   int rows_per_lane;     // T (8 or 16)
   int min_blocks;        // launch-bounds variant for T = 8 (3 or 4 blocks/SM)
   int t_begin, t_end, c_begin, c_end;  // phases (target, b-chunk) evaluated by this launch
-  int uni;               // 1: warp-uniform lane tiles use the constant-bank tables (c_mem)
-  int cu_off_lut, cu_off_btab;         // c_mem layout (32-bit words)
   const int *bperm;      // [Kb] canonical option of u-sorted column j
   const int *dv;         // [Dall] distinct b unit values, ascending
   const int *dcnt;       // [Dall+1] dcnt[i] = #u-sorted columns with u <= dv[i-1] (dcnt[0] = 0)
@@ -103,10 +101,6 @@ struct PredictArgs {
 cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st);
 cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
-// Build phase (t, c)'s constant-bank tables into `scratch` (device, >= const_words_max() words) and
-// copy them into the kernel's constant bank, stream-ordered on st.
-cudaError_t launch_const_tables(const SearchArgs &a, int t, int c, uint32_t *scratch, cudaStream_t st);
-int const_words_max();
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
 int search_max_blocks_per_sm(const SearchArgs &a);

@@ -145,14 +145,6 @@ struct Smem {
 
 constexpr int kBigUnits = 1 << 28;
 
-// Constant-bank copy of one phase's tables for the warp-uniform path (see process_items): with all
-// 32 lanes on the same masked row, the b values are read with uniform addresses (LDCU) into uniform
-// registers, so FADD2 takes b from the uniform datapath instead of the vector register file.
-// Layout (32-bit words): [0, 2*Ka) a-table {tau_a bits, -u_a}; [cu_off_lut, +2*(R+2)) {row word
-// offset, #finite} for r = -1..R; [cu_off_btab, ...) masked rows (row_stride words each).
-constexpr int kConstWords = 16384;  // 64 KB
-__constant__ uint32_t c_mem[kConstWords];
-
 // a-table entry for option a (infeasible a gets +inf units -> maps to the all-+inf row)
 __device__ __forceinline__ float2 a_entry(const SearchArgs &P, const float *tau_t, int a) {
   if (P.a_llm < 0) return make_float2(0.f, __int_as_float(0));
@@ -288,65 +280,6 @@ __device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], floa
   if constexpr (TAIL2) eval2<T>(lds64(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
 }
 
-// Warp-uniform variant of eval_row: the masked row lives in the constant bank at word offset
-// `row` (uniform), so every b value is an LDCU into a uniform register.
-template <int T, int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row_c(uint32_t row, const float (&Qa)[T], float (&acc)[T], int ng4) {
-  if constexpr (NB4 > 0) {
-#pragma unroll
-    for (int g = 0; g < NB4; ++g) {
-      const uint32_t o = row + 4 * g;
-      eval4<T>(make_float4(__uint_as_float(c_mem[o]), __uint_as_float(c_mem[o + 1]), __uint_as_float(c_mem[o + 2]),
-                           __uint_as_float(c_mem[o + 3])), Qa, acc);
-    }
-  } else {
-#pragma unroll 2
-    for (int g = 0; g < ng4; ++g) {
-      const uint32_t o = row + 4 * g;
-      eval4<T>(make_float4(__uint_as_float(c_mem[o]), __uint_as_float(c_mem[o + 1]), __uint_as_float(c_mem[o + 2]),
-                           __uint_as_float(c_mem[o + 3])), Qa, acc);
-    }
-  }
-  if constexpr (TAIL2) {
-    const uint32_t o = row + (NB4 > 0 ? NB4 : ng4) * 4;
-    eval2<T>(make_float2(__uint_as_float(c_mem[o]), __uint_as_float(c_mem[o + 1])), Qa, acc);
-  }
-}
-
-// Builds one phase's constant-bank tables (layout above) into a global buffer; the host copies it
-// into c_mem (cudaMemcpyToSymbolAsync, device to device) before the phase's k_search launch.
-__global__ void k_const_tables(const __grid_constant__ SearchArgs P, int t, int c, uint32_t *out) {
-  __shared__ unsigned rowcnt[ALP_MAX_K + 1];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const float *tau_t = P.tau + (size_t)t * P.M * P.K;
-  const int c0 = c * P.bchunk_w, c1 = min(c0 + P.bchunk_w, P.Kb);
-  const int R = qbudget(P, t), D = row_of(P.dv, P.D, R);
-  const int rows = D + 1;
-  for (int a = tid; a < P.Ka; a += nt) {
-    const float2 v = a_entry(P, tau_t, a);
-    out[2 * a] = __float_as_uint(v.x);
-    out[2 * a + 1] = __float_as_uint(v.y);
-  }
-  for (int i = tid; i < rows * P.row_stride; i += nt) {
-    const int row = i / P.row_stride, j = i % P.row_stride;
-    out[P.cu_off_btab + i] = __float_as_uint(j < P.bchunk_wpad ? btab_entry(P, tau_t, P.dcnt, row, j, c0, c1) : 0.f);
-  }
-  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
-  for (int row = warp; row < rows; row += nwarp) {
-    unsigned n = 0;
-    for (int j = lane; j < P.bchunk_wpad; j += 32)
-      n += (btab_entry(P, tau_t, P.dcnt, row, j, c0, c1) < finf()) ? 1u : 0u;
-    n = __reduce_add_sync(0xffffffffu, n);
-    if (lane == 0) rowcnt[row] = n;
-  }
-  __syncthreads();
-  for (int r = tid - 1; r <= R; r += nt) {
-    const int row = row_of(P.dv, D, r);
-    out[P.cu_off_lut + 2 * (r + 1)] = (uint32_t)(P.cu_off_btab + row * P.row_stride);
-    out[P.cu_off_lut + 2 * (r + 1) + 1] = rowcnt[row];
-  }
-}
-
 // Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
 // row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
 // The tile's packed digits are read only when a row can improve the best (rare).
@@ -444,35 +377,17 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     unsigned c32 = 0;
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
-    // warp-uniform lane tiles (every lane on the same remaining budget, or all over budget) take
-    // the constant-bank path; mixed tiles read their own masked rows from shared memory.
-    const int r0 = __shfl_sync(0xffffffffu, r_tile, 0);
-    if (P.uni && __all_sync(0xffffffffu, (r_tile == r0) || (r_tile < 0 && r0 < 0))) {
-      const int a0u = __shfl_sync(0xffffffffu, a0, 0), a1u = __shfl_sync(0xffffffffu, a1, 0);
+    const float2 *ap = s.a + a0;
 #pragma unroll(kAUnroll)
-      for (int a = a0u; a < a1u; ++a) {
-        const float ta = __uint_as_float(c_mem[2 * a]);
-        const int ra = max(r0 + (int)c_mem[2 * a + 1], -1);
-        const uint32_t lrow = c_mem[P.cu_off_lut + 2 * (ra + 1)];
-        c32 += c_mem[P.cu_off_lut + 2 * (ra + 1) + 1];
-        float Qa[T];
+    for (int a = a0; a < a1; ++a, ++ap) {
+      const float2 av = *ap;
+      const int ra = max(r_tile + __float_as_int(av.y), -1);
+      const int2 lu = s.lut[ra + 1];
+      c32 += (unsigned)lu.y;
+      float Qa[T];
 #pragma unroll
-        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], ta);
-        eval_row_c<T, NB4, TAIL2>(lrow, Qa, acc, ng4);
-      }
-    } else {
-      const float2 *ap = s.a + a0;
-#pragma unroll(kAUnroll)
-      for (int a = a0; a < a1; ++a, ++ap) {
-        const float2 av = *ap;
-        const int ra = max(r_tile + __float_as_int(av.y), -1);
-        const int2 lu = s.lut[ra + 1];
-        c32 += (unsigned)lu.y;
-        float Qa[T];
-#pragma unroll
-        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-        eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
-      }
+      for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+      eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
     }
     cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
     // advance to the next item (q fastest); fold when the lane tile changes
@@ -489,11 +404,9 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
 }
 
-// T = rows per lane.  Deliberately no minimum-blocks launch bound: any register cap (launch bounds
-// min blocks, -maxrregcount) stops ptxas from using the uniform datapath, which the warp-uniform
-// path needs (FADD2 with a uniform-register b operand); the natural allocation fits 3 blocks/SM.
-template <int T, int NB4, bool TAIL2>
-__global__ void __launch_bounds__(kThreads)
+// T = rows per lane; MB = minimum resident blocks per SM (register cap 65536 / (256 * MB)).
+template <int T, int NB4, bool TAIL2, int MB>
+__global__ void __launch_bounds__(kThreads, MB)
     k_search(const __grid_constant__ SearchArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
@@ -535,10 +448,12 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
+// Register-cap variants: T = 8 -> 3 (default) or 4 blocks/SM; T = 16 -> 2 (default) or 3.
 template <int T, int NB4, bool TAIL2>
 static auto pick(const SearchArgs &a) {
-  (void)a;
-  return k_search<T, NB4, TAIL2>;
+  constexpr int kLo = (T == 8) ? 3 : 2, kHi = (T == 8) ? 4 : 3;
+  if (a.min_blocks == kHi) return k_search<T, NB4, TAIL2, kHi>;
+  return k_search<T, NB4, TAIL2, kLo>;
 }
 
 template <int T, int NB4, bool TAIL2>
@@ -588,16 +503,6 @@ static int occ_one(const SearchArgs &a) {
     if (a.rows_per_lane == 16) ALP_DISPATCH_W(CALL, 16); \
     ALP_DISPATCH_W(CALL, 8);                \
   } while (0)
-
-cudaError_t launch_const_tables(const SearchArgs &a, int t, int c, uint32_t *scratch, cudaStream_t st) {
-  k_const_tables<<<1, 256, 0, st>>>(a, t, c, scratch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const size_t words = (size_t)a.cu_off_btab + (size_t)(a.D + 1) * a.row_stride;
-  return cudaMemcpyToSymbolAsync(c_mem, scratch, words * 4, 0, cudaMemcpyDeviceToDevice, st);
-}
-
-int const_words_max() { return kConstWords; }
 
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st) {
 #define CALL(T, N, T2) launch_one<T, N, T2>(a, grid, st)
