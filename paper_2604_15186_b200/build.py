@@ -4,6 +4,7 @@
 """
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -12,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libscepsy_alp.so")
-SOURCES = ["alp_api.cu", "alp_kernels.cu"]
-HEADERS = ["alp_internal.h", os.path.join("..", "..", "include", "alp.h")]
+SOURCES = ["alp_api.cu", "alp_kernels.cu", "alp_search_t8.cu", "alp_search_t16.cu"]
+HEADERS = ["alp_internal.h", "alp_search.cuh", os.path.join("..", "..", "include", "alp.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # IEEE semantics: no fast-math, no FTZ; explicit __d*_rn intrinsics in the FP64 option terms.
@@ -35,8 +36,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     if not force and out is None and not _stale():
         return LIB
     os.makedirs(os.path.dirname(lib), exist_ok=True)
-    objs = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(os.path.dirname(lib), src.replace(".cu", ".o") if out is None else
                            os.path.basename(lib) + "." + src.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
@@ -48,7 +49,10 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
             f.write(r.stderr)
         if verbose:
             sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return obj
+
+    with concurrent.futures.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     subprocess.check_call(cmd)

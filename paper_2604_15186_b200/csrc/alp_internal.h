@@ -74,6 +74,9 @@ struct SearchArgs {
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
 };
 
+// budget of query t (per-query budgets for budget sweeps, else the common budget)
+__device__ __forceinline__ int qbudget(const SearchArgs &P, int t) { return P.q_budget ? P.q_budget[t] : P.budget; }
+
 struct FinalizeArgs {
   SearchArgs s;
   const double *term;    // [n_t][M][K]

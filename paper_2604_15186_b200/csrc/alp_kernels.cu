@@ -28,13 +28,7 @@
 
 #include "alp_internal.h"
 
-#ifndef ALP_A_UNROLL
-#define ALP_A_UNROLL 2  // a-loop unroll (tuned: 2 beats 1 on C3 and C4, profiles/r01_variant_sweep.txt)
-#endif
-
 namespace alp {
-
-constexpr int kAUnroll = ALP_A_UNROLL;
 
 __device__ __forceinline__ float finf() { return __int_as_float(0x7f800000); }
 
@@ -113,407 +107,19 @@ __global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts
   }
 }
 
-// ------------------------------------------------------------------ search kernel (K2)
-// add.rn.f32x2 {v0,v1} = {q,q} + {b0,b1}  (SASS: FADD2 with scalar-broadcast operand)
-__device__ __forceinline__ void add2(float &v0, float &v1, float q, float b0, float b1) {
-  asm("{.reg .b64 x,y,z;\n\tmov.b64 x,{%2,%2};\n\tmov.b64 y,{%3,%4};\n\tadd.rn.f32x2 z,x,y;\n\tmov.b64 {%0,%1},z;}"
-      : "=f"(v0), "=f"(v1)
-      : "f"(q), "f"(b0), "f"(b1));
-}
-// add.rn.f32x2 {v0,v1} = {q0,q1} + {b,b}
-__device__ __forceinline__ void add2b(float &v0, float &v1, float q0, float q1, float b) {
-  asm("{.reg .b64 x,y,z;\n\tmov.b64 x,{%2,%3};\n\tmov.b64 y,{%4,%4};\n\tadd.rn.f32x2 z,x,y;\n\tmov.b64 {%0,%1},z;}"
-      : "=f"(v0), "=f"(v1)
-      : "f"(q0), "f"(q1), "f"(b));
-}
-// 3-input min (SASS: FMNMX3)
-__device__ __forceinline__ float min3(float a, float b, float c) {
-  float d;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-
-struct Smem {
-  float *tau;      // [g1*K + 2] tau of prefix + sort-group LLMs (current target), then {0, +inf}; offset 0
-  int *u;          // [g0*K] units of prefix LLMs
-  float2 *a;       // [Ka] {tau_a, bits(-u_a)}; u_a := kBigUnits when tau_a is +inf
-  int2 *lut;       // [R+2] {shared address of the masked row, #finite entries in it} for r = -1..R
-  int *dv;         // [D] distinct b unit values <= R, ascending
-  int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
-  float *btab;     // [rows][row_stride] masked rows
-};
-
-constexpr int kBigUnits = 1 << 28;
-
-// a-table entry for option a (infeasible a gets +inf units -> maps to the all-+inf row)
-__device__ __forceinline__ float2 a_entry(const SearchArgs &P, const float *tau_t, int a) {
-  if (P.a_llm < 0) return make_float2(0.f, __int_as_float(0));
-  const float ta = tau_t[P.a_llm * P.K + a];
-  return make_float2(ta, __int_as_float(ta < __int_as_float(0x7f800000) ? -P.u[P.a_llm * P.K + a] : -kBigUnits));
-}
-// masked-row element (row, j) of b-chunk [c0, c1): tau_b of the j-th u-sorted column if it fits
-__device__ __forceinline__ float btab_entry(const SearchArgs &P, const float *tau_t, const int *dcnt, int row, int j,
-                                            int c0, int c1) {
-  const int len = min(max(dcnt[row], c0), c1) - c0;
-  return (j < len) ? tau_t[P.b_llm * P.K + P.bperm[c0 + j]] : __int_as_float(0x7f800000);
-}
-// budget of query t (per-query budgets for budget sweeps, else the common budget)
-__device__ __forceinline__ int qbudget(const SearchArgs &P, int t) { return P.q_budget ? P.q_budget[t] : P.budget; }
-
-// masked-row index for remaining budget r: #{distinct b unit values <= r}
-__device__ __forceinline__ int row_of(const int *dv, int D, int r) {
-  int lo = 0, hi = D;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (dv[mid] <= r) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
-  Smem s;
-  s.tau = reinterpret_cast<float *>(base + P.off_tau);
-  s.u = reinterpret_cast<int *>(base + P.off_u);
-  s.a = reinterpret_cast<float2 *>(base + P.off_a);
-  s.lut = reinterpret_cast<int2 *>(base + P.off_lut);
-  s.dv = reinterpret_cast<int *>(base + P.off_tmp);
-  s.dcnt = s.dv + (P.Kb + 1);
-  s.btab = reinterpret_cast<float *>(base + P.off_btab);
-  return s;
-}
-
-// Build the per-(target, b-chunk) tables in shared memory.  All threads participate.
-__device__ void build_tables(const SearchArgs &P, const Smem &s, int t, int c, int R) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int K = P.K, D = row_of(P.dv, P.D, R);
-  const float *tau_t = P.tau + (size_t)t * P.M * K;
-  const int c0 = c * P.bchunk_w;
-  const int c1 = min(c0 + P.bchunk_w, P.Kb);
-  for (int i = tid; i < P.g1 * K; i += nt) s.tau[i] = tau_t[i];
-  if (tid == 0) {
-    s.tau[P.g1 * K] = 0.f;         // unused sort-group digit slot: x + 0 = x exactly
-    s.tau[P.g1 * K + 1] = finf();  // padded (dummy) row
-  }
-  for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
-  for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, a);
-  for (int i = tid; i < D; i += nt) s.dv[i] = P.dv[i];
-  for (int i = tid; i <= D; i += nt) s.dcnt[i] = P.dcnt[i];
-  __syncthreads();
-  // masked row i holds the u-sorted columns [c0, c1) with u <= dv[i-1] (row 0: none), +inf elsewhere
-  const int rows = D + 1;
-  for (int i = tid; i < rows * P.bchunk_wpad; i += nt) {
-    const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
-    s.btab[row * P.row_stride + j] = btab_entry(P, tau_t, s.dcnt, row, j, c0, c1);
-  }
-  __syncthreads();
-  // finite entries per masked row (feasible b count), kept in the row's padding column
-  const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
-  for (int row = warp; row < rows; row += nwarp) {
-    unsigned n = 0;
-    for (int j = lane; j < P.bchunk_wpad; j += 32) n += (s.btab[row * P.row_stride + j] < finf()) ? 1u : 0u;
-    n = __reduce_add_sync(0xffffffffu, n);
-    if (lane == 0) s.btab[row * P.row_stride + P.bchunk_wpad] = __int_as_float((int)n);
-  }
-  __syncthreads();
-  // r -> masked row: index = #{distinct b unit values <= r}
-  for (int r = tid - 1; r <= R; r += nt) {
-    const int lo = row_of(s.dv, D, r);
-    s.lut[r + 1] = make_int2((int)(uint32_t)__cvta_generic_to_shared(s.btab + lo * P.row_stride),
-                             __float_as_int(s.btab[lo * P.row_stride + P.bchunk_wpad]));
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ float2 lds64(uint32_t addr) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
-  return v;
-}
-
-// "candidate = Q_a + tau_b; acc = min(acc, candidate)" for 4 b values and T rows:
-//   FADD2 {Q_i, Q_i+1} + {b, b} per (row pair, b)   (add.rn.f32x2; the b operand is a scalar broadcast)
-//   FMNMX3 acc_i = min(acc_i, v_b0, v_b1)           (3-input min)
-// = one issue slot per candidate.  The row-pair form lets the Q pair sit in the operand-reuse cache
-// across the 4 b values (tools/microbench/pipes3: fastest of the encodings tried).
-template <int T>
-__device__ __forceinline__ void eval4(const float4 bv, const float (&Qa)[T], float (&acc)[T]) {
-#pragma unroll
-  for (int i = 0; i < T; i += 2) {
-    float a0, b0, a1, b1, a2, b2, a3, b3;
-    add2b(a0, b0, Qa[i], Qa[i + 1], bv.x);
-    add2b(a1, b1, Qa[i], Qa[i + 1], bv.y);
-    add2b(a2, b2, Qa[i], Qa[i + 1], bv.z);
-    add2b(a3, b3, Qa[i], Qa[i + 1], bv.w);
-    acc[i] = min3(acc[i], a0, a1);
-    acc[i + 1] = min3(acc[i + 1], b0, b1);
-    acc[i] = min3(acc[i], a2, a3);
-    acc[i + 1] = min3(acc[i + 1], b2, b3);
-  }
-}
-
-template <int T>
-__device__ __forceinline__ void eval2(const float2 bv, const float (&Qa)[T], float (&acc)[T]) {
-#pragma unroll
-  for (int i = 0; i < T; i += 2) {
-    float a0, b0, a1, b1;
-    add2b(a0, b0, Qa[i], Qa[i + 1], bv.x);
-    add2b(a1, b1, Qa[i], Qa[i + 1], bv.y);
-    acc[i] = min3(acc[i], a0, a1);
-    acc[i + 1] = min3(acc[i + 1], b0, b1);
-  }
-}
-
-template <int T, int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], float (&acc)[T], int ng4) {
-  if constexpr (NB4 > 0) {
-#pragma unroll
-    for (int g = 0; g < NB4; ++g) eval4<T>(lds128(rp + 16 * g), Qa, acc);
-  } else {
-#pragma unroll 2
-    for (int g = 0; g < ng4; ++g) eval4<T>(lds128(rp + 16 * g), Qa, acc);
-  }
-  if constexpr (TAIL2) eval2<T>(lds64(rp + (NB4 > 0 ? NB4 : ng4) * 16), Qa, acc);
-}
-
-// Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
-// row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
-// The tile's packed digits are read only when a row can improve the best (rare).
-template <int T>
-__device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[T], uint32_t tile, uint32_t chunk,
-                                          uint32_t q0, float &best, uint32_t &best_seg) {
-  bool any = false;
-#pragma unroll
-  for (int i = 0; i < T; ++i) any |= (acc[i] <= best) && (acc[i] < finf());
-  if (!any) return;
-  const uint32_t dmask = (1u << P.dig_bits) - 1u;
-  for (int i = 0; i < T; ++i) {
-    if (acc[i] <= best && acc[i] < finf()) {
-      const uint32_t e = __ldg(P.tile_e + (size_t)tile * T + i);
-      uint32_t ec = 0;  // canonical within-group index: LLM g0 most significant
-      for (int j = 0; j < P.ng; ++j) ec = ec * (uint32_t)P.K + ((e >> (j * P.dig_bits)) & dmask);
-      const uint32_t seg = (chunk * P.L + ec) * P.nQ + q0;
-      if (acc[i] < best || seg < best_seg) {
-        best = acc[i];
-        best_seg = seg;
-      }
-    }
-  }
-}
-
-template <int T, int NB4, bool TAIL2>
-__device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
-                              uint32_t &best_seg, unsigned long long &cnt, int R) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nW = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint64_t n = P.item_hi - P.item_lo;
-  uint64_t it = P.item_lo + n * w / nW;
-  const uint64_t end = P.item_lo + n * (w + 1) / nW;
-  if (it >= end) return;
-  const int K = P.K;
-  const int ng4 = P.bchunk_wpad >> 2;
-  uint32_t q = (uint32_t)(it % P.nQ);
-  const uint64_t tq = it / P.nQ;
-  uint32_t grp = (uint32_t)(tq % P.n_groups);
-  uint32_t chunk = (uint32_t)(tq / P.n_groups);
-  // state of the lane tile currently loaded
-  float Qr[T], acc[T];
-  int r_tile = 0;
-  unsigned nfin = 0;
-  uint32_t q0 = q, tchunk = chunk, ttile = 0;
-  bool loaded = false;
-  float Pfx = 0.f;
-  int Upfx = 0;
-  uint32_t pchunk = 0xffffffffu;
-  const unsigned char *tau_b = reinterpret_cast<const unsigned char *>(s.tau);
-  for (; it < end; ++it) {
-    if (!loaded) {
-      if (chunk != pchunk) {
-        // canonical partial sum over LLMs 0..g0-1 (LLM 0 most significant): ((0 + tau_0) + tau_1) + ...
-        float pa = 0.f;
-        int U = 0;
-        for (int m = 0; m < P.g0; ++m) {
-          const uint32_t d = (chunk / P.pw[m]) % (uint32_t)K;
-          pa = __fadd_rn(pa, s.tau[m * K + d]);
-          U += s.u[m * K + d];
-        }
-        Pfx = pa;
-        Upfx = U;
-        pchunk = chunk;
-      }
-      const uint32_t tile = grp * kWarpTiles + lane;
-      const int stile = __ldg(P.tile_s + tile);
-      // per row: 4 smem byte offsets (16 bits each) of the sort-group terms, in LLM order;
-      // unused digits point at 0.0f, padded rows at +inf
-      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * (T / 2);
-      nfin = 0;
-#pragma unroll
-      for (int v = 0; v < T / 2; ++v) {
-        const uint4 o = __ldg(op + v);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t w0 = h ? o.z : o.x, w1 = h ? o.w : o.y;
-          float qv = Pfx;
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w0 & 0xffffu)));
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w0 >> 16)));
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w1 & 0xffffu)));
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w1 >> 16)));
-          Qr[2 * v + h] = qv;
-          nfin += (qv < finf()) ? 1u : 0u;
-          acc[2 * v + h] = finf();
-        }
-      }
-      r_tile = R - Upfx - stile;
-      q0 = q;
-      tchunk = chunk;
-      ttile = tile;
-      loaded = true;
-    }
-    unsigned c32 = 0;
-    const int a0 = (int)(q * P.A);
-    const int a1 = min(a0 + (int)P.A, P.Ka);
-    const float2 *ap = s.a + a0;
-#pragma unroll(kAUnroll)
-    for (int a = a0; a < a1; ++a, ++ap) {
-      const float2 av = *ap;
-      const int ra = max(r_tile + __float_as_int(av.y), -1);
-      const int2 lu = s.lut[ra + 1];
-      c32 += (unsigned)lu.y;
-      float Qa[T];
-#pragma unroll
-      for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-      eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
-    }
-    cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
-    // advance to the next item (q fastest); fold when the lane tile changes
-    if (++q == P.nQ) {
-      q = 0;
-      fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
-      loaded = false;
-      if (++grp == P.n_groups) {
-        grp = 0;
-        ++chunk;
-      }
-    }
-  }
-  if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
-}
-
-// T = rows per lane; MB = minimum resident blocks per SM (register cap 65536 / (256 * MB)).
-template <int T, int NB4, bool TAIL2, int MB>
-__global__ void __launch_bounds__(kThreads, MB)
-    k_search(const __grid_constant__ SearchArgs P) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
-  const Smem s = smem_layout(P, smem);
-  for (int t = P.t_begin; t < P.t_end; ++t) {
-    float best = finf();
-    uint32_t best_seg = 0xffffffffu;
-    unsigned long long cnt = 0ull;
-    for (int c = P.c_begin; c < P.c_end; ++c) {
-      __syncthreads();
-      const int R = qbudget(P, t);
-      build_tables(P, s, t, c, R);
-      process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt, R);
-    }
-    unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
-      const unsigned long long oc = __shfl_xor_sync(0xffffffffu, cnt, o);
-      key = ok < key ? ok : key;
-      cnt += oc;
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-      red_key[warp] = key;
-      red_cnt[warp] = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long k = red_key[0], n = red_cnt[0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-        k = red_key[w] < k ? red_key[w] : k;
-        n += red_cnt[w];
-      }
-      if (k != kKeyNone) atomicMin(P.keys + t, k);
-      if (n) atomicAdd(P.counts + t, n);
-    }
-  }
-}
-
-// Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
-// Register-cap variants: T = 8 -> 3 (default) or 4 blocks/SM; T = 16 -> 2 (default) or 3.
-template <int T, int NB4, bool TAIL2>
-static auto pick(const SearchArgs &a) {
-  constexpr int kLo = (T == 8) ? 3 : 2, kHi = (T == 8) ? 4 : 3;
-  if (a.min_blocks == kHi) return k_search<T, NB4, TAIL2, kHi>;
-  return k_search<T, NB4, TAIL2, kLo>;
-}
-
-template <int T, int NB4, bool TAIL2>
-static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
-  auto fn = pick<T, NB4, TAIL2>(a);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
-  if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <int T, int NB4, bool TAIL2>
-static int occ_one(const SearchArgs &a) {
-  auto fn = pick<T, NB4, TAIL2>(a);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess) return 0;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, a.smem_bytes) != cudaSuccess) return 0;
-  return n;
-}
-
-// Fully unrolled b loop for chunk widths <= 34 columns: NB4 LDS.128 groups plus an optional LDS.64
-// tail; wider chunks use the runtime loop (NB4 = 0).
-#define ALP_DISPATCH_W(CALL, T)                                              \
-  do {                                                                       \
-    const int w = a.bchunk_wpad;                                             \
-    const bool t2 = (w % 4) == 2;                                            \
-    if (w > 34) {                                                            \
-      if (t2) return CALL(T, 0, true);                                       \
-      return CALL(T, 0, false);                                              \
-    }                                                                        \
-    switch (w) {                                                             \
-      case 2: return CALL(T, 0, true);                                       \
-      case 4: return CALL(T, 1, false); case 6: return CALL(T, 1, true);     \
-      case 8: return CALL(T, 2, false); case 10: return CALL(T, 2, true);    \
-      case 12: return CALL(T, 3, false); case 14: return CALL(T, 3, true);   \
-      case 16: return CALL(T, 4, false); case 18: return CALL(T, 4, true);   \
-      case 20: return CALL(T, 5, false); case 22: return CALL(T, 5, true);   \
-      case 24: return CALL(T, 6, false); case 26: return CALL(T, 6, true);   \
-      case 28: return CALL(T, 7, false); case 30: return CALL(T, 7, true);   \
-      case 32: return CALL(T, 8, false); case 34: return CALL(T, 8, true);   \
-      default: if (t2) return CALL(T, 0, true); return CALL(T, 0, false);    \
-    }                                                                        \
-  } while (0)
-
-#define ALP_DISPATCH(CALL)                  \
-  do {                                      \
-    if (a.rows_per_lane == 16) ALP_DISPATCH_W(CALL, 16); \
-    ALP_DISPATCH_W(CALL, 8);                \
-  } while (0)
+// ------------------------------------------------------------------ search kernel (K2) dispatch
+// The kernel templates live in alp_search.cuh; each rows-per-lane value is its own translation unit.
+cudaError_t launch_search_t8(const SearchArgs &a, int grid, cudaStream_t st);
+cudaError_t launch_search_t16(const SearchArgs &a, int grid, cudaStream_t st);
+int occ_search_t8(const SearchArgs &a);
+int occ_search_t16(const SearchArgs &a);
 
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st) {
-#define CALL(T, N, T2) launch_one<T, N, T2>(a, grid, st)
-  ALP_DISPATCH(CALL);
-#undef CALL
+  return a.rows_per_lane == 16 ? launch_search_t16(a, grid, st) : launch_search_t8(a, grid, st);
 }
 
 int search_max_blocks_per_sm(const SearchArgs &a) {
-#define CALL(T, N, T2) occ_one<T, N, T2>(a)
-  ALP_DISPATCH(CALL);
-#undef CALL
+  return a.rows_per_lane == 16 ? occ_search_t16(a) : occ_search_t8(a);
 }
 
 // ------------------------------------------------------------------ finalize (K3)
