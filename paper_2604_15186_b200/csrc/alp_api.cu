@@ -199,6 +199,7 @@ struct alp_s {
   int last_launches = 0;
   uint64_t h2d = 0;
   SearchArgs last_args{};
+  std::map<long long, int> occ_cache;  // (smem bytes, b width, T, MB) -> resident blocks per SM
 
   DevProfiles dprof() const {
     DevProfiles d;
@@ -541,7 +542,11 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.min_blocks = h->min_blocks;
   a.dv = h->d_dv; a.dcnt = h->d_dcnt;
   a.t_begin = 0; a.t_end = n_targets; a.c_begin = 0; a.c_end = a.n_bchunks;
-  int bps = search_max_blocks_per_sm(a);
+  // occupancy per kernel variant and smem size (cached: the query costs microseconds per search)
+  const long long okey = ((long long)a.smem_bytes << 24) | ((long long)a.bchunk_wpad << 8) |
+                         ((long long)a.rows_per_lane << 3) | a.min_blocks;
+  auto oit = h->occ_cache.find(okey);
+  const int bps = (oit != h->occ_cache.end()) ? oit->second : (h->occ_cache[okey] = search_max_blocks_per_sm(a));
   if (bps < 1) return fail(ALP_ECUDA, "search kernel cannot be resident (smem %d B)", a.smem_bytes);
   g.grid = h->sm_count * bps;
   return ALP_OK;

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+
 #include "alp_internal.h"
 
 #ifndef ALP_A_UNROLL
@@ -356,10 +359,24 @@ static auto pick(const SearchArgs &a) {
   return k_search<T, NB4, TAIL2, kLo>;
 }
 
+// cudaFuncSetAttribute only when a kernel needs more dynamic smem than already granted (per device)
+static cudaError_t ensure_smem(const void *fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> granted;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int &g = granted[{fn, dev}];
+  if (bytes <= g) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) g = bytes;
+  return e;
+}
+
 template <int T, int NB4, bool TAIL2>
 static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
   auto fn = pick<T, NB4, TAIL2>(a);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
+  cudaError_t e = ensure_smem(reinterpret_cast<const void *>(fn), a.smem_bytes);
   if (e != cudaSuccess) return e;
   fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
   return cudaGetLastError();
@@ -368,7 +385,7 @@ static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
 template <int T, int NB4, bool TAIL2>
 static int occ_one(const SearchArgs &a) {
   auto fn = pick<T, NB4, TAIL2>(a);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess) return 0;
+  if (ensure_smem(reinterpret_cast<const void *>(fn), a.smem_bytes) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, a.smem_bytes) != cudaSuccess) return 0;
   return n;
