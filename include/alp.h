@@ -141,6 +141,16 @@ alp_status alp_schedule_egalitarian(alp_t *const *hs, const double *targets, int
                                     int32_t units_per_gpu, int32_t *gpus_out, alp_result *results_out,
                                     double *min_utility, double *sum_utility);
 
+/* Workflow statistics from execution traces (the input side of alp_build):
+ * n_m = invocations of LLM m per workflow request; p_m = request-level parallelism, the time
+ * average of the number of concurrently running invocations of m over the intervals where it is
+ * >= 1, averaged over requests weighted by each request's busy time for m
+ * = sum_r (summed durations) / sum_r (length of the union of m's intervals in request r); 1 for an
+ * LLM with no (or only zero-length) invocations.  Host computation (traces are small).
+ * Invocation i: request req[i] in [0, n_req), LLM llm[i] in [0, M), start[i] <= end[i] (seconds). */
+alp_status alp_workflow_stats(int32_t n_req, int32_t M, int64_t n_inv, const int32_t *req, const int32_t *llm,
+                              const double *start, const double *end, double *n_out, double *p_out);
+
 /* ---- multi-GPU building blocks (PyTorch owns memory, streams and the process group) ----
  * The candidate space is cut into equal-cost work items; rank r of world w gets the contiguous
  * item range [lo, hi).  Every rank calls alp_search_shard on its range (async on `stream`),

@@ -51,7 +51,7 @@ class _Result(ctypes.Structure):
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
            "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_error",
-           "alp_plan_cache_clear", "alp_search_queries", "alp_schedule_egalitarian"]
+           "alp_plan_cache_clear", "alp_search_queries", "alp_schedule_egalitarian", "alp_workflow_stats"]
 
 _lib = None
 
@@ -78,6 +78,7 @@ def lib():
             "alp_last_error": (ctypes.c_char_p, []), "alp_plan_cache_clear": (None, []),
             "alp_search_queries": (i32, [vp, vp, vp, i32, vp]),
             "alp_schedule_egalitarian": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp]),
+            "alp_workflow_stats": (i32, [i32, i32, i64, vp, vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -105,6 +106,19 @@ def schedule_egalitarian(alps: Sequence["Alp"], targets: Sequence[float], gpus: 
     _check(lib().alp_schedule_egalitarian(hs, t.ctypes.data, W, gpus, units_per_gpu, g.ctypes.data, out,
                                           ctypes.byref(mn), ctypes.byref(sm)), (ALP_OK, ALP_EINFEASIBLE))
     return g.tolist(), [Result._from(x) for x in out], mn.value, sm.value
+
+
+def workflow_stats(n_req: int, M: int, req, llm, start, end):
+    """alp_workflow_stats: (n_m, p_m) per LLM from invocation records."""
+    r = _arr(req, np.int32)
+    l = _arr(llm, np.int32)
+    s = _arr(start, np.float64)
+    e = _arr(end, np.float64)
+    n = np.zeros(M, np.float64)
+    p = np.zeros(M, np.float64)
+    _check(lib().alp_workflow_stats(n_req, M, len(r), r.ctypes.data, l.ctypes.data, s.ctypes.data, e.ctypes.data,
+                                    n.ctypes.data, p.ctypes.data))
+    return n, p
 
 
 def _check(st: int, ok=(ALP_OK,)) -> int:

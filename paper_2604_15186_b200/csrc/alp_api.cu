@@ -1036,6 +1036,59 @@ alp_status alp_schedule_egalitarian(alp_t *const *hs, const double *targets, int
   return all ? ALP_OK : ALP_EINFEASIBLE;
 }
 
+alp_status alp_workflow_stats(int32_t n_req, int32_t M, int64_t n_inv, const int32_t *req, const int32_t *llm,
+                              const double *start, const double *end, double *n_out, double *p_out) {
+  if (n_req < 1) return fail(ALP_EINVAL, "n_req must be >= 1 (empty trace list)");
+  if (M < 1 || M > ALP_MAX_M) return fail(ALP_EINVAL, "M must be in 1..%d", ALP_MAX_M);
+  if (n_inv < 0 || (n_inv > 0 && (!req || !llm || !start || !end))) return fail(ALP_EINVAL, "NULL invocation arrays");
+  if (!n_out || !p_out) return fail(ALP_EINVAL, "n_out/p_out is NULL");
+  for (int64_t i = 0; i < n_inv; ++i) {
+    if (req[i] < 0 || req[i] >= n_req) return fail(ALP_EINVAL, "req[%lld] out of range", (long long)i);
+    if (llm[i] < 0 || llm[i] >= M) return fail(ALP_EINVAL, "llm[%lld] out of range", (long long)i);
+    if (!std::isfinite(start[i]) || !std::isfinite(end[i]) || end[i] < start[i])
+      return fail(ALP_EINVAL, "invocation %lld: need finite start <= end", (long long)i);
+  }
+  // group invocations by (request, LLM), sorted by start; per group: summed durations and the length
+  // of the union of the intervals (busy time).  p_m = sum_r dur_rm / sum_r busy_rm, i.e. the
+  // busy-time-weighted average over requests of the time-averaged concurrency.
+  std::vector<int64_t> order(n_inv);
+  std::iota(order.begin(), order.end(), (int64_t)0);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    if (req[a] != req[b]) return req[a] < req[b];
+    if (llm[a] != llm[b]) return llm[a] < llm[b];
+    if (start[a] != start[b]) return start[a] < start[b];
+    return a < b;
+  });
+  std::vector<double> dur(M, 0.0), busy(M, 0.0);
+  std::vector<int64_t> cnt(M, 0);
+  for (int64_t i = 0; i < n_inv;) {
+    const int r = req[order[i]], m = llm[order[i]];
+    double lo = start[order[i]], hi = end[order[i]], d = 0.0, b = 0.0;
+    int64_t j = i;
+    for (; j < n_inv && req[order[j]] == r && llm[order[j]] == m; ++j) {
+      const int64_t k = order[j];
+      d += end[k] - start[k];
+      if (start[k] > hi) {  // gap: close the current busy run
+        b += hi - lo;
+        lo = start[k];
+        hi = end[k];
+      } else if (end[k] > hi) {
+        hi = end[k];
+      }
+    }
+    b += hi - lo;
+    dur[m] += d;
+    busy[m] += b;
+    cnt[m] += j - i;
+    i = j;
+  }
+  for (int m = 0; m < M; ++m) {
+    n_out[m] = (double)cnt[m] / (double)n_req;
+    p_out[m] = busy[m] > 0.0 ? dur[m] / busy[m] : 1.0;  // never invoked / zero-length busy: 1
+  }
+  return ALP_OK;
+}
+
 float alp_last_kernel_ms(const alp_t *h) {
   if (!h) return 0.f;
   alp_s *m = const_cast<alp_s *>(h);
