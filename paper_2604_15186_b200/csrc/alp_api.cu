@@ -86,7 +86,8 @@ struct Arena {
     static std::mutex mu;
     static void *pinned = nullptr;
     static size_t pinned_bytes = 0;
-    cudaError_t e = cudaMalloc(base, total ? total : 1);
+    // stream-ordered allocation from the device's default memory pool (kept warm across handles)
+    cudaError_t e = cudaMallocAsync(base, total ? total : 1, st);
     if (e != cudaSuccess) return e;
     if (copied) {
       std::lock_guard<std::mutex> lock(mu);
@@ -218,7 +219,8 @@ struct alp_s {
     g_keys.release();
     g_counts.release();
     d_punits.release();
-    if (d_arena) cudaFree(d_arena);
+    if (d_arena) cudaFreeAsync(d_arena, stream);
+    if (stream) cudaStreamSynchronize(stream);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -473,6 +475,13 @@ alp_status init_device(alp_s *h) {
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  {  // keep freed handle memory in the default pool so the next alp_build reuses it cheaply
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   CU(cudaEventCreate(&h->ev0));
   CU(cudaEventCreate(&h->ev1));
   return ALP_OK;
