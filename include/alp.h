@@ -151,6 +151,16 @@ alp_status alp_schedule_egalitarian(alp_t *const *hs, const double *targets, int
 alp_status alp_workflow_stats(int32_t n_req, int32_t M, int64_t n_inv, const int32_t *req, const int32_t *llm,
                               const double *start, const double *end, double *n_out, double *p_out);
 
+/* Topology-aware placement of an allocation ("hierarchical placement",
+ * most-constrained-first; SPEC.md:440-445 tie-breaks).  Cluster: G GPUs of F units; gpu_node[g],
+ * gpu_domain[g] = node and NVLink domain of GPU g (a domain never spans nodes).  Allocation: per LLM
+ * share_units (per shard, 1..F), tp, replicas; every replica is a tensor group of tp shards.
+ * Output shard_gpu[sum_m tp_m*replicas_m], ordered (LLM, replica, shard): the GPU of each shard.
+ * Tensor groups use distinct GPUs of one NVLink domain.  ALP_EINFEASIBLE names the first shard
+ * group that cannot be placed. */
+alp_status alp_place(int32_t G, int32_t F, const int32_t *gpu_node, const int32_t *gpu_domain, int32_t M,
+                     const int32_t *share_units, const int32_t *tp, const int32_t *replicas, int32_t *shard_gpu);
+
 /* ---- multi-GPU building blocks (PyTorch owns memory, streams and the process group) ----
  * The candidate space is cut into equal-cost work items; rank r of world w gets the contiguous
  * item range [lo, hi).  Every rank calls alp_search_shard on its range (async on `stream`),

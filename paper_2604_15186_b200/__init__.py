@@ -51,7 +51,8 @@ class _Result(ctypes.Structure):
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
            "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_error",
-           "alp_plan_cache_clear", "alp_search_queries", "alp_schedule_egalitarian", "alp_workflow_stats"]
+           "alp_plan_cache_clear", "alp_search_queries", "alp_schedule_egalitarian", "alp_workflow_stats",
+           "alp_place"]
 
 _lib = None
 
@@ -79,6 +80,7 @@ def lib():
             "alp_search_queries": (i32, [vp, vp, vp, i32, vp]),
             "alp_schedule_egalitarian": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp]),
             "alp_workflow_stats": (i32, [i32, i32, i64, vp, vp, vp, vp, vp, vp]),
+            "alp_place": (i32, [i32, i32, vp, vp, i32, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -119,6 +121,19 @@ def workflow_stats(n_req: int, M: int, req, llm, start, end):
     _check(lib().alp_workflow_stats(n_req, M, len(r), r.ctypes.data, l.ctypes.data, s.ctypes.data, e.ctypes.data,
                                     n.ctypes.data, p.ctypes.data))
     return n, p
+
+
+def place(gpu_node, gpu_domain, F: int, share_units, tp, replicas):
+    """alp_place: GPU index of every shard, ordered (LLM, replica, shard)."""
+    gn = _arr(gpu_node, np.int32)
+    gd = _arr(gpu_domain, np.int32)
+    s = _arr(share_units, np.int32)
+    t = _arr(tp, np.int32)
+    r = _arr(replicas, np.int32)
+    out = np.zeros(int((t * r).sum()), np.int32)
+    _check(lib().alp_place(len(gn), F, gn.ctypes.data, gd.ctypes.data, len(s), s.ctypes.data, t.ctypes.data,
+                           r.ctypes.data, out.ctypes.data))
+    return out.tolist()
 
 
 def _check(st: int, ok=(ALP_OK,)) -> int:

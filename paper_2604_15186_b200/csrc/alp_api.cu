@@ -1098,6 +1098,115 @@ alp_status alp_workflow_stats(int32_t n_req, int32_t M, int64_t n_inv, const int
   return ALP_OK;
 }
 
+// Topology-aware placement of a chosen allocation (PAPER.md:411-416
+// "Hierarchical placement algorithm"; tie-breaks and the imbalance definition from).
+//
+// Host code (alp_place): the placement is a short sequential heuristic over a handful of shards (the paper
+// calls the optimum NP-hard and uses this greedy; it runs once per chosen allocation).
+//  * every replica of LLM m is a tensor group of tp_m shards demanding share_units_m units each;
+//  * groups are placed most-constrained-first: tensor-parallel groups before single shards, larger
+//    total demand first, then (LLM, replica) order;
+//  * a tensor group goes to one NVLink domain: among domains with tp free GPUs of enough capacity
+//    keep those with the smallest imbalance (max - min free units over the domain's GPUs), then
+//    the least total free capacity, then the lowest (node, domain); inside it the tp GPUs with the
+//    least sufficient free units (lowest index on ties);
+//  * single shards are packed onto already occupied GPUs first, best fit by free units, then onto
+//    empty GPUs; ties by (node, GPU index).
+alp_status alp_place(int32_t G, int32_t F, const int32_t *gpu_node, const int32_t *gpu_domain, int32_t M,
+                     const int32_t *share_units, const int32_t *tp, const int32_t *replicas, int32_t *shard_gpu) {
+  if (G < 1 || F < 1) return fail(ALP_EINVAL, "need G >= 1 GPUs and F >= 1 units per GPU");
+  if (!gpu_node || !gpu_domain || !share_units || !tp || !replicas || !shard_gpu)
+    return fail(ALP_EINVAL, "NULL argument");
+  if (M < 1) return fail(ALP_EINVAL, "M must be >= 1");
+  std::map<int, int> dom_node;
+  for (int g = 0; g < G; ++g) {
+    auto it = dom_node.find(gpu_domain[g]);
+    if (it != dom_node.end() && it->second != gpu_node[g])
+      return fail(ALP_EINVAL, "NVLink domain %d spans nodes", gpu_domain[g]);
+    dom_node[gpu_domain[g]] = gpu_node[g];
+  }
+  struct Group {
+    int m, r, tp, units, first;  // first = index of the group's first shard in shard_gpu
+  };
+  std::vector<Group> groups;
+  int shards = 0;
+  long long demand = 0;
+  for (int m = 0; m < M; ++m) {
+    if (share_units[m] < 1 || share_units[m] > F || tp[m] < 1 || replicas[m] < 1)
+      return fail(ALP_EINVAL, "LLM %d: need 1 <= share_units <= F, tp >= 1, replicas >= 1", m);
+    for (int r = 0; r < replicas[m]; ++r) {
+      groups.push_back({m, r, tp[m], share_units[m], shards});
+      shards += tp[m];
+      demand += (long long)tp[m] * share_units[m];
+    }
+  }
+  if (demand > (long long)G * F)
+    return fail(ALP_EINFEASIBLE, "demand %lld units exceeds the cluster's %lld", demand, (long long)G * F);
+  std::stable_sort(groups.begin(), groups.end(), [](const Group &a, const Group &b) {
+    const bool ta = a.tp > 1, tb = b.tp > 1;
+    if (ta != tb) return ta;
+    const long long ua = (long long)a.tp * a.units, ub = (long long)b.tp * b.units;
+    if (ua != ub) return ua > ub;
+    return a.m != b.m ? a.m < b.m : a.r < b.r;
+  });
+  std::vector<int> free_units(G, F);
+  // domains in (node, domain id) order with their GPUs in index order
+  std::map<std::pair<int, int>, std::vector<int>> domains;
+  for (int g = 0; g < G; ++g) domains[{gpu_node[g], gpu_domain[g]}].push_back(g);
+  for (const Group &grp : groups) {
+    if (grp.tp > 1) {
+      const std::vector<int> *best = nullptr;
+      long long best_imb = 0, best_cap = 0;
+      for (const auto &kv : domains) {
+        const std::vector<int> &gs = kv.second;
+        int fit = 0, mx = 0, mn = F;
+        long long cap = 0;
+        for (int g : gs) {
+          fit += free_units[g] >= grp.units;
+          mx = std::max(mx, free_units[g]);
+          mn = std::min(mn, free_units[g]);
+          cap += free_units[g];
+        }
+        if (fit < grp.tp) continue;
+        const long long imb = mx - mn;
+        if (!best || imb < best_imb || (imb == best_imb && cap < best_cap)) {
+          best = &gs;
+          best_imb = imb;
+          best_cap = cap;
+        }
+      }
+      if (!best)
+        return fail(ALP_EINFEASIBLE, "no NVLink domain fits LLM %d replica %d (tp %d x %d units)", grp.m, grp.r,
+                    grp.tp, grp.units);
+      std::vector<int> cand;
+      for (int g : *best)
+        if (free_units[g] >= grp.units) cand.push_back(g);
+      std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return free_units[a] < free_units[b]; });
+      std::vector<int> chosen(cand.begin(), cand.begin() + grp.tp);
+      std::sort(chosen.begin(), chosen.end());
+      for (int s = 0; s < grp.tp; ++s) {
+        shard_gpu[grp.first + s] = chosen[s];
+        free_units[chosen[s]] -= grp.units;
+      }
+    } else {
+      int pick = -1;
+      for (int pass = 0; pass < 2 && pick < 0; ++pass) {  // occupied GPUs first, then empty ones
+        for (int g = 0; g < G; ++g) {
+          const bool occupied = free_units[g] < F;
+          if ((pass == 0) != occupied || free_units[g] < grp.units) continue;
+          if (pick < 0 || free_units[g] < free_units[pick]) pick = g;
+        }
+      }
+      if (pick < 0)
+        return fail(ALP_EINFEASIBLE, "no GPU fits LLM %d replica %d (%d units)", grp.m, grp.r, grp.units);
+      shard_gpu[grp.first] = pick;
+      free_units[pick] -= grp.units;
+    }
+  }
+  return ALP_OK;
+}
+
+
 float alp_last_kernel_ms(const alp_t *h) {
   if (!h) return 0.f;
   alp_s *m = const_cast<alp_s *>(h);

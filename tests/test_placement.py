@@ -1,0 +1,75 @@
+"""NEXT-3: topology-aware placement (alp_place, host library code) vs the placement oracle."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import placement as op
+
+
+def _pairs(n_gpus):  # one node, NVLink pairs {0,1}, {2,3}, ... ("connected in two pairs")
+    return [0] * n_gpus, [g // 2 for g in range(n_gpus)]
+
+
+def test_spec_example_least_capacity_balanced_pair():
+    # with both NVLink pairs feasible, the occupied (least-capacity) balanced pair wins
+    import paper_2604_15186_b200 as P
+    node, dom = _pairs(4)
+    out = P.place(node, dom, 10, [5], [2], [2])   # two tp=2 groups of 5 units
+    assert out == [0, 1, 0, 1]
+    assert op.validate(node, dom, 10, [5], [2], [2], out) == []
+
+
+def test_spec_example_best_fit_fractions():
+    # fractions 6,6,4,4 onto 2 GPUs of F=10 -> {6,4} and {6,4}
+    import paper_2604_15186_b200 as P
+    out = P.place([0, 0], [0, 1], 10, [6, 4], [1, 1], [2, 2])
+    assert out == [0, 1, 0, 1]
+
+
+def test_demand_exceeding_capacity_fails():
+    import paper_2604_15186_b200 as P
+    with pytest.raises(P.AlpError, match="exceeds"):
+        P.place([0, 0], [0, 0], 4, [4], [1], [3])
+
+
+def test_fragmentation_trap():
+    # SPEC.md:456 / PAPER.md:413: small fractions placed first could block the only NVLink pair
+    # that can host a tp=2 whole-GPU group; most-constrained-first places the tensor group first.
+    import paper_2604_15186_b200 as P
+    node, dom = [0, 0, 0], [0, 0, 1]
+    out = P.place(node, dom, 4, [1, 4], [1, 2], [4, 1])
+    assert op.validate(node, dom, 4, [1, 4], [1, 2], [4, 1], out) == []
+    assert out[4:] == [0, 1]
+
+
+def test_random_instances_vs_exact():
+    import paper_2604_15186_b200 as P
+    rng = np.random.default_rng(3)
+    ok = feasible = 0
+    for _ in range(150):
+        G = int(rng.integers(1, 7))
+        F = int(rng.choice([2, 4, 8]))
+        node = [0] * G
+        dom = [g // int(rng.choice([1, 2, 4])) for g in range(G)]
+        M = int(rng.integers(1, 4))
+        s = [int(rng.integers(1, F + 1)) for _ in range(M)]
+        t = [int(rng.choice([1, 1, 2])) for _ in range(M)]
+        d = [int(rng.integers(1, 3)) for _ in range(M)]
+        exact = op.exact_place(node, dom, F, s, t, d)
+        try:
+            out = P.place(node, dom, F, s, t, d)
+        except P.AlpError:
+            out = None
+        if out is not None:
+            assert op.validate(node, dom, F, s, t, d, out) == []
+            assert exact  # a heuristic success is a witness
+            ok += 1
+        feasible += exact
+    assert feasible > 20 and ok >= 0.8 * feasible
+
+
+def test_validate_catches_violations():
+    node, dom = _pairs(4)
+    assert op.validate(node, dom, 10, [5], [2], [1], [0, 2])  # tensor group spans pairs
+    assert op.validate(node, dom, 10, [6], [1], [2], [0, 0])  # GPU over capacity
