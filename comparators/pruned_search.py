@@ -108,10 +108,10 @@ def pruned_search(alp, d: dict, lam: float, gpus: int, nvlink: int = 8, batch: i
     base = kidx.get((F, 1, 1))
     if base is None:
         raise ValueError("the grid needs the baseline option (share F, tp 1, d 1)")
-    lam_ref = min(lam, float(min(tab["b"][m][base] for m in range(M))))
+    # (just below the smallest baseline Eq. 2 term: at b itself x may exceed T by one rounding)
+    lam_ref = min(lam, 0.999999 * float(min(tab["b"][m][base] for m in range(M))))
     tref = alp.option_table(lam_ref, K)["term"][:, base]
-    ratios = tref / tref.sum()
-    order = sorted(range(M), key=lambda m: (-ratios[m], m))
+    order = sorted(range(M), key=lambda m: (-tref[m], m))  # descending latency ratio
     mins = [1] * M
     mu = d.get("min_units")
     if mu is not None:
