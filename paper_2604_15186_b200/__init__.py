@@ -168,18 +168,11 @@ def _arr(x, dt):
     return np.ascontiguousarray(np.asarray(x, dtype=dt))
 
 
-class Alp:
-    """Handle to an immutable ALP (alp_t).  Not thread-safe; one handle per host thread."""
+class Desc:
+    """Host-side alp_desc: the profile tables and workflow statistics of an instance dict
+    (workloads/instances/*.json layout) as contiguous arrays, kept alive with the struct."""
 
-    def __init__(self, handle: int, M: int, keep: Any = None):
-        self._h = ctypes.c_void_p(handle)
-        self.M = M
-        self._keep = keep
-
-    # ------------------------------------------------------------------ construction
-    @classmethod
-    def from_instance(cls, d: dict, percentile: str | None = None) -> "Alp":
-        """alp_build from an instance dict (workloads/instances/*.json layout)."""
+    def __init__(self, d: dict, percentile: str | None = None):
         M, T = d["M"], d["tp"]
         off, rate, lat, tmax = [0], [], {k: [] for k in PCT}, []
         for m in range(M):
@@ -197,20 +190,46 @@ class Alp:
         mu = d.get("min_units")
         if mu is not None:
             keep["minu"] = _arr(mu, np.int32).reshape(-1)
-        desc = _Desc()
-        desc.M, desc.F = M, d["F"]
-        desc.n, desc.p = keep["n"].ctypes.data, keep["p"].ctypes.data
-        desc.nS, desc.nT, desc.nR = len(keep["S"]), len(keep["T"]), len(keep["R"])
-        desc.share_units, desc.tp, desc.replicas = keep["S"].ctypes.data, keep["T"].ctypes.data, keep["R"].ctypes.data
-        desc.prof_off, desc.rate = keep["off"].ctypes.data, keep["rate"].ctypes.data
+        c = _Desc()
+        c.M, c.F = M, d["F"]
+        c.n, c.p = keep["n"].ctypes.data, keep["p"].ctypes.data
+        c.nS, c.nT, c.nR = len(keep["S"]), len(keep["T"]), len(keep["R"])
+        c.share_units, c.tp, c.replicas = keep["S"].ctypes.data, keep["T"].ctypes.data, keep["R"].ctypes.data
+        c.prof_off, c.rate = keep["off"].ctypes.data, keep["rate"].ctypes.data
         for k, i in PCT.items():
-            desc.lat[i] = keep[f"lat_{k}"].ctypes.data
-        desc.tmax = keep["tmax"].ctypes.data
-        desc.min_units = keep["minu"].ctypes.data if "minu" in keep else None
-        desc.pct = PCT[percentile or d.get("percentile", "mean")]
+            c.lat[i] = keep[f"lat_{k}"].ctypes.data
+        c.tmax = keep["tmax"].ctypes.data
+        c.min_units = keep["minu"].ctypes.data if "minu" in keep else None
+        c.pct = PCT[percentile or d.get("percentile", "mean")]
+        self.c, self.M, self._keep = c, M, keep
+
+    @property
+    def nbytes(self) -> int:
+        """Bytes of the arrays alp_build reads (the selected latency column only)."""
+        sel = {"lat_" + k for k, i in PCT.items() if i == self.c.pct}
+        return int(sum(v.nbytes for k, v in self._keep.items() if not k.startswith("lat_") or k in sel))
+
+
+class Alp:
+    """Handle to an immutable ALP (alp_t).  Not thread-safe; one handle per host thread."""
+
+    def __init__(self, handle: int, M: int, keep: Any = None):
+        self._h = ctypes.c_void_p(handle)
+        self.M = M
+        self._keep = keep
+
+    # ------------------------------------------------------------------ construction
+    @classmethod
+    def from_instance(cls, d: dict, percentile: str | None = None) -> "Alp":
+        """alp_build from an instance dict (workloads/instances/*.json layout)."""
+        return cls.build(Desc(d, percentile))
+
+    @classmethod
+    def build(cls, desc: "Desc") -> "Alp":
+        """alp_build from prepared host arrays (Desc)."""
         h = ctypes.c_void_p()
-        _check(lib().alp_build(ctypes.byref(desc), ctypes.byref(h)))
-        return cls(h.value, M)
+        _check(lib().alp_build(ctypes.byref(desc.c), ctypes.byref(h)))
+        return cls(h.value, desc.M)
 
     @classmethod
     def from_terms(cls, tau: np.ndarray, u: np.ndarray) -> "Alp":
