@@ -158,12 +158,10 @@ struct alp_s {
   int a_llm = -1, b_llm = 0, Ka = 1, Kb = 1, g0 = 0, g1 = 0, ng = 0, dig_bits = 1;
   uint32_t L = 1, n_chunks = 1, n_groups = 1, nQ = 1, A = 1;
   uint32_t pw[ALP_MAX_M] = {0};
-  std::vector<int> tile_s, bperm, bu, dv, dcnt, a_order;
-  std::vector<int4> cls_info;
+  std::vector<int> tile_s, bperm, bu, dv, dcnt;
   std::vector<uint32_t> tile_e, tile_off;
   int rows_per_lane = 8;
   int min_blocks = 0;  // 0: per rows-per-lane default (T = 8: 3 blocks/SM, T = 16: 2); ALP_BLOCKS_PER_SM overrides
-  int use_cls = 1;  // ALP_CLASS_PATH=0 disables the a-class path
   int umax_a = 0, umax_b = 0;
   long long umax_total = 0;
   // device
@@ -172,9 +170,7 @@ struct alp_s {
   void *d_arena = nullptr;  // every static table + single-target scratch (one allocation)
   double *d_n = nullptr, *d_p = nullptr, *d_rate = nullptr, *d_lat = nullptr, *d_tmax = nullptr;
   int *d_S = nullptr, *d_T = nullptr, *d_R = nullptr, *d_off = nullptr, *d_minu = nullptr, *d_u = nullptr;
-  int *d_tile_s = nullptr, *d_bperm = nullptr, *d_dv = nullptr, *d_dcnt = nullptr, *d_a_order = nullptr;
-  int4 *d_cls_info = nullptr;
-  int n_cls = 0;
+  int *d_tile_s = nullptr, *d_bperm = nullptr, *d_dv = nullptr, *d_dcnt = nullptr;
   uint32_t *d_tile_e = nullptr, *d_tile_off = nullptr;
   float *d_tau_fixed = nullptr;
   double *d_term_fixed = nullptr, *d_b_fixed = nullptr;
@@ -340,20 +336,6 @@ alp_status make_plan(alp_s *h) {
   h->dcnt.assign(h->dv.size() + 1, 0);
   for (size_t i = 1; i <= h->dv.size(); ++i)
     h->dcnt[i] = (int)(std::upper_bound(h->bu.begin(), h->bu.end(), h->dv[i - 1]) - h->bu.begin());
-  // a options sorted by units (stable); runs of equal units form classes that share a masked row
-  h->a_order.resize(h->Ka);
-  std::iota(h->a_order.begin(), h->a_order.end(), 0);
-  h->cls_info.clear();
-  if (h->a_llm >= 0) {
-    std::stable_sort(h->a_order.begin(), h->a_order.end(), [&](int a, int b) { return U(h->a_llm, a) < U(h->a_llm, b); });
-    for (int j = 0; j < h->Ka;) {
-      int e = j;
-      while (e < h->Ka && U(h->a_llm, h->a_order[e]) == U(h->a_llm, h->a_order[j])) ++e;
-      h->cls_info.push_back(make_int4(j, e, -U(h->a_llm, h->a_order[j]), 0));
-      j = e;
-    }
-  }
-  h->n_cls = (int)h->cls_info.size();
   h->umax_b = h->bu.back();
   h->umax_a = 0;
   if (h->a_llm >= 0)
@@ -387,9 +369,7 @@ struct PlanSnap {
   uint32_t pw[ALP_MAX_M];
   long long umax_total;
   std::vector<int> dv;
-  int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt, *d_a_order;
-  int4 *d_cls_info;
-  int n_cls;
+  int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt;
   uint32_t *d_tile_e, *d_tile_off;
   std::shared_ptr<PlanDev> dev;
 };
@@ -430,10 +410,7 @@ alp_status get_plan(alp_s *h) {
     A.add(h->bperm, &P->d_bperm);
     A.add(h->dv, &P->d_dv);
     A.add(h->dcnt, &P->d_dcnt);
-    A.add(h->a_order, &P->d_a_order);
-    A.add(h->cls_info, &P->d_cls_info);
     CU(A.commit(&P->dev->mem, h->h2d, h->stream));
-    P->n_cls = h->n_cls;
     P->N = h->N; P->a_llm = h->a_llm; P->b_llm = h->b_llm; P->Ka = h->Ka; P->Kb = h->Kb; P->g0 = h->g0;
     P->g1 = h->g1; P->ng = h->ng; P->dig_bits = h->dig_bits; P->umax_a = h->umax_a; P->umax_b = h->umax_b;
     P->L = h->L; P->n_chunks = h->n_chunks; P->n_groups = h->n_groups; P->nQ = h->nQ; P->A = h->A;
@@ -451,7 +428,6 @@ alp_status get_plan(alp_s *h) {
   h->dv = P->dv;
   h->d_u = P->d_u; h->d_tile_s = P->d_tile_s; h->d_tile_e = P->d_tile_e; h->d_tile_off = P->d_tile_off;
   h->d_bperm = P->d_bperm; h->d_dv = P->d_dv; h->d_dcnt = P->d_dcnt;
-  h->d_a_order = P->d_a_order; h->d_cls_info = P->d_cls_info; h->n_cls = P->n_cls;
   h->plan_dev = P->dev;
   return ALP_OK;
 }
@@ -496,7 +472,6 @@ alp_status init_device(alp_s *h) {
   h->rows_per_lane = (h->K >= 64) ? 16 : 8;
   if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 16) ? 16 : 8;
   if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = std::min(4, std::max(2, atoi(v)));
-  if (const char *v = getenv("ALP_CLASS_PATH")) h->use_cls = atoi(v) != 0;
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -564,7 +539,6 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
     a.off_lut = off; off = align16(off + (a.budget + 2) * 8);
     a.off_tmp = off; off = align16(off + (2 * h->Kb + 3) * 4);
     a.off_btab = off; off = align16(off + rows * a.row_stride * 4);
-    a.off_cls = off; off = align16(off + h->n_cls * 16);
     a.smem_bytes = off;
     return off;
   };
@@ -576,9 +550,6 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.rows_per_lane = h->rows_per_lane;
   a.min_blocks = h->min_blocks;
   a.dv = h->d_dv; a.dcnt = h->d_dcnt;
-  a.a_order = h->d_a_order; a.cls_info = h->d_cls_info; a.n_cls = h->n_cls;
-  // class path: whole rows per item (segments start at a = 0) and short b rows kept in registers
-  a.cls_path = (h->a_llm >= 0 && h->nQ == 1 && a.n_bchunks == 1 && a.bchunk_wpad <= 22 && h->use_cls) ? 1 : 0;
   a.t_begin = 0; a.t_end = n_targets; a.c_begin = 0; a.c_end = a.n_bchunks;
   // occupancy per kernel variant and smem size (cached: the query costs microseconds per search)
   const long long okey = ((long long)a.smem_bytes << 24) | ((long long)a.bchunk_wpad << 8) |

@@ -63,10 +63,6 @@ struct SearchArgs {
   int rows_per_lane;     // T (8 or 16)
   int min_blocks;        // launch-bounds variant for T = 8 (3 or 4 blocks/SM)
   int t_begin, t_end, c_begin, c_end;  // phases (target, b-chunk) evaluated by this launch
-  int cls_path;          // 1: a options visited in unit-sorted classes sharing one masked row (nQ == 1)
-  int n_cls;             // number of a classes (equal units)
-  const int *a_order;    // [Ka] canonical a option at sorted position
-  const int4 *cls_info;  // [n_cls] {first, end (sorted positions), -u, 0}
   const int *bperm;      // [Kb] canonical option of u-sorted column j
   const int *dv;         // [Dall] distinct b unit values, ascending
   const int *dcnt;       // [Dall+1] dcnt[i] = #u-sorted columns with u <= dv[i-1] (dcnt[0] = 0)
@@ -75,7 +71,7 @@ struct SearchArgs {
   unsigned long long *keys;
   unsigned long long *counts;
   // shared memory layout (byte offsets)
-  int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, off_cls, smem_bytes;
+  int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
 };
 
 // budget of query t (per-query budgets for budget sweeps, else the common budget)

@@ -47,7 +47,6 @@ struct Smem {
   int *dv;         // [D] distinct b unit values <= R, ascending
   int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
   float *btab;     // [rows][row_stride] masked rows
-  int4 *cls;       // [n_cls] {first, end, -u, #finite a} when the class path is on
 };
 
 constexpr int kBigUnits = 1 << 28;
@@ -83,7 +82,6 @@ __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *
   s.dv = reinterpret_cast<int *>(base + P.off_tmp);
   s.dcnt = s.dv + (P.Kb + 1);
   s.btab = reinterpret_cast<float *>(base + P.off_btab);
-  s.cls = reinterpret_cast<int4 *>(base + P.off_cls);
   return s;
 }
 
@@ -100,19 +98,7 @@ __device__ inline void build_tables(const SearchArgs &P, const Smem &s, int t, i
     s.tau[P.g1 * K + 1] = finf();  // padded (dummy) row
   }
   for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
-  if (P.cls_path) {
-    // a options in unit-sorted order; per class of equal units: its range and #finite options
-    for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, P.a_order[a]);
-    for (int c = tid; c < P.n_cls; c += nt) {
-      int4 ci = P.cls_info[c];
-      int nf = 0;
-      for (int j = ci.x; j < ci.y; ++j) nf += tau_t[P.a_llm * K + P.a_order[j]] < finf() ? 1 : 0;
-      ci.w = nf;
-      s.cls[c] = ci;
-    }
-  } else {
-    for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, a);
-  }
+  for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, a);
   for (int i = tid; i < D; i += nt) s.dv[i] = P.dv[i];
   for (int i = tid; i <= D; i += nt) s.dcnt[i] = P.dcnt[i];
   __syncthreads();
@@ -294,35 +280,6 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     unsigned c32 = 0;
     const int a0 = (int)(q * P.A);
     const int a1 = min(a0 + (int)P.A, P.Ka);
-    if constexpr (NB4 > 0 && NB4 <= 5) {
-      if (P.cls_path) {
-        // a options of equal units share one masked row: load its b values once per class into
-        // registers, then stream the class's a options over them (whole row: q == 0)
-        for (int c = 0; c < P.n_cls; ++c) {
-          const int4 ci = s.cls[c];
-          const int ra = max(r_tile + ci.z, -1);
-          const int2 lu = s.lut[ra + 1];
-          c32 += (unsigned)(lu.y * ci.w);
-          float4 bv[NB4];
-#pragma unroll
-          for (int g = 0; g < NB4; ++g) bv[g] = lds128((uint32_t)lu.x + 16 * g);
-          float2 bt = make_float2(0.f, 0.f);
-          if constexpr (TAIL2) bt = lds64((uint32_t)lu.x + 16 * NB4);
-#pragma unroll 1
-          for (int j = ci.x; j < ci.y; ++j) {
-            const float ta = s.a[j].x;
-            float Qa[T];
-#pragma unroll
-            for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], ta);
-#pragma unroll
-            for (int g = 0; g < NB4; ++g) eval4<T>(bv[g], Qa, acc);
-            if constexpr (TAIL2) eval2<T>(bt, Qa, acc);
-          }
-        }
-        goto item_done;
-      }
-    }
-    {
     const float2 *ap = s.a + a0;
 #pragma unroll(kAUnroll)
     for (int a = a0; a < a1; ++a, ++ap) {
@@ -335,8 +292,6 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
       eval_row<T, NB4, TAIL2>((uint32_t)lu.x, Qa, acc, ng4);
     }
-    }
-  item_done:
     cnt += (unsigned long long)c32 * nfin;  // rows with a finite partial sum x feasible (a, b) pairs
     // advance to the next item (q fastest); fold when the lane tile changes
     if (++q == P.nQ) {
