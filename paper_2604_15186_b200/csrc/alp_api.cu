@@ -25,6 +25,7 @@ using namespace alp;
 namespace {
 
 thread_local std::string g_err = "no error";
+constexpr size_t kArenaWork = 64;  // work counters kept in the handle arena (phases of one search)
 
 alp_status fail(alp_status st, const char *fmt, ...) {
   char buf[512];
@@ -182,8 +183,9 @@ struct alp_s {
   DBuf<double> g_targets, g_term, g_b;
   DBuf<float> g_tau;
   DBuf<alp_result> g_res;
-  DBuf<unsigned long long> g_keys, g_counts;
+  DBuf<unsigned long long> g_keys, g_counts, g_work;
   int *a_qb = nullptr;
+  unsigned long long *a_work = nullptr;  // kArenaWork work counters
   DBuf<int> g_qb;
   int *s_qb = nullptr;  // per-query budgets (device) when the last search used them, else nullptr
   double *s_targets = nullptr, *s_term = nullptr, *s_b = nullptr;
@@ -218,6 +220,7 @@ struct alp_s {
     g_res.release();
     g_keys.release();
     g_counts.release();
+    g_work.release();
     d_punits.release();
     if (d_arena) cudaFreeAsync(d_arena, stream);
     if (stream) cudaStreamSynchronize(stream);
@@ -462,6 +465,7 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_keys);
   A.scratch(1, &h->a_counts);
   A.scratch(1, &h->a_qb);
+  A.scratch(kArenaWork, &h->a_work);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
   return ALP_OK;
 }
@@ -667,6 +671,17 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   int launches = 1;  // K1
   if (hi > lo) {
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
+    // work counters (one per phase) and the grab size: ~16 grabs per warp
+    const size_t nctr = (size_t)n * g.a.n_bchunks;
+    unsigned long long *work = h->a_work;
+    if (nctr > kArenaWork) {
+      CU(h->g_work.ensure(nctr));
+      work = h->g_work.p;
+    }
+    CU(cudaMemsetAsync(work, 0, nctr * sizeof(unsigned long long), st));
+    g.a.work = work;
+    const uint64_t warps = (uint64_t)g.grid * (kThreads / 32);
+    g.a.grab = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, (hi - lo) / (warps * 16)));
     CU(launch_search(g.a, g.grid, st));
     launches += 1;
   }

@@ -48,6 +48,8 @@ struct SearchArgs {
   uint32_t n_groups;     // warp groups of 32 lane tiles
   uint32_t nQ, A;        // a-ranges: a in [q*A, min((q+1)*A, Ka))
   uint64_t item_lo, item_hi;
+  unsigned long long *work;  // [n_targets * n_bchunks] work counters (zeroed before the launch)
+  int grab;              // items per dynamic work grab
   int budget;            // R (capped at the total max units); max over queries when q_budget is set
   const int *q_budget;   // [n_targets] per-query budgets (capped) or nullptr (all = budget)
   int n_targets;

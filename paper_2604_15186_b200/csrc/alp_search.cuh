@@ -210,30 +210,36 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
 
 template <int T, int NB4, bool TAIL2>
 __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
-                              uint32_t &best_seg, unsigned long long &cnt, int R) {
+                              uint32_t &best_seg, unsigned long long &cnt, int R, int work_slot) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nW = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const uint64_t n = P.item_hi - P.item_lo;
-  uint64_t it = P.item_lo + n * w / nW;
-  const uint64_t end = P.item_lo + n * (w + 1) / nW;
-  if (it >= end) return;
   const int K = P.K;
   const int ng4 = P.bchunk_wpad >> 2;
-  uint32_t q = (uint32_t)(it % P.nQ);
-  const uint64_t tq = it / P.nQ;
-  uint32_t grp = (uint32_t)(tq % P.n_groups);
-  uint32_t chunk = (uint32_t)(tq / P.n_groups);
+  // Dynamic work distribution: warps take runs of P.grab consecutive items from this phase's
+  // counter (the result is independent of who evaluates what: keys carry (value, segment) and the
+  // counts are sums).  The next run is requested while the current one is evaluated.
+  unsigned long long *ctr = P.work + work_slot;
+  unsigned long long nxt = 0;
+  if (lane == 0) nxt = atomicAdd(ctr, (unsigned long long)P.grab);
+  nxt = __shfl_sync(0xffffffffu, nxt, 0);
   // state of the lane tile currently loaded
   float Qr[T], acc[T];
   int r_tile = 0;
   unsigned nfin = 0;
-  uint32_t q0 = q, tchunk = chunk, ttile = 0;
-  bool loaded = false;
+  uint32_t q0 = 0, tchunk = 0, ttile = 0;
   float Pfx = 0.f;
   int Upfx = 0;
   uint32_t pchunk = 0xffffffffu;
   const unsigned char *tau_b = reinterpret_cast<const unsigned char *>(s.tau);
+  while (nxt < n) {
+  uint64_t it = P.item_lo + nxt;
+  const uint64_t end = P.item_lo + min((unsigned long long)n, nxt + (unsigned long long)P.grab);
+  if (lane == 0) nxt = atomicAdd(ctr, (unsigned long long)P.grab);
+  uint32_t q = (uint32_t)(it % P.nQ);
+  const uint64_t tq = it / P.nQ;
+  uint32_t grp = (uint32_t)(tq % P.n_groups);
+  uint32_t chunk = (uint32_t)(tq / P.n_groups);
+  bool loaded = false;
   for (; it < end; ++it) {
     if (!loaded) {
       if (chunk != pchunk) {
@@ -305,6 +311,8 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     }
   }
   if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
+  nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  }
 }
 
 // T = rows per lane; MB = minimum resident blocks per SM (register cap 65536 / (256 * MB)).
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, MB)
       __syncthreads();
       const int R = qbudget(P, t);
       build_tables(P, s, t, c, R);
-      process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt, R);
+      process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt, R, t * P.n_bchunks + c);
     }
     unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
 #pragma unroll
