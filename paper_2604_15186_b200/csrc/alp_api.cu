@@ -27,6 +27,33 @@ namespace {
 thread_local std::string g_err = "no error";
 constexpr size_t kArenaWork = 64;  // work counters kept in the handle arena (phases of one search)
 
+// Small pinned host buffer per host thread (allocated once, shared by all handles the thread uses)
+// for the per-search H2D of targets and D2H of results: pageable copies cost a staging hop each.
+// Two fixed halves: [0, 32 KB) feeds target H2D copies, [32 KB, 64 KB) receives result D2H copies.
+constexpr size_t kPinHalf = 32 * 1024;
+void *pinned_scratch(size_t bytes) {
+  struct Buf {
+    void *p = nullptr;
+    size_t n = 0;
+    ~Buf() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Buf b;
+  if (bytes > b.n) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    const size_t want = std::max<size_t>(bytes, 2 * kPinHalf);
+    if (cudaHostAlloc(&b.p, want, cudaHostAllocDefault) != cudaSuccess) {
+      b.p = nullptr;
+      return nullptr;
+    }
+    b.n = want;
+  }
+  return b.p;
+}
+
 alp_status fail(alp_status st, const char *fmt, ...) {
   char buf[512];
   va_list ap;
@@ -586,16 +613,27 @@ alp_status ensure_scratch(alp_s *h, int n) {
 
 // K1 for n targets into the scratch tables (profiles mode) or replicate the fixed terms.
 alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st, unsigned long long *keys,
-                         unsigned long long *counts) {
+                         unsigned long long *counts, unsigned long long *work = nullptr, int n_work = 0) {
   const size_t MK = (size_t)h->M * h->K;
-  CU(cudaMemcpyAsync(h->s_targets, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  double *pin = (n * sizeof(double) <= kPinHalf) ? static_cast<double *>(pinned_scratch(2 * kPinHalf)) : nullptr;
+  if (pin) {
+    // the pinned buffer may still feed an earlier copy (any stream): wait for that copy only
+    static thread_local cudaEvent_t pin_ev = nullptr;
+    if (!pin_ev) CU(cudaEventCreateWithFlags(&pin_ev, cudaEventDisableTiming));
+    CU(cudaEventSynchronize(pin_ev));
+    memcpy(pin, targets, n * sizeof(double));
+    CU(cudaMemcpyAsync(h->s_targets, pin, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(pin_ev, st));
+  } else {
+    CU(cudaMemcpyAsync(h->s_targets, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
   if (h->from_terms) {
     for (int t = 0; t < n; ++t) {
       CU(cudaMemcpyAsync(h->s_tau + t * MK, h->d_tau_fixed, MK * sizeof(float), cudaMemcpyDeviceToDevice, st));
       CU(cudaMemcpyAsync(h->s_term + t * MK, h->d_term_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
       CU(cudaMemcpyAsync(h->s_b + t * MK, h->d_b_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
-    if (keys) CU(launch_init_keys(keys, counts, n, st));
+    if (keys) CU(launch_init_keys(keys, counts, n, work, n_work, st));
     return ALP_OK;
   }
   OptionArgs o;
@@ -608,6 +646,8 @@ alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st
   o.u = h->d_u;
   o.keys = keys;
   o.counts = counts;
+  o.work = work;
+  o.n_work = n_work;
   CU(launch_option_table(o, st));
   return ALP_OK;
 }
@@ -659,7 +699,14 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
   if (lo > hi || hi > items) return fail(ALP_EINVAL, "item range [%llu, %llu) outside [0, %llu)",
                                          (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)items);
-  s = option_tables(h, targets, n, st, keys, counts);
+  // work counters (one per phase, zeroed by K1) and the grab size: ~16 grabs per warp
+  const size_t nctr = (size_t)n * g.a.n_bchunks;
+  unsigned long long *work = h->a_work;
+  if (nctr > kArenaWork) {
+    CU(h->g_work.ensure(nctr));
+    work = h->g_work.p;
+  }
+  s = option_tables(h, targets, n, st, keys, counts, work, (int)nctr);
   if (s != ALP_OK) return s;
   g.a.q_budget = h->s_qb;
   g.a.item_lo = lo;
@@ -671,14 +718,6 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   int launches = 1;  // K1
   if (hi > lo) {
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
-    // work counters (one per phase) and the grab size: ~16 grabs per warp
-    const size_t nctr = (size_t)n * g.a.n_bchunks;
-    unsigned long long *work = h->a_work;
-    if (nctr > kArenaWork) {
-      CU(h->g_work.ensure(nctr));
-      work = h->g_work.p;
-    }
-    CU(cudaMemsetAsync(work, 0, nctr * sizeof(unsigned long long), st));
     g.a.work = work;
     const uint64_t warps = (uint64_t)g.grid * (kThreads / 32);
     g.a.grab = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, (hi - lo) / (warps * 16)));
@@ -725,8 +764,16 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
   f.counts = counts;
   f.out = h->s_res;
   CU(launch_finalize(f, st));
-  CU(cudaMemcpyAsync(out, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  void *pin = (n * sizeof(alp_result) <= kPinHalf) ? pinned_scratch(2 * kPinHalf) : nullptr;
+  if (pin) {
+    pin = static_cast<unsigned char *>(pin) + kPinHalf;
+    CU(cudaMemcpyAsync(pin, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    memcpy(out, pin, n * sizeof(alp_result));
+  } else {
+    CU(cudaMemcpyAsync(out, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
   h->last_launches += 1;
   if (h->ev_pending) {
     CU(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));

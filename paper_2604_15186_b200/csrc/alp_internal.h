@@ -34,6 +34,8 @@ struct OptionArgs {
   int *u;          // [M][K]
   unsigned long long *keys;    // [n_t] initialised to kKeyNone (may be null)
   unsigned long long *counts;  // [n_t] initialised to 0 (may be null)
+  unsigned long long *work;    // [n_work] search work counters, zeroed (may be null)
+  int n_work;
 };
 
 // Search kernel (K2) arguments: the static plan + per-search values.
@@ -104,7 +106,8 @@ struct PredictArgs {
 
 // Launchers (alp_kernels.cu). Return cudaError_t of the launch.
 cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st);
-cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, cudaStream_t st);
+cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
+                             int n_work, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);

@@ -87,6 +87,7 @@ __global__ void k_option_table(const OptionArgs A) {
     if (A.keys) A.keys[i] = kKeyNone;
     if (A.counts) A.counts[i] = 0ull;
   }
+  if (i < A.n_work) A.work[i] = 0ull;
   if (i >= A.n_targets * MK) return;
   const int t = i / MK, mk = i % MK, m = mk / A.prof.K, k = mk % A.prof.K;
   float tau;
@@ -99,12 +100,14 @@ __global__ void k_option_table(const OptionArgs A) {
   if (t == 0) A.u[mk] = u;
 }
 
-__global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts, int n) {
+__global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
+                            int n_work) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     keys[i] = kKeyNone;
     counts[i] = 0ull;
   }
+  if (i < n_work) work[i] = 0ull;
 }
 
 // ------------------------------------------------------------------ search kernel (K2) dispatch
@@ -180,6 +183,40 @@ __global__ void k_finalize(const FinalizeArgs F) {
     atomicMin(&s_best, mine);
   }
   __syncthreads();
+  // winner digits, then the per-LLM FP64 terms gathered in parallel (one thread per LLM)
+  __shared__ int s_k[ALP_MAX_M];
+  __shared__ double s_term[ALP_MAX_M], s_bterm[ALP_MAX_M];
+  __shared__ int s_u[ALP_MAX_M], s_grid[3][ALP_MAX_M];
+  const bool win = found && s_best != ~0ull;
+  if (threadIdx.x == 0 && win) {
+    const int a0 = (int)(q * P.A);
+    const int a = a0 + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
+    uint32_t rem = chunk;
+    for (int m = P.g0 - 1; m >= 0; --m) {
+      s_k[m] = (int)(rem % (uint32_t)K);
+      rem /= (uint32_t)K;
+    }
+    rem = e;
+    for (int j = P.ng - 1; j >= 0; --j) {
+      s_k[P.g0 + j] = (int)(rem % (uint32_t)K);
+      rem /= (uint32_t)K;
+    }
+    if (P.a_llm >= 0) s_k[P.a_llm] = a;
+    s_k[P.b_llm] = b;
+  }
+  __syncthreads();
+  if (win && (int)threadIdx.x < P.M) {
+    const int m = threadIdx.x, km = s_k[m];
+    s_term[m] = F.term[((size_t)t * P.M + m) * K + km];
+    s_bterm[m] = F.b[((size_t)t * P.M + m) * K + km];
+    s_u[m] = P.u[m * K + km];
+    if (F.S) {
+      s_grid[0][m] = F.S[km / (F.nR * F.nT)];
+      s_grid[1][m] = F.T[(km / F.nR) % F.nT];
+      s_grid[2][m] = F.R[km % F.nR];
+    }
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
   alp_result r;
   memset(&r, 0, sizeof(r));
@@ -188,39 +225,19 @@ __global__ void k_finalize(const FinalizeArgs F) {
   r.candidates = F.N;
   r.index = ~0ull;
   r.latency_key = finf();
-  if (found && s_best != ~0ull) {
-    const int a0 = (int)(q * P.A);
-    const int a = a0 + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
-    int k[ALP_MAX_M];
-    uint32_t rem = chunk;
-    for (int m = P.g0 - 1; m >= 0; --m) {
-      k[m] = (int)(rem % (uint32_t)K);
-      rem /= (uint32_t)K;
-    }
-    rem = e;
-    for (int j = P.ng - 1; j >= 0; --j) {
-      k[P.g0 + j] = (int)(rem % (uint32_t)K);
-      rem /= (uint32_t)K;
-    }
-    if (P.a_llm >= 0) k[P.a_llm] = a;
-    k[P.b_llm] = b;
+  if (win) {
     unsigned long long idx = 0;
     double L = 0.0, Tw = CUDART_INF;
     long long U = 0;
-    const double *term_t = F.term + (size_t)t * P.M * K;
-    const double *b_t = F.b + (size_t)t * P.M * K;
     for (int m = 0; m < P.M; ++m) {
-      idx = idx * (unsigned long long)K + (unsigned long long)k[m];
-      const double tm = term_t[m * K + k[m]];
-      L = (m == 0) ? tm : __dadd_rn(L, tm);  // Eq. 1 in canonical order (FP64)
-      const double bm = b_t[m * K + k[m]];
-      Tw = bm < Tw ? bm : Tw;                // Eq. 2
-      U += P.u[m * K + k[m]];
+      idx = idx * (unsigned long long)K + (unsigned long long)s_k[m];
+      L = (m == 0) ? s_term[m] : __dadd_rn(L, s_term[m]);  // Eq. 1 in canonical order (FP64)
+      Tw = s_bterm[m] < Tw ? s_bterm[m] : Tw;               // Eq. 2
+      U += s_u[m];
       if (F.S) {
-        const int s_i = k[m] / (F.nR * F.nT), t_i = (k[m] / F.nR) % F.nT, r_i = k[m] % F.nR;
-        r.share_units[m] = F.S[s_i];
-        r.tp[m] = F.T[t_i];
-        r.replicas[m] = F.R[r_i];
+        r.share_units[m] = s_grid[0][m];
+        r.tp[m] = s_grid[1][m];
+        r.replicas[m] = s_grid[2][m];
       }
     }
     r.found = 1;
@@ -323,13 +340,15 @@ __global__ void k_predict(const PredictArgs A) {
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st) {
   const int total = a.n_targets * a.prof.M * a.prof.K;
-  const int n = total > a.n_targets ? total : a.n_targets;
+  const int n = max(max(total, a.n_targets), a.n_work);
   k_option_table<<<(n + 255) / 256, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, cudaStream_t st) {
-  k_init_keys<<<(n + 255) / 256, 256, 0, st>>>(keys, counts, n);
+cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
+                             int n_work, cudaStream_t st) {
+  const int m = n > n_work ? n : n_work;
+  k_init_keys<<<(m + 255) / 256, 256, 0, st>>>(keys, counts, n, work, n_work);
   return cudaGetLastError();
 }
 
