@@ -212,6 +212,10 @@ struct alp_s {
   DBuf<alp_result> g_res;
   DBuf<unsigned long long> g_keys, g_counts, g_work;
   int *a_qb = nullptr;
+  unsigned long long *a_fbest = nullptr;  // finalize scratch (1 target), ~0 / 0 between calls
+  unsigned *a_fdone = nullptr;
+  DBuf<unsigned long long> g_fbest;
+  DBuf<unsigned> g_fdone;
   unsigned long long *a_work = nullptr;  // kArenaWork work counters
   DBuf<int> g_qb;
   int *s_qb = nullptr;  // per-query budgets (device) when the last search used them, else nullptr
@@ -248,6 +252,8 @@ struct alp_s {
     g_keys.release();
     g_counts.release();
     g_work.release();
+    g_fbest.release();
+    g_fdone.release();
     d_punits.release();
     if (d_arena) cudaFreeAsync(d_arena, stream);
     if (stream) cudaStreamSynchronize(stream);
@@ -492,8 +498,12 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_keys);
   A.scratch(1, &h->a_counts);
   A.scratch(1, &h->a_qb);
+  A.scratch(1, &h->a_fbest);
+  A.scratch(1, &h->a_fdone);
   A.scratch(kArenaWork, &h->a_work);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
+  CU(cudaMemsetAsync(h->a_fbest, 0xff, sizeof(unsigned long long), h->stream));
+  CU(cudaMemsetAsync(h->a_fdone, 0, sizeof(unsigned), h->stream));
   return ALP_OK;
 }
 
@@ -763,6 +773,19 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
   f.keys = keys;
   f.counts = counts;
   f.out = h->s_res;
+  if (n <= 1) {
+    f.best = h->a_fbest;
+    f.done = h->a_fdone;
+  } else {
+    if (h->g_fbest.n < (size_t)n) {
+      CU(h->g_fbest.ensure(n));
+      CU(h->g_fdone.ensure(n));
+      CU(cudaMemsetAsync(h->g_fbest.p, 0xff, n * sizeof(unsigned long long), st));
+      CU(cudaMemsetAsync(h->g_fdone.p, 0, n * sizeof(unsigned), st));
+    }
+    f.best = h->g_fbest.p;
+    f.done = h->g_fdone.p;
+  }
   CU(launch_finalize(f, st));
   void *pin = (n * sizeof(alp_result) <= kPinHalf) ? pinned_scratch(2 * kPinHalf) : nullptr;
   if (pin) {

@@ -91,6 +91,8 @@ struct FinalizeArgs {
   const unsigned long long *keys;
   const unsigned long long *counts;
   alp_result *out;       // [n_t] device
+  unsigned long long *best;  // [n_t] scratch: ~0 between calls (self-resetting)
+  unsigned *done;            // [n_t] scratch: 0 between calls (self-resetting)
 };
 
 struct PredictArgs {

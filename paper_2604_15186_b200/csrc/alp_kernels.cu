@@ -26,6 +26,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "alp_internal.h"
 
 namespace alp {
@@ -126,9 +128,11 @@ int search_max_blocks_per_sm(const SearchArgs &a) {
 }
 
 // ------------------------------------------------------------------ finalize (K3)
+// grid (nb, n_targets): the nb blocks of a target split the re-scan of the winning segment; the
+// last block to finish (ticket) assembles the result and resets the target's scratch.
 __global__ void k_finalize(const FinalizeArgs F) {
   const SearchArgs &P = F.s;
-  const int t = blockIdx.x;
+  const int t = blockIdx.y;
   const unsigned long long key = F.keys[t];
   const unsigned long long count = F.counts[t];
   __shared__ unsigned long long s_best;
@@ -165,7 +169,8 @@ __global__ void k_finalize(const FinalizeArgs F) {
     const int a0 = (int)(q * P.A), a1 = P.Ka;
     const unsigned long long n = (unsigned long long)(a1 - a0) * P.Kb;
     unsigned long long mine = ~0ull;
-    for (unsigned long long li = threadIdx.x; li < n; li += blockDim.x) {
+    for (unsigned long long li = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; li < n;
+         li += (unsigned long long)gridDim.x * blockDim.x) {
       const int a = a0 + (int)(li / P.Kb), b = (int)(li % P.Kb);
       float ta = 0.f;
       int ua = 0;
@@ -181,6 +186,22 @@ __global__ void k_finalize(const FinalizeArgs F) {
       }
     }
     atomicMin(&s_best, mine);
+  }
+  __syncthreads();
+  // combine the blocks of this target: global min, then only the last block continues
+  __shared__ unsigned s_last;
+  if (threadIdx.x == 0) {
+    if (found) atomicMin(F.best + t, s_best);
+    __threadfence();
+    s_last = (atomicAdd(F.done + t, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_best = atomicAdd(F.best + t, 0ull);  // coherent read of the combined minimum
+    F.best[t] = ~0ull;                    // reset for the next finalize on this scratch
+    F.done[t] = 0u;
   }
   __syncthreads();
   // winner digits, then the per-LLM FP64 terms gathered in parallel (one thread per LLM)
@@ -353,7 +374,10 @@ cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *count
 }
 
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st) {
-  k_finalize<<<a.s.n_targets, 256, 0, st>>>(a);
+  // blocks per target for the winning-segment re-scan (<= Ka*Kb candidates): ~16 per thread
+  const long long cand = (long long)a.s.Ka * a.s.Kb;
+  const int nb = (int)std::min<long long>(64, std::max<long long>(1, cand / (256 * 16)));
+  k_finalize<<<dim3(nb, a.s.n_targets), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
