@@ -151,6 +151,18 @@ struct Trace {
   }
 };
 
+// FastDiv (alp_internal.h): p = 31 + ceil(log2 d), mul = ceil(2^p / d), shift = p - 32; exact for n < 2^31
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{0u, 0u};
+  if (d <= 1) return f;
+  int s = 0;
+  while ((1ull << s) < d) ++s;
+  const int p = 31 + s;
+  f.mul = (uint32_t)(((1ull << p) + d - 1) / d);
+  f.shift = (uint32_t)(p - 32);
+  return f;
+}
+
 int ceil_log2(int k) {
   int b = 0;
   while ((1 << b) < k) ++b;
@@ -320,20 +332,12 @@ alp_status make_plan(alp_s *h) {
   h->tile_s.clear();
   h->tile_e.clear();
   const int T = h->rows_per_lane;
-  auto pack = [&](uint32_t e) {
-    uint32_t rem = e, v = 0;
-    for (int j = ng - 1; j >= 0; --j) {
-      v |= (rem % (uint32_t)K) << (j * h->dig_bits);
-      rem /= (uint32_t)K;
-    }
-    return v;
-  };
   for (size_t i = 0; i < order.size();) {
     const int s = sum[order[i]];
     h->tile_s.push_back(s);
     for (int r = 0; r < T; ++r) {
       if (i < order.size() && sum[order[i]] == s) {
-        h->tile_e.push_back(pack(order[i]));
+        h->tile_e.push_back(order[i]);  // canonical within-group index (LLM g0 most significant)
         ++i;
       } else {
         h->tile_e.push_back(kDummy);
@@ -349,13 +353,16 @@ alp_status make_plan(alp_s *h) {
   // slot g1*K holds 0.0f for unused digits, slot g1*K+1 holds +inf for padded rows)
   const uint32_t zero_off = (uint32_t)(h->g1 * K) * 4u, inf_off = zero_off + 4u;
   h->tile_off.assign(h->tile_e.size() * 2, 0u);
-  const uint32_t dm = (1u << h->dig_bits) - 1u;
   for (size_t i = 0; i < h->tile_e.size(); ++i) {
     uint32_t off[4] = {zero_off, zero_off, zero_off, zero_off};
     if (h->tile_e[i] == kDummy) {
       off[0] = inf_off;
     } else {
-      for (int j = 0; j < ng; ++j) off[j] = (uint32_t)((h->g0 + j) * K + ((h->tile_e[i] >> (j * h->dig_bits)) & dm)) * 4u;
+      uint32_t rem = h->tile_e[i];
+      for (int j = ng - 1; j >= 0; --j) {
+        off[j] = (uint32_t)((h->g0 + j) * K + (int)(rem % (uint32_t)K)) * 4u;
+        rem /= (uint32_t)K;
+      }
     }
     h->tile_off[2 * i] = off[0] | (off[1] << 16);
     h->tile_off[2 * i + 1] = off[2] | (off[3] << 16);
@@ -560,6 +567,8 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.M = h->M; a.K = h->K; a.g0 = h->g0; a.g1 = h->g1; a.a_llm = h->a_llm; a.b_llm = h->b_llm;
   a.Ka = h->Ka; a.Kb = h->Kb; a.ng = h->ng; a.dig_bits = h->dig_bits; a.L = h->L; a.n_chunks = h->n_chunks;
   a.n_groups = h->n_groups; a.nQ = h->nQ; a.A = h->A; a.item_lo = lo; a.item_hi = hi;
+  a.fd_nQ = make_fastdiv(h->nQ);
+  a.fd_ng = make_fastdiv(h->n_groups);
   a.budget = (int)Reff;
   a.n_targets = n_targets;
   a.D = (int)(std::upper_bound(h->dv.begin(), h->dv.end(), (int)Reff) - h->dv.begin());
@@ -580,6 +589,11 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
     a.off_lut = off; off = align16(off + (a.budget + 2) * 8);
     a.off_tmp = off; off = align16(off + (2 * h->Kb + 3) * 4);
     a.off_btab = off; off = align16(off + rows * a.row_stride * 4);
+    a.off_pfx = -1;
+    if (h->g0 > 0 && h->n_chunks <= kPfxTableMax) {
+      a.off_pfx = off;
+      off = align16(off + (int)h->n_chunks * 8);
+    }
     a.smem_bytes = off;
     return off;
   };
@@ -729,8 +743,12 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   if (hi > lo) {
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
     g.a.work = work;
+    // ~16 grabs per warp; the last ~1/8 of the items go in grabs a quarter that size (tail balance)
     const uint64_t warps = (uint64_t)g.grid * (kThreads / 32);
-    g.a.grab = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, (hi - lo) / (warps * 16)));
+    const uint64_t n_items = hi - lo;
+    g.a.grab = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, n_items / (warps * 16)));
+    g.a.grab2 = std::max(1, g.a.grab / 4);
+    g.a.grab_t1 = (n_items - n_items / 8) / (uint64_t)g.a.grab;
     CU(launch_search(g.a, g.grid, st));
     launches += 1;
   }

@@ -10,8 +10,15 @@ namespace alp {
 
 constexpr int kWarpTiles = 32;           // lane tiles per warp group
 constexpr int kThreads = 256;            // threads per search block
+constexpr uint32_t kPfxTableMax = 4096;  // prefix chunks tabulated in shared memory (8 B each)
 constexpr uint32_t kDummy = 0xFFFFFFFFu; // padded row marker in the tile list
 constexpr unsigned long long kKeyNone = 0x7FFFFFFFFFFFFFFFull;  // INT64_MAX: nothing feasible
+
+// Division by a fixed divisor d for dividends < 2^31: q = umulhi(n, mul) >> shift, with
+// shift = ceil(log2 d), mul = ceil(2^(32+shift) / d); mul = 0 encodes d = 1.
+struct FastDiv {
+  uint32_t mul, shift;
+};
 
 // Device-resident profile description (uploaded by alp_build).
 struct DevProfiles {
@@ -51,7 +58,9 @@ struct SearchArgs {
   uint32_t nQ, A;        // a-ranges: a in [q*A, min((q+1)*A, Ka))
   uint64_t item_lo, item_hi;
   unsigned long long *work;  // [n_targets * n_bchunks] work counters (zeroed before the launch)
-  int grab;              // items per dynamic work grab
+  int grab, grab2;       // items per dynamic work grab: tickets [0, grab_t1) take grab, later ones grab2
+  unsigned long long grab_t1;
+  FastDiv fd_nQ, fd_ng;  // item -> (chunk, group, a-range) decode when item_hi < 2^31
   int budget;            // R (capped at the total max units); max over queries when q_budget is set
   const int *q_budget;   // [n_targets] per-query budgets (capped) or nullptr (all = budget)
   int n_targets;
@@ -62,7 +71,7 @@ struct SearchArgs {
   const float *tau;      // [n_t][M][K]
   const int *u;          // [M][K]
   const int *tile_s;     // [n_tiles] units of the lane tile's sort-group options
-  const uint32_t *tile_e;// [n_tiles][T] packed sort-group digits (kDummy = padding)
+  const uint32_t *tile_e;// [n_tiles][T] canonical sort-group entry index (kDummy = padding)
   const uint32_t *tile_off;// [n_tiles][T][2] smem byte offsets of the row's sort-group terms (4 x 16 bit)
   int rows_per_lane;     // T (8 or 16)
   int min_blocks;        // launch-bounds variant for T = 8 (3 or 4 blocks/SM)
@@ -76,6 +85,7 @@ struct SearchArgs {
   unsigned long long *counts;
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
+  int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it
 };
 
 // budget of query t (per-query budgets for budget sweeps, else the common budget)

@@ -47,6 +47,7 @@ struct Smem {
   int *dv;         // [D] distinct b unit values <= R, ascending
   int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
   float *btab;     // [rows][row_stride] masked rows
+  float2 *pfx;     // [n_chunks] {prefix partial sum, bits(prefix units)} when P.off_pfx >= 0
 };
 
 constexpr int kBigUnits = 1 << 28;
@@ -73,6 +74,23 @@ __device__ __forceinline__ int row_of(const int *dv, int D, int r) {
   return lo;
 }
 
+// n / d for n < 2^31 with a host-computed multiplier (FastDiv in alp_internal.h)
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+  return f.mul ? (__umulhi(n, f.mul) >> f.shift) : n;
+}
+
+// canonical partial sum over LLMs 0..g0-1 of a prefix chunk (LLM 0 most significant):
+// ((0 + tau_0) + tau_1) + ..., and its units
+__device__ __forceinline__ void prefix_sum(const SearchArgs &P, const Smem &s, uint32_t chunk, float &pa, int &U) {
+  pa = 0.f;
+  U = 0;
+  for (int m = 0; m < P.g0; ++m) {
+    const uint32_t d = (chunk / P.pw[m]) % (uint32_t)P.K;
+    pa = __fadd_rn(pa, s.tau[m * P.K + d]);
+    U += s.u[m * P.K + d];
+  }
+}
+
 __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *base) {
   Smem s;
   s.tau = reinterpret_cast<float *>(base + P.off_tau);
@@ -82,6 +100,7 @@ __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *
   s.dv = reinterpret_cast<int *>(base + P.off_tmp);
   s.dcnt = s.dv + (P.Kb + 1);
   s.btab = reinterpret_cast<float *>(base + P.off_btab);
+  s.pfx = reinterpret_cast<float2 *>(base + (P.off_pfx >= 0 ? P.off_pfx : 0));
   return s;
 }
 
@@ -118,6 +137,14 @@ __device__ inline void build_tables(const SearchArgs &P, const Smem &s, int t, i
     if (lane == 0) s.btab[row * P.row_stride + P.bchunk_wpad] = __int_as_float((int)n);
   }
   __syncthreads();
+  // prefix chunk table (small prefix spaces): one canonical partial sum per chunk
+  if (P.off_pfx >= 0)
+    for (uint32_t c = tid; c < P.n_chunks; c += nt) {
+      float pa;
+      int U;
+      prefix_sum(P, s, c, pa, U);
+      s.pfx[c] = make_float2(pa, __int_as_float(U));
+    }
   // r -> masked row: index = #{distinct b unit values <= r}
   for (int r = tid - 1; r <= R; r += nt) {
     const int lo = row_of(s.dv, D, r);
@@ -185,7 +212,7 @@ __device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], floa
 
 // Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
 // row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
-// The tile's packed digits are read only when a row can improve the best (rare).
+// The row's canonical within-group index is read only when the row can improve the best.
 template <int T>
 __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[T], uint32_t tile, uint32_t chunk,
                                           uint32_t q0, float &best, uint32_t &best_seg) {
@@ -193,12 +220,9 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
 #pragma unroll
   for (int i = 0; i < T; ++i) any |= (acc[i] <= best) && (acc[i] < finf());
   if (!any) return;
-  const uint32_t dmask = (1u << P.dig_bits) - 1u;
   for (int i = 0; i < T; ++i) {
     if (acc[i] <= best && acc[i] < finf()) {
-      const uint32_t e = __ldg(P.tile_e + (size_t)tile * T + i);
-      uint32_t ec = 0;  // canonical within-group index: LLM g0 most significant
-      for (int j = 0; j < P.ng; ++j) ec = ec * (uint32_t)P.K + ((e >> (j * P.dig_bits)) & dmask);
+      const uint32_t ec = __ldg(P.tile_e + (size_t)tile * T + i);  // canonical within-group index
       const uint32_t seg = (chunk * P.L + ec) * P.nQ + q0;
       if (acc[i] < best || seg < best_seg) {
         best = acc[i];
@@ -218,10 +242,12 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   // Dynamic work distribution: warps take runs of P.grab consecutive items from this phase's
   // counter (the result is independent of who evaluates what: keys carry (value, segment) and the
   // counts are sums).  The next run is requested while the current one is evaluated.
+  // Guided tickets: the first grab_t1 tickets cover P.grab items each, later ones P.grab2 (<= grab)
+  // so the last grabs of the phase are short (tail balance).
   unsigned long long *ctr = P.work + work_slot;
-  unsigned long long nxt = 0;
-  if (lane == 0) nxt = atomicAdd(ctr, (unsigned long long)P.grab);
-  nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  unsigned long long tk = 0;
+  if (lane == 0) tk = atomicAdd(ctr, 1ull);
+  tk = __shfl_sync(0xffffffffu, tk, 0);
   // state of the lane tile currently loaded
   float Qr[T], acc[T];
   int r_tile = 0;
@@ -231,28 +257,39 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   int Upfx = 0;
   uint32_t pchunk = 0xffffffffu;
   const unsigned char *tau_b = reinterpret_cast<const unsigned char *>(s.tau);
-  while (nxt < n) {
+  const bool small = P.item_hi < (1ull << 31);  // 32-bit item decode with host-computed fast divisors
+  for (;;) {
+  const uint64_t t1 = (uint64_t)P.grab_t1;
+  const uint64_t nxt = tk < t1 ? tk * (uint64_t)P.grab : t1 * (uint64_t)P.grab + (tk - t1) * (uint64_t)P.grab2;
+  if (nxt >= n) break;
   uint64_t it = P.item_lo + nxt;
-  const uint64_t end = P.item_lo + min((unsigned long long)n, nxt + (unsigned long long)P.grab);
-  if (lane == 0) nxt = atomicAdd(ctr, (unsigned long long)P.grab);
-  uint32_t q = (uint32_t)(it % P.nQ);
-  const uint64_t tq = it / P.nQ;
-  uint32_t grp = (uint32_t)(tq % P.n_groups);
-  uint32_t chunk = (uint32_t)(tq / P.n_groups);
+  const uint64_t end = P.item_lo + min((unsigned long long)n,
+                                       nxt + (unsigned long long)(tk < t1 ? P.grab : P.grab2));
+  if (lane == 0) tk = atomicAdd(ctr, 1ull);
+  uint32_t q, grp, chunk;
+  if (small) {
+    const uint32_t i32 = (uint32_t)it;
+    const uint32_t tq = fdiv(i32, P.fd_nQ);
+    q = i32 - tq * P.nQ;
+    chunk = fdiv(tq, P.fd_ng);
+    grp = tq - chunk * P.n_groups;
+  } else {
+    q = (uint32_t)(it % P.nQ);
+    const uint64_t tq = it / P.nQ;
+    grp = (uint32_t)(tq % P.n_groups);
+    chunk = (uint32_t)(tq / P.n_groups);
+  }
   bool loaded = false;
   for (; it < end; ++it) {
     if (!loaded) {
       if (chunk != pchunk) {
-        // canonical partial sum over LLMs 0..g0-1 (LLM 0 most significant): ((0 + tau_0) + tau_1) + ...
-        float pa = 0.f;
-        int U = 0;
-        for (int m = 0; m < P.g0; ++m) {
-          const uint32_t d = (chunk / P.pw[m]) % (uint32_t)K;
-          pa = __fadd_rn(pa, s.tau[m * K + d]);
-          U += s.u[m * K + d];
+        if (P.off_pfx >= 0) {
+          const float2 pf = s.pfx[chunk];  // table built per phase (build_tables)
+          Pfx = pf.x;
+          Upfx = __float_as_int(pf.y);
+        } else {
+          prefix_sum(P, s, chunk, Pfx, Upfx);
         }
-        Pfx = pa;
-        Upfx = U;
         pchunk = chunk;
       }
       const uint32_t tile = grp * kWarpTiles + lane;
@@ -311,7 +348,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     }
   }
   if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
-  nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  tk = __shfl_sync(0xffffffffu, tk, 0);
   }
 }
 
