@@ -179,9 +179,16 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
                         const int64_t *d_keys, const int64_t *d_counts, void *stream, alp_result *out);
 
 /* Device time (ms) of the last search kernel launched through this handle (CUDA events on the
- * launching stream), and the number of kernels the last search/finalize launched. */
+ * launching stream), and the number of kernels the last search/finalize launched.  Searches of at
+ * most 8 targets with a common budget run as ONE kernel (option terms, exhaustive search and
+ * finalize fused); larger batches and per-query budgets run K1 + K2 + K3. */
 float alp_last_kernel_ms(const alp_t *h);
 int32_t alp_last_launches(const alp_t *h);
+/* Device time (ms) of the last complete search step through this handle: CUDA events on the
+ * search stream from the start of alp_search* / alp_search_shard to the completion of the
+ * result D2H in alp_search* / alp_finalize (includes an all-reduce issued in between on that
+ * stream; excludes the host's wake-up after the final synchronisation). */
+float alp_last_step_ms(const alp_t *h);
 
 /* Static search plans (sort-list tiles, u-sorted columns; they depend only on the grids) are cached
  * process-wide and shared by handles built on the same device with the same grids.  This drops the

@@ -29,7 +29,8 @@ constexpr size_t kArenaWork = 64;  // work counters kept in the handle arena (ph
 
 // Small pinned host buffer per host thread (allocated once, shared by all handles the thread uses)
 // for the per-search H2D of targets and D2H of results: pageable copies cost a staging hop each.
-// Two fixed halves: [0, 32 KB) feeds target H2D copies, [32 KB, 64 KB) receives result D2H copies.
+// Two fixed halves: [0, 32 KB) feeds target H2D copies, [32 KB, 64 KB) receives result D2H copies
+// (or, for the fused search, the kernel's own zero-copy result stores).
 constexpr size_t kPinHalf = 32 * 1024;
 void *pinned_scratch(size_t bytes) {
   struct Buf {
@@ -45,7 +46,8 @@ void *pinned_scratch(size_t bytes) {
     b.p = nullptr;
     b.n = 0;
     const size_t want = std::max<size_t>(bytes, 2 * kPinHalf);
-    if (cudaHostAlloc(&b.p, want, cudaHostAllocDefault) != cudaSuccess) {
+    // mapped: the fused search kernel writes its results straight into the upper half (zero-copy)
+    if (cudaHostAlloc(&b.p, want, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
       b.p = nullptr;
       return nullptr;
     }
@@ -229,6 +231,11 @@ struct alp_s {
   DBuf<unsigned long long> g_fbest;
   DBuf<unsigned> g_fdone;
   unsigned long long *a_work = nullptr;  // kArenaWork work counters
+  // fused-launch scratch (rest state ~0 / 0, restored by the last block of every fused launch)
+  unsigned long long *a_fzkeys = nullptr, *a_fzcounts = nullptr, *a_fzwork = nullptr;
+  unsigned *a_fzticket = nullptr;
+  cudaEvent_t evs0 = nullptr, evs1 = nullptr;  // step events: search start .. result D2H enqueued
+  float last_step_ms = 0.f;
   DBuf<int> g_qb;
   int *s_qb = nullptr;  // per-query budgets (device) when the last search used them, else nullptr
   double *s_targets = nullptr, *s_term = nullptr, *s_b = nullptr;
@@ -271,6 +278,8 @@ struct alp_s {
     if (stream) cudaStreamSynchronize(stream);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (evs0) cudaEventDestroy(evs0);
+    if (evs1) cudaEventDestroy(evs1);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -505,12 +514,18 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_keys);
   A.scratch(1, &h->a_counts);
   A.scratch(1, &h->a_qb);
-  A.scratch(1, &h->a_fbest);
-  A.scratch(1, &h->a_fdone);
   A.scratch(kArenaWork, &h->a_work);
+  // self-resetting scratch, initialised through the copied section (rest state)
+  static const std::vector<unsigned long long> ones1(1, ~0ull), onesT(kInlineTargets, ~0ull),
+      zerosT(kInlineTargets, 0ull), zerosW(kArenaWork, 0ull);
+  static const std::vector<unsigned> zero1(1, 0u);
+  A.add(ones1, &h->a_fbest);
+  A.add(zero1, &h->a_fdone);
+  A.add(onesT, &h->a_fzkeys);
+  A.add(zerosT, &h->a_fzcounts);
+  A.add(zerosW, &h->a_fzwork);
+  A.add(zero1, &h->a_fzticket);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
-  CU(cudaMemsetAsync(h->a_fbest, 0xff, sizeof(unsigned long long), h->stream));
-  CU(cudaMemsetAsync(h->a_fdone, 0, sizeof(unsigned), h->stream));
   return ALP_OK;
 }
 
@@ -532,6 +547,8 @@ alp_status init_device(alp_s *h) {
   }
   CU(cudaEventCreate(&h->ev0));
   CU(cudaEventCreate(&h->ev1));
+  CU(cudaEventCreate(&h->evs0));
+  CU(cudaEventCreate(&h->evs1));
   return ALP_OK;
 }
 
@@ -558,7 +575,8 @@ struct Geometry {
   int grid;
 };
 
-alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, uint64_t hi, Geometry &g) {
+alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, uint64_t hi, Geometry &g,
+                         bool fused = false) {
   if (budget < 0) return fail(ALP_EINVAL, "budget_units < 0");
   const long long Reff = std::min<long long>(budget, h->umax_total);
   if (Reff > 16384) return fail(ALP_EINVAL, "budget_units (capped at the total max units) exceeds 16384");
@@ -593,6 +611,11 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
     if (h->g0 > 0 && h->n_chunks <= kPfxTableMax) {
       a.off_pfx = off;
       off = align16(off + (int)h->n_chunks * 8);
+    }
+    a.fz.off_opt = 0;
+    if (fused) {
+      a.fz.off_opt = off;
+      off = align16(off + h->M * h->K * 4);
     }
     a.smem_bytes = off;
     return off;
@@ -640,7 +663,9 @@ alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st
                          unsigned long long *counts, unsigned long long *work = nullptr, int n_work = 0) {
   const size_t MK = (size_t)h->M * h->K;
   double *pin = (n * sizeof(double) <= kPinHalf) ? static_cast<double *>(pinned_scratch(2 * kPinHalf)) : nullptr;
-  if (pin) {
+  const bool inline_t = !h->from_terms && n <= kInlineTargets;  // targets travel in K1's parameters
+  if (inline_t) {
+  } else if (pin) {
     // the pinned buffer may still feed an earlier copy (any stream): wait for that copy only
     static thread_local cudaEvent_t pin_ev = nullptr;
     if (!pin_ev) CU(cudaEventCreateWithFlags(&pin_ev, cudaEventDisableTiming));
@@ -662,7 +687,8 @@ alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st
   }
   OptionArgs o;
   o.prof = h->dprof();
-  o.targets = h->s_targets;
+  o.targets = inline_t ? nullptr : h->s_targets;
+  for (int i = 0; i < kInlineTargets; ++i) o.tgt[i] = (inline_t && i < n) ? targets[i] : 0.0;
   o.n_targets = n;
   o.tau = h->s_tau;
   o.term = h->s_term;
@@ -707,40 +733,114 @@ alp_status prepare_budgets(alp_s *h, const int64_t *budgets, int n, cudaStream_t
   return ALP_OK;
 }
 
+// Fused single launch (no K1 / K3): few targets, a common budget, and a small option table (every
+// block recomputes it: cheaper than a K1 launch only while M*K is small) and a short finalize
+// re-scan (one block, <= Ka*Kb candidates; larger ones use K3's multi-block re-scan).
+// Injected terms (alp_build_from_terms) describe one target only.
+bool use_fused(const alp_s *h, int n, const int64_t *budgets) {
+  if (getenv("ALP_NO_FUSED")) return false;  // A/B switch for measurements
+  return !budgets && n <= kInlineTargets && h->M * h->K <= kFusedMaxTerms &&
+         (uint64_t)h->Ka * h->Kb <= kFusedMaxRescan && (!h->from_terms || n == 1);
+}
+
+// Finalize inputs of the handle's scratch (K3 and the fused last block).
+void fill_finalize(alp_s *h, SearchArgs &a) {
+  FinalizeExtra &f = a.fin;
+  f.term = h->s_term;
+  f.b = h->s_b;
+  if (h->from_terms && a.fz.on) {
+    f.term = h->d_term_fixed;
+    f.b = h->d_b_fixed;
+  }
+  f.S = h->from_terms ? nullptr : h->d_S;
+  f.T = h->d_T;
+  f.R = h->d_R;
+  f.nS = h->nS; f.nT = h->nT; f.nR = h->nR;
+  f.N = h->N;
+  f.out = h->s_res;
+  const int n = a.n_targets;
+  f.best = h->a_fbest;
+  f.done = h->a_fdone;
+  if (n > 1) {
+    f.best = h->g_fbest.p;
+    f.done = h->g_fdone.p;
+  }
+}
+
+alp_status ensure_finalize_scratch(alp_s *h, int n, cudaStream_t st) {
+  if (n > 1 && h->g_fbest.n < (size_t)n) {
+    CU(h->g_fbest.ensure(n));
+    CU(h->g_fdone.ensure(n));
+    CU(cudaMemsetAsync(h->g_fbest.p, 0xff, n * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(h->g_fdone.p, 0, n * sizeof(unsigned), st));
+  }
+  return ALP_OK;
+}
+
+// K2 over work items [lo, hi) (classic: after K1; fused: alone, finalize optional).  Writes the
+// per-target (key, count) of this shard to keys/counts; async on st.
 alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
                              uint64_t lo, uint64_t hi, cudaStream_t st, unsigned long long *keys,
-                             unsigned long long *counts) {
+                             unsigned long long *counts, bool fuse_finalize = false,
+                             alp_result *fused_out = nullptr) {
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
+  CU(cudaEventRecord(h->evs0, st));
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   s = prepare_budgets(h, budgets, n, st, &budget);
   if (s != ALP_OK) return s;
+  const bool fused = use_fused(h, n, budgets);
   Geometry g;
-  s = make_geometry(h, n, budget, 0, 0, g);
+  s = make_geometry(h, n, budget, 0, 0, g, fused);
   if (s != ALP_OK) return s;
   const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
   if (lo > hi || hi > items) return fail(ALP_EINVAL, "item range [%llu, %llu) outside [0, %llu)",
                                          (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)items);
-  // work counters (one per phase, zeroed by K1) and the grab size: ~16 grabs per warp
   const size_t nctr = (size_t)n * g.a.n_bchunks;
+  int launches = 0;
   unsigned long long *work = h->a_work;
-  if (nctr > kArenaWork) {
-    CU(h->g_work.ensure(nctr));
-    work = h->g_work.p;
+  if (fused) {
+    if (nctr > kArenaWork) return fail(ALP_EINTERNAL, "fused search: %zu work counters", nctr);
+    FusedArgs &z = g.a.fz;
+    z.on = 1;
+    z.finalize = fuse_finalize ? 1 : 0;
+    if (!h->from_terms) z.prof = h->dprof();
+    for (int i = 0; i < kInlineTargets; ++i) z.tgt[i] = i < n ? targets[i] : 0.0;
+    z.tau_fixed = h->from_terms ? h->d_tau_fixed : nullptr;
+    z.o_tau = h->s_tau;
+    z.o_term = h->s_term;
+    z.o_b = h->s_b;
+    z.acc_keys = h->a_fzkeys;
+    z.acc_counts = h->a_fzcounts;
+    z.work = h->a_fzwork;
+    z.ticket = h->a_fzticket;
+    work = h->a_fzwork;
+    if (fuse_finalize) {
+      s = ensure_finalize_scratch(h, n, st);
+      if (s != ALP_OK) return s;
+    }
+  } else {
+    // work counters (one per phase, zeroed by K1)
+    if (nctr > kArenaWork) {
+      CU(h->g_work.ensure(nctr));
+      work = h->g_work.p;
+    }
+    s = option_tables(h, targets, n, st, keys, counts, work, (int)nctr);
+    if (s != ALP_OK) return s;
+    launches = 1;  // K1
   }
-  s = option_tables(h, targets, n, st, keys, counts, work, (int)nctr);
-  if (s != ALP_OK) return s;
   g.a.q_budget = h->s_qb;
   g.a.item_lo = lo;
   g.a.item_hi = hi;
   g.a.tau = h->s_tau;
   g.a.keys = keys;
   g.a.counts = counts;
+  fill_finalize(h, g.a);
+  if (fused_out) g.a.fin.out = fused_out;
   CU(cudaEventRecord(h->ev0, st));
-  int launches = 1;  // K1
-  if (hi > lo) {
+  if (hi > lo || fused) {  // the fused launch also computes the terms and writes keys/counts
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
     g.a.work = work;
     // ~16 grabs per warp; the last ~1/8 of the items go in grabs a quarter that size (tail balance)
@@ -757,6 +857,30 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   h->last_args = g.a;
   h->last_launches = launches;
   return ALP_OK;
+}
+
+// D2H of the n results (pinned staging), step-end event, sync; status from the results.
+alp_status collect_results(alp_s *h, int n, cudaStream_t st, alp_result *out) {
+  void *pin = (n * sizeof(alp_result) <= kPinHalf) ? pinned_scratch(2 * kPinHalf) : nullptr;
+  if (pin) {
+    pin = static_cast<unsigned char *>(pin) + kPinHalf;
+    CU(cudaMemcpyAsync(pin, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(h->evs1, st));
+    CU(cudaStreamSynchronize(st));
+    memcpy(out, pin, n * sizeof(alp_result));
+  } else {
+    CU(cudaMemcpyAsync(out, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(h->evs1, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  CU(cudaEventElapsedTime(&h->last_step_ms, h->evs0, h->evs1));
+  if (h->ev_pending) {
+    CU(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
+    h->ev_pending = false;
+  }
+  int any = 0;
+  for (int i = 0; i < n; ++i) any |= out[i].found;
+  return any ? ALP_OK : ALP_EINFEASIBLE;
 }
 
 alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
@@ -777,52 +901,16 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
   if (s != ALP_OK) return s;
   // option tables must describe these targets (the shard call computed them on this handle)
   (void)targets;
-  FinalizeArgs f;
-  f.s = g.a;
-  f.s.q_budget = h->s_qb;
-  f.s.tau = h->s_tau;
-  f.term = h->s_term;
-  f.b = h->s_b;
-  f.S = h->from_terms ? nullptr : h->d_S;
-  f.T = h->d_T;
-  f.R = h->d_R;
-  f.nS = h->nS; f.nT = h->nT; f.nR = h->nR;
-  f.N = h->N;
-  f.keys = keys;
-  f.counts = counts;
-  f.out = h->s_res;
-  if (n <= 1) {
-    f.best = h->a_fbest;
-    f.done = h->a_fdone;
-  } else {
-    if (h->g_fbest.n < (size_t)n) {
-      CU(h->g_fbest.ensure(n));
-      CU(h->g_fdone.ensure(n));
-      CU(cudaMemsetAsync(h->g_fbest.p, 0xff, n * sizeof(unsigned long long), st));
-      CU(cudaMemsetAsync(h->g_fdone.p, 0, n * sizeof(unsigned), st));
-    }
-    f.best = h->g_fbest.p;
-    f.done = h->g_fdone.p;
-  }
-  CU(launch_finalize(f, st));
-  void *pin = (n * sizeof(alp_result) <= kPinHalf) ? pinned_scratch(2 * kPinHalf) : nullptr;
-  if (pin) {
-    pin = static_cast<unsigned char *>(pin) + kPinHalf;
-    CU(cudaMemcpyAsync(pin, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    memcpy(out, pin, n * sizeof(alp_result));
-  } else {
-    CU(cudaMemcpyAsync(out, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-  }
+  g.a.q_budget = h->s_qb;
+  g.a.tau = h->s_tau;
+  s = ensure_finalize_scratch(h, n, st);
+  if (s != ALP_OK) return s;
+  fill_finalize(h, g.a);
+  g.a.fin.keys = keys;
+  g.a.fin.counts = counts;
+  CU(launch_finalize(g.a, st));
   h->last_launches += 1;
-  if (h->ev_pending) {
-    CU(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
-    h->ev_pending = false;
-  }
-  int any = 0;
-  for (int i = 0; i < n; ++i) any |= out[i].found;
-  return any ? ALP_OK : ALP_EINFEASIBLE;
+  return collect_results(h, n, st, out);
 }
 
 }  // namespace
@@ -1063,12 +1151,35 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
                                  int64_t budget_units, alp_result *out) {
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (!out) return fail(ALP_EINVAL, "out is NULL");
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   const uint64_t items = alp_num_items(h, budget_units);
+  if (use_fused(h, n, budgets)) {  // one launch: terms + search + finalize
+    // the kernel's last block stores the results into mapped pinned memory (no D2H copy)
+    auto *pin = static_cast<unsigned char *>(pinned_scratch(2 * kPinHalf));
+    alp_result *hres = pin ? reinterpret_cast<alp_result *>(pin + kPinHalf) : nullptr, *dres = nullptr;
+    if (hres && cudaHostGetDevicePointer(reinterpret_cast<void **>(&dres), hres, 0) != cudaSuccess) {
+      cudaGetLastError();
+      dres = nullptr;
+    }
+    s = search_shard_impl(h, targets, nullptr, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts, true,
+                          dres);
+    if (s != ALP_OK) return s;
+    if (!dres) return collect_results(h, n, h->stream, out);
+    CU(cudaEventRecord(h->evs1, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    memcpy(out, hres, n * sizeof(alp_result));
+    CU(cudaEventElapsedTime(&h->last_step_ms, h->evs0, h->evs1));
+    CU(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
+    h->ev_pending = false;
+    int any = 0;
+    for (int i = 0; i < n; ++i) any |= out[i].found;
+    return any ? ALP_OK : ALP_EINFEASIBLE;
+  }
   s = search_shard_impl(h, targets, budgets, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts);
   if (s != ALP_OK) return s;
   return finalize_impl(h, targets, budgets, n, budget_units, h->s_keys, h->s_counts, h->stream, out);
@@ -1321,6 +1432,8 @@ float alp_last_kernel_ms(const alp_t *h) {
 }
 
 int32_t alp_last_launches(const alp_t *h) { return h ? h->last_launches : 0; }
+
+float alp_last_step_ms(const alp_t *h) { return h ? h->last_step_ms : 0.f; }
 
 void alp_plan_cache_clear(void) {
   std::lock_guard<std::mutex> lock(g_plan_mu);

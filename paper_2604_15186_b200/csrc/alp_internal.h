@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/alp.h"
 
@@ -13,6 +14,15 @@ constexpr int kThreads = 256;            // threads per search block
 constexpr uint32_t kPfxTableMax = 4096;  // prefix chunks tabulated in shared memory (8 B each)
 constexpr uint32_t kDummy = 0xFFFFFFFFu; // padded row marker in the tile list
 constexpr unsigned long long kKeyNone = 0x7FFFFFFFFFFFFFFFull;  // INT64_MAX: nothing feasible
+constexpr int kInlineTargets = 8;        // targets passed in kernel parameters (no H2D copy)
+constexpr int kFusedMaxTerms = 1024;     // max option terms (M*K) recomputed per block by the fused launch
+constexpr uint64_t kFusedMaxRescan = 65536;  // max finalize re-scan (Ka*Kb) done by one block
+
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-serialization
+// attribute may start while its predecessor on the stream still runs; it waits here before
+// touching anything the predecessor writes.  No-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Division by a fixed divisor d for dividends < 2^31: q = umulhi(n, mul) >> shift, with
 // shift = ceil(log2 d), mul = ceil(2^(32+shift) / d); mul = 0 encodes d = 1.
@@ -33,7 +43,8 @@ struct DevProfiles {
 // Option-term kernel (K1) arguments.
 struct OptionArgs {
   DevProfiles prof;
-  const double *targets;
+  const double *targets;            // [n_targets] device, or nullptr when n_targets <= kInlineTargets
+  double tgt[kInlineTargets];       // inline targets
   int n_targets;
   float *tau;      // [n_t][M][K]
   double *term;    // [n_t][M][K]
@@ -43,6 +54,38 @@ struct OptionArgs {
   unsigned long long *counts;  // [n_t] initialised to 0 (may be null)
   unsigned long long *work;    // [n_work] search work counters, zeroed (may be null)
   int n_work;
+};
+
+// Finalize inputs/outputs (K3, or the fused search's last block).
+struct FinalizeExtra {
+  const double *term;    // [n_t][M][K] FP64 Eq. 1 terms
+  const double *b;       // [n_t][M][K] FP64 Eq. 2 terms
+  const int *S, *T, *R;  // grids (for the winner's (share, tp, replicas)); S == nullptr: injected terms
+  int nS, nT, nR;
+  uint64_t N;
+  const unsigned long long *keys;    // [n_t] reduced keys (K3 input)
+  const unsigned long long *counts;  // [n_t] reduced counts (K3 input)
+  alp_result *out;       // [n_t] device
+  unsigned long long *best;  // [n_t] scratch: ~0 between calls (self-resetting)
+  unsigned *done;            // [n_t] scratch: 0 between calls (self-resetting)
+};
+
+// Fused single-launch search (targets <= kInlineTargets): every block computes the option terms of
+// the phase's target in its prologue (no K1), blocks accumulate into self-resetting scratch, and
+// the last block to finish writes the (key, count) pairs, resets the scratch and (finalize = 1)
+// runs the finalize (no K3).
+struct FusedArgs {
+  int on, finalize;
+  DevProfiles prof;
+  double tgt[kInlineTargets];
+  const float *tau_fixed;     // injected terms (alp_build_from_terms) instead of prof, or nullptr
+  float *o_tau;               // [n_t][M][K] written by block 0 (K3 / finalize inputs)
+  double *o_term, *o_b;       // [n_t][M][K] written by block 0 (nullptr with injected terms)
+  unsigned long long *acc_keys;    // [n_t] ~0 at rest
+  unsigned long long *acc_counts;  // [n_t] 0 at rest
+  unsigned long long *work;        // [n_t * n_bchunks] 0 at rest
+  unsigned *ticket;                // 0 at rest
+  int off_opt;                // smem offset of the phase's option terms [M*K] floats
 };
 
 // Search kernel (K2) arguments: the static plan + per-search values.
@@ -83,6 +126,8 @@ struct SearchArgs {
   uint32_t pw[ALP_MAX_M];// pw[m] = K^(g0-1-m): prefix digit m of a chunk index
   unsigned long long *keys;
   unsigned long long *counts;
+  FusedArgs fz;
+  FinalizeExtra fin;
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
   int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it
@@ -90,20 +135,6 @@ struct SearchArgs {
 
 // budget of query t (per-query budgets for budget sweeps, else the common budget)
 __device__ __forceinline__ int qbudget(const SearchArgs &P, int t) { return P.q_budget ? P.q_budget[t] : P.budget; }
-
-struct FinalizeArgs {
-  SearchArgs s;
-  const double *term;    // [n_t][M][K]
-  const double *b;       // [n_t][M][K]
-  const int *S, *T, *R;  // grids (for the winner's (share, tp, replicas))
-  int nS, nT, nR;
-  uint64_t N;
-  const unsigned long long *keys;
-  const unsigned long long *counts;
-  alp_result *out;       // [n_t] device
-  unsigned long long *best;  // [n_t] scratch: ~0 between calls (self-resetting)
-  unsigned *done;            // [n_t] scratch: 0 between calls (self-resetting)
-};
 
 struct PredictArgs {
   DevProfiles prof;
@@ -116,12 +147,29 @@ struct PredictArgs {
   int *feasible;
 };
 
+// Launch with the programmatic-stream-serialization attribute (see pdl_wait).
+template <typename Args>
+inline cudaError_t launch_pdl(void (*fn)(Args), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const Args &a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool off = getenv("ALP_NO_PDL") != nullptr;  // A/B switch for measurements
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
 // Launchers (alp_kernels.cu). Return cudaError_t of the launch.
 cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st);
 cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
                              int n_work, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
-cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
+cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
 int search_max_blocks_per_sm(const SearchArgs &a);
 cudaError_t launch_egalitarian(const double *lat, int W, int G, long long *best_idx, double *best_min,

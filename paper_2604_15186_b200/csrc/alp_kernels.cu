@@ -27,62 +27,19 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
 
 #include "alp_internal.h"
+#include "alp_terms.cuh"
+#include "alp_finalize.cuh"
 
 namespace alp {
 
 __device__ __forceinline__ float finf() { return __int_as_float(0x7f800000); }
 
-// ------------------------------------------------------------------ option terms (FP64, no FMA)
-// SURVEY.md §8(c) / DESIGN.md §3: every operation is an explicit IEEE RNE intrinsic, in the
-// order written, so the result is bit-identical to the oracle's -ffp-contract=off C code.
-__device__ double lookup_latency(const double *r, const double *l, int P, double x) {
-  // R3: clamp below r_0; i = max{i : r_i <= x}; hold L_last at/after the last point.
-  if (x <= r[0]) return l[0];
-  int i = 0;
-  for (int j = 0; j < P; ++j)
-    if (r[j] <= x) i = j;
-  if (i == P - 1) return l[P - 1];
-  double dl = __dsub_rn(l[i + 1], l[i]);
-  double dx = __dsub_rn(x, r[i]);
-  double dr = __dsub_rn(r[i + 1], r[i]);
-  double w = __ddiv_rn(dx, dr);
-  return __dadd_rn(l[i], __dmul_rn(dl, w));
-}
-
-__device__ int option_terms(const DevProfiles &P, double lambda, int m, int k, float *tau, double *term,
-                            double *b, int *u) {
-  const int r_i = k % P.nR;
-  const int t_i = (k / P.nR) % P.nT;
-  const int s_i = k / (P.nR * P.nT);
-  const int s_units = P.S[s_i], t = P.T[t_i], d = P.R[r_i];
-  const int c = m * P.nT + t_i;
-  const double T = P.tmax[c];
-  const double lam_m = __dmul_rn(lambda, P.n[m]);              // lambda_m = lambda_W n_m
-  const double rate = __ddiv_rn(lam_m, (double)d);            // per replica
-  const double f = __ddiv_rn((double)s_units, (double)P.F);   // per-shard share
-  const double x = __ddiv_rn(rate, f);                        // L'(l) = L(l/f)/f
-  const double cap = __dmul_rn(f, T);
-  const double bb = __ddiv_rn(__dmul_rn((double)d, cap), P.n[m]);  // Eq. 2 term
-  int ok = (x <= T) && (bb >= lambda);                        // R4
-  if (P.min_units && s_units < P.min_units[c]) ok = 0;        // memory floor
-  *b = bb;
-  *u = s_units * t * d;
-  if (ok) {
-    const int o = P.prof_off[c];
-    const double L = lookup_latency(P.rate + o, P.lat + o, P.prof_off[c + 1] - o, x);
-    const double tt = __dmul_rn(__ddiv_rn(L, f), __ddiv_rn(P.n[m], P.p[m]));  // Eq. 1 term
-    *term = tt;
-    *tau = __double2float_rn(tt);
-  } else {
-    *term = CUDART_INF;
-    *tau = finf();
-  }
-  return ok;
-}
-
-__global__ void k_option_table(const OptionArgs A) {
+__global__ void k_option_table(const __grid_constant__ OptionArgs A) {
+  pdl_trigger();  // let K2 launch and stage its static tables while the terms are computed
   const int MK = A.prof.M * A.prof.K;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < A.n_targets) {
@@ -95,7 +52,7 @@ __global__ void k_option_table(const OptionArgs A) {
   float tau;
   double term, b;
   int u;
-  option_terms(A.prof, A.targets[t], m, k, &tau, &term, &b, &u);
+  option_terms(A.prof, A.targets ? A.targets[t] : A.tgt[t], m, k, &tau, &term, &b, &u);
   A.tau[i] = tau;
   A.term[i] = term;
   A.b[i] = b;
@@ -128,150 +85,11 @@ int search_max_blocks_per_sm(const SearchArgs &a) {
 }
 
 // ------------------------------------------------------------------ finalize (K3)
-// grid (nb, n_targets): the nb blocks of a target split the re-scan of the winning segment; the
-// last block to finish (ticket) assembles the result and resets the target's scratch.
-__global__ void k_finalize(const FinalizeArgs F) {
-  const SearchArgs &P = F.s;
+// grid (nb, n_targets): the nb blocks of a target split the re-scan of the winning segment.
+__global__ void k_finalize(const __grid_constant__ SearchArgs P) {
+  pdl_wait();  // keys/counts/terms come from K2 (or the all-reduce after it)
   const int t = blockIdx.y;
-  const unsigned long long key = F.keys[t];
-  const unsigned long long count = F.counts[t];
-  __shared__ unsigned long long s_best;
-  const int K = P.K;
-  const float *tau_t = P.tau + (size_t)t * P.M * K;
-  const uint32_t seg = (uint32_t)(key & 0xffffffffull);
-  const float val = __uint_as_float((uint32_t)(key >> 32));
-  const bool found = key != kKeyNone && val < finf();
-  uint32_t q = 0, chunk = 0, e = 0;
-  float Qrow = 0.f;
-  int Urow = 0;
-  if (found) {
-    q = seg % P.nQ;
-    const uint32_t row = seg / P.nQ;
-    chunk = row / P.L;
-    e = row % P.L;
-    // canonical partial sum over LLMs 0..g1-1 (digits of chunk then e, most significant first)
-    int kd[ALP_MAX_M];
-    uint32_t rem = chunk;
-    for (int m = P.g0 - 1; m >= 0; --m) { kd[m] = (int)(rem % (uint32_t)K); rem /= (uint32_t)K; }
-    rem = e;
-    for (int j = P.ng - 1; j >= 0; --j) { kd[P.g0 + j] = (int)(rem % (uint32_t)K); rem /= (uint32_t)K; }
-    for (int m = 0; m < P.g1; ++m) {
-      Qrow = __fadd_rn(Qrow, tau_t[m * K + kd[m]]);
-      Urow += P.u[m * K + kd[m]];
-    }
-  }
-  if (threadIdx.x == 0) {
-    s_best = ~0ull;
-  }
-  __syncthreads();
-  if (found) {
-    // the segment starts at a-range q and runs to the end of the row (see fold_rows)
-    const int a0 = (int)(q * P.A), a1 = P.Ka;
-    const unsigned long long n = (unsigned long long)(a1 - a0) * P.Kb;
-    unsigned long long mine = ~0ull;
-    for (unsigned long long li = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; li < n;
-         li += (unsigned long long)gridDim.x * blockDim.x) {
-      const int a = a0 + (int)(li / P.Kb), b = (int)(li % P.Kb);
-      float ta = 0.f;
-      int ua = 0;
-      if (P.a_llm >= 0) {
-        ta = tau_t[P.a_llm * K + a];
-        ua = P.u[P.a_llm * K + a];
-      }
-      const float v = __fadd_rn(__fadd_rn(Qrow, ta), tau_t[P.b_llm * K + b]);
-      const int units = Urow + ua + P.u[P.b_llm * K + b];
-      if (v == val && units <= qbudget(P, t)) {
-        mine = li;
-        break;
-      }
-    }
-    atomicMin(&s_best, mine);
-  }
-  __syncthreads();
-  // combine the blocks of this target: global min, then only the last block continues
-  __shared__ unsigned s_last;
-  if (threadIdx.x == 0) {
-    if (found) atomicMin(F.best + t, s_best);
-    __threadfence();
-    s_last = (atomicAdd(F.done + t, 1u) == gridDim.x - 1) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_best = atomicAdd(F.best + t, 0ull);  // coherent read of the combined minimum
-    F.best[t] = ~0ull;                    // reset for the next finalize on this scratch
-    F.done[t] = 0u;
-  }
-  __syncthreads();
-  // winner digits, then the per-LLM FP64 terms gathered in parallel (one thread per LLM)
-  __shared__ int s_k[ALP_MAX_M];
-  __shared__ double s_term[ALP_MAX_M], s_bterm[ALP_MAX_M];
-  __shared__ int s_u[ALP_MAX_M], s_grid[3][ALP_MAX_M];
-  const bool win = found && s_best != ~0ull;
-  if (threadIdx.x == 0 && win) {
-    const int a0 = (int)(q * P.A);
-    const int a = a0 + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
-    uint32_t rem = chunk;
-    for (int m = P.g0 - 1; m >= 0; --m) {
-      s_k[m] = (int)(rem % (uint32_t)K);
-      rem /= (uint32_t)K;
-    }
-    rem = e;
-    for (int j = P.ng - 1; j >= 0; --j) {
-      s_k[P.g0 + j] = (int)(rem % (uint32_t)K);
-      rem /= (uint32_t)K;
-    }
-    if (P.a_llm >= 0) s_k[P.a_llm] = a;
-    s_k[P.b_llm] = b;
-  }
-  __syncthreads();
-  if (win && (int)threadIdx.x < P.M) {
-    const int m = threadIdx.x, km = s_k[m];
-    s_term[m] = F.term[((size_t)t * P.M + m) * K + km];
-    s_bterm[m] = F.b[((size_t)t * P.M + m) * K + km];
-    s_u[m] = P.u[m * K + km];
-    if (F.S) {
-      s_grid[0][m] = F.S[km / (F.nR * F.nT)];
-      s_grid[1][m] = F.T[(km / F.nR) % F.nT];
-      s_grid[2][m] = F.R[km % F.nR];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  alp_result r;
-  memset(&r, 0, sizeof(r));
-  r.M = P.M;
-  r.feasible_count = count;
-  r.candidates = F.N;
-  r.index = ~0ull;
-  r.latency_key = finf();
-  if (win) {
-    unsigned long long idx = 0;
-    double L = 0.0, Tw = CUDART_INF;
-    long long U = 0;
-    for (int m = 0; m < P.M; ++m) {
-      idx = idx * (unsigned long long)K + (unsigned long long)s_k[m];
-      L = (m == 0) ? s_term[m] : __dadd_rn(L, s_term[m]);  // Eq. 1 in canonical order (FP64)
-      Tw = s_bterm[m] < Tw ? s_bterm[m] : Tw;               // Eq. 2
-      U += s_u[m];
-      if (F.S) {
-        r.share_units[m] = s_grid[0][m];
-        r.tp[m] = s_grid[1][m];
-        r.replicas[m] = s_grid[2][m];
-      }
-    }
-    r.found = 1;
-    r.index = idx;
-    r.latency_key = val;
-    r.latency = L;
-    r.throughput = Tw;
-    r.units = U;
-  } else {
-    r.latency = CUDART_INF;
-    r.throughput = 0.0;
-  }
-  F.out[t] = r;
+  finalize_target(P, t, P.fin.keys[t], P.fin.counts[t], blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------ multi-workflow split (NEXT-1)
@@ -359,9 +177,22 @@ __global__ void k_predict(const PredictArgs A) {
 }
 
 // ------------------------------------------------------------------ launchers
+// Every kernel of a search prefers the maximum shared-memory carveout, like K2, so consecutive
+// launches on a stream do not reconfigure the SMs' L1/shared split in between.
+static void max_carveout(const void *fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({fn, dev}).second)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
 cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st) {
   const int total = a.n_targets * a.prof.M * a.prof.K;
   const int n = max(max(total, a.n_targets), a.n_work);
+  max_carveout(reinterpret_cast<const void *>(k_option_table));
   k_option_table<<<(n + 255) / 256, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
@@ -369,16 +200,17 @@ cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st) {
 cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
                              int n_work, cudaStream_t st) {
   const int m = n > n_work ? n : n_work;
+  max_carveout(reinterpret_cast<const void *>(k_init_keys));
   k_init_keys<<<(m + 255) / 256, 256, 0, st>>>(keys, counts, n, work, n_work);
   return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st) {
+cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st) {
   // blocks per target for the winning-segment re-scan (<= Ka*Kb candidates): ~16 per thread
-  const long long cand = (long long)a.s.Ka * a.s.Kb;
+  const long long cand = (long long)a.Ka * a.Kb;
   const int nb = (int)std::min<long long>(64, std::max<long long>(1, cand / (256 * 16)));
-  k_finalize<<<dim3(nb, a.s.n_targets), 256, 0, st>>>(a);
-  return cudaGetLastError();
+  max_carveout(reinterpret_cast<const void *>(k_finalize));
+  return launch_pdl(k_finalize, dim3(nb, a.n_targets), dim3(256), 0, st, a);
 }
 
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st) {

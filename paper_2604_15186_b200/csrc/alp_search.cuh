@@ -7,7 +7,9 @@
 #include <map>
 #include <mutex>
 
+#include "alp_finalize.cuh"
 #include "alp_internal.h"
+#include "alp_terms.cuh"
 
 #ifndef ALP_A_UNROLL
 #define ALP_A_UNROLL 2  // a-loop unroll (tuned: 2 beats 1 on C3 and C4, profiles/r01_variant_sweep.txt)
@@ -48,6 +50,7 @@ struct Smem {
   int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
   float *btab;     // [rows][row_stride] masked rows
   float2 *pfx;     // [n_chunks] {prefix partial sum, bits(prefix units)} when P.off_pfx >= 0
+  float *opt;      // [M*K] option terms of the phase's target (fused mode)
 };
 
 constexpr int kBigUnits = 1 << 28;
@@ -101,14 +104,14 @@ __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *
   s.dcnt = s.dv + (P.Kb + 1);
   s.btab = reinterpret_cast<float *>(base + P.off_btab);
   s.pfx = reinterpret_cast<float2 *>(base + (P.off_pfx >= 0 ? P.off_pfx : 0));
+  s.opt = reinterpret_cast<float *>(base + (P.fz.on ? P.fz.off_opt : 0));
   return s;
 }
 
 // Build the per-(target, b-chunk) tables in shared memory.  All threads participate.
-__device__ inline void build_tables(const SearchArgs &P, const Smem &s, int t, int c, int R) {
+__device__ inline void build_tables(const SearchArgs &P, const Smem &s, const float *tau_t, int c, int R) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int K = P.K, D = row_of(P.dv, P.D, R);
-  const float *tau_t = P.tau + (size_t)t * P.M * K;
   const int c0 = c * P.bchunk_w;
   const int c1 = min(c0 + P.bchunk_w, P.Kb);
   for (int i = tid; i < P.g1 * K; i += nt) s.tau[i] = tau_t[i];
@@ -352,6 +355,59 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
   }
 }
 
+// Fused prologue: the option terms of target t (K1's arithmetic, alp_terms.cuh) into shared memory;
+// block 0 also publishes them (with the FP64 Eq. 1 / Eq. 2 terms) for the finalize.
+__device__ inline void fused_terms(const SearchArgs &P, const Smem &s, int t, bool publish) {
+  const int MK = P.M * P.K;
+  const bool wr = publish && blockIdx.x == 0;
+  for (int i = threadIdx.x; i < MK; i += blockDim.x) {
+    float tau;
+    if (P.fz.tau_fixed) {
+      tau = P.fz.tau_fixed[i];
+    } else {
+      double term, b;
+      int u;
+      option_terms(P.fz.prof, P.fz.tgt[t], i / P.K, i % P.K, &tau, &term, &b, &u);
+      if (wr) {
+        P.fz.o_term[(size_t)t * MK + i] = term;
+        P.fz.o_b[(size_t)t * MK + i] = b;
+      }
+    }
+    s.opt[i] = tau;
+    if (wr) P.fz.o_tau[(size_t)t * MK + i] = tau;
+  }
+  __syncthreads();
+}
+
+// Fused epilogue: the last block to finish writes the reduced (key, count) of every target, resets
+// the scratch to its rest state and (fz.finalize) finalizes every target.
+__device__ inline void fused_epilogue(const SearchArgs &P) {
+  __shared__ unsigned s_last;
+  __shared__ unsigned long long s_key[kInlineTargets], s_cnt[kInlineTargets];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(P.fz.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int t = threadIdx.x; t < P.n_targets; t += blockDim.x) {
+    unsigned long long k = atomicExch(P.fz.acc_keys + t, ~0ull);
+    const unsigned long long n = atomicExch(P.fz.acc_counts + t, 0ull);
+    if (k == ~0ull) k = kKeyNone;
+    P.keys[t] = k;
+    P.counts[t] = n;
+    s_key[t] = k;
+    s_cnt[t] = n;
+  }
+  for (int i = threadIdx.x; i < P.n_targets * P.n_bchunks; i += blockDim.x) P.fz.work[i] = 0ull;
+  if (threadIdx.x == 0) atomicExch(P.fz.ticket, 0u);
+  __syncthreads();
+  if (P.fz.finalize)
+    for (int t = 0; t < P.n_targets; ++t) finalize_target(P, t, s_key[t], s_cnt[t], 0, 1);
+}
+
 // T = rows per lane; MB = minimum resident blocks per SM (register cap 65536 / (256 * MB)).
 template <int T, int NB4, bool TAIL2, int MB>
 __global__ void __launch_bounds__(kThreads, MB)
@@ -359,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, MB)
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
   const Smem s = smem_layout(P, smem);
+  pdl_wait();  // option terms, zeroed work counters and keys come from K1
   for (int t = P.t_begin; t < P.t_end; ++t) {
     float best = finf();
     uint32_t best_seg = 0xffffffffu;
@@ -366,9 +423,15 @@ __global__ void __launch_bounds__(kThreads, MB)
     for (int c = P.c_begin; c < P.c_end; ++c) {
       __syncthreads();
       const int R = qbudget(P, t);
-      build_tables(P, s, t, c, R);
+      const float *tau_t = P.tau + (size_t)t * P.M * P.K;
+      if (P.fz.on) {
+        if (c == P.c_begin) fused_terms(P, s, t, true);  // kept in shared memory across b-chunks
+        tau_t = s.opt;
+      }
+      build_tables(P, s, tau_t, c, R);
       process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt, R, t * P.n_bchunks + c);
     }
+    if (t + 1 == P.t_end) pdl_trigger();  // K3 may launch; it waits for this grid to complete
     unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -389,10 +452,13 @@ __global__ void __launch_bounds__(kThreads, MB)
         k = red_key[w] < k ? red_key[w] : k;
         n += red_cnt[w];
       }
-      if (k != kKeyNone) atomicMin(P.keys + t, k);
-      if (n) atomicAdd(P.counts + t, n);
+      unsigned long long *kd = P.fz.on ? P.fz.acc_keys : P.keys;
+      unsigned long long *cd = P.fz.on ? P.fz.acc_counts : P.counts;
+      if (k != kKeyNone) atomicMin(kd + t, k);
+      if (n) atomicAdd(cd + t, n);
     }
   }
+  if (P.fz.on) fused_epilogue(P);
 }
 
 // Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
@@ -414,6 +480,7 @@ static cudaError_t ensure_smem(const void *fn, int bytes) {
   std::lock_guard<std::mutex> lock(mu);
   int &g = granted[{fn, dev}];
   if (bytes <= g) return cudaSuccess;
+  if (g == 0) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) g = bytes;
   return e;
@@ -424,8 +491,7 @@ static cudaError_t launch_one(const SearchArgs &a, int grid, cudaStream_t st) {
   auto fn = pick<T, NB4, TAIL2>(a);
   cudaError_t e = ensure_smem(reinterpret_cast<const void *>(fn), a.smem_bytes);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, a.smem_bytes, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(fn, dim3(grid), dim3(kThreads), (size_t)a.smem_bytes, st, a);
 }
 
 template <int T, int NB4, bool TAIL2>
