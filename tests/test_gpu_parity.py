@@ -344,3 +344,58 @@ def test_egalitarian_vs_oracle(P, names, gpus, F):
         tab = oracle.option_table(I, t)
         f, v, idx, cnt = dp.search(tab["tau"], tab["u"], g * F)
         _same(r, f, v, idx, cnt, (d["name"], g))
+
+
+# ----------------------------------------------------------------------------- fused vs classic launch paths
+@pytest.mark.parametrize("name", ["hand", "C1", "C2", "C4"])
+def test_fused_and_classic_paths_agree(P, name, monkeypatch):
+    """<= 8 targets run as one fused kernel (terms + search + finalize); ALP_NO_FUSED forces the
+    K1 + K2 + K3 path.  Both must give the same, oracle-identical results."""
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    lam0 = d["targets"][0]
+    lams = [lam0 * f for f in (0.5, 1.0, 1.7, 3.0, 40.0)]  # includes an infeasible target
+    alp = P.Alp.from_instance(d)
+    fused = alp.search_batch(lams, I.budget)
+    assert alp.last_launches == 1
+    monkeypatch.setenv("ALP_NO_FUSED", "1")
+    classic = alp.search_batch(lams, I.budget)
+    assert alp.last_launches == 3
+    monkeypatch.delenv("ALP_NO_FUSED")
+    for lam, a, b in zip(lams, fused, classic):
+        assert (a.found, a.index, a.feasible_count, a.units) == (b.found, b.index, b.feasible_count, b.units)
+        assert np.float32(a.latency_key).view(np.uint32) == np.float32(b.latency_key).view(np.uint32)
+        assert (a.latency == b.latency) or (not a.found)
+        assert a.throughput == b.throughput or not a.found
+        assert (a.share_units, a.tp, a.replicas) == (b.share_units, b.tp, b.replicas)
+        if name != "C4":
+            o = oracle.search(I, lam, I.budget, threads=4)
+            _same(a, o.found, o.latency_key, o.index, o.count, (name, lam))
+    # fused scratch returns to its rest state: repeating the search gives the same answer
+    again = alp.search_batch(lams, I.budget)
+    assert [(x.index, x.feasible_count) for x in again] == [(x.index, x.feasible_count) for x in fused]
+
+
+def test_fused_empty_shard_and_uneven_world(P):
+    """A rank with an empty item range still writes (KeyNone, 0) and the option terms its finalize
+    needs; more ranks than items is legal."""
+    import torch
+    d = generate.load("C1")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = [d["targets"][0]]
+    ref = alp.search(lam[0], I.budget)
+    items = alp.num_items(I.budget)
+    world = items + 3
+    keys = torch.empty((world, 1), dtype=torch.int64, device="cuda")
+    counts = torch.empty((world, 1), dtype=torch.int64, device="cuda")
+    for rank in range(world):
+        lo, hi = alp.shard_range(I.budget, rank, world)
+        alp.search_shard(lam, I.budget, lo, hi, keys[rank].data_ptr(), counts[rank].data_ptr())
+        torch.cuda.synchronize()
+        if hi == lo:
+            assert int(keys[rank, 0]) == 0x7FFFFFFFFFFFFFFF and int(counts[rank, 0]) == 0
+    k = keys.min(dim=0).values.contiguous()
+    c = counts.sum(dim=0).contiguous()
+    r = alp.finalize(lam, I.budget, k.data_ptr(), c.data_ptr())[0]
+    assert (r.index, r.feasible_count, r.latency_key) == (ref.index, ref.feasible_count, ref.latency_key)
