@@ -111,7 +111,7 @@ struct Arena {
     total = off + count * sizeof(T);
     fix.push_back({off, reinterpret_cast<void **>(dptr)});
   }
-  // H2D through a process-wide pinned staging buffer (one cudaMemcpyAsync; synchronises `st`).
+  // H2D through a process-wide pinned staging buffer (one cudaMemcpyAsync, stream-ordered on `st`).
   cudaError_t commit(void **base, uint64_t &h2d, cudaStream_t st) {
     static std::mutex mu;
     static void *pinned = nullptr;
@@ -131,9 +131,17 @@ struct Arena {
           return e;
         }
       }
+      // the staging buffer may still feed the previous (async) upload: wait for that copy only
+      static cudaEvent_t staged = nullptr;
+      if (staged) {
+        e = cudaEventSynchronize(staged);
+      } else {
+        e = cudaEventCreateWithFlags(&staged, cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) return e;
       memcpy(pinned, host.data(), copied);
       e = cudaMemcpyAsync(*base, pinned, copied, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaEventRecord(staged, st);
     }
     h2d += copied;
     for (auto &f : fix) *f.second = static_cast<unsigned char *>(*base) + f.first;
@@ -172,6 +180,42 @@ int ceil_log2(int k) {
 }
 
 }  // namespace
+
+// Stream + events of a handle, pooled process-wide per device: alp_build / alp_destroy are on the
+// end-to-end path, and creating a stream and six events costs more than the whole build otherwise.
+struct StreamCtx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;  // timing events
+  cudaEvent_t ready = nullptr, last = nullptr;                              // ordering only
+};
+std::mutex g_ctx_mu;
+std::vector<StreamCtx> g_ctx_pool;
+
+cudaError_t ctx_acquire(int device, StreamCtx &c) {
+  {
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    for (size_t i = 0; i < g_ctx_pool.size(); ++i)
+      if (g_ctx_pool[i].device == device) {
+        c = g_ctx_pool[i];
+        g_ctx_pool.erase(g_ctx_pool.begin() + i);
+        return cudaSuccess;
+      }
+  }
+  c.device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+  for (cudaEvent_t *ev : {&c.ev0, &c.ev1, &c.evs0, &c.evs1})
+    if (e == cudaSuccess) e = cudaEventCreate(ev);
+  for (cudaEvent_t *ev : {&c.ready, &c.last})
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  return e;
+}
+
+void ctx_release(const StreamCtx &c) {
+  if (!c.stream) return;
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  g_ctx_pool.push_back(c);
+}
 
 // Device copy of a static search plan (sort-list tiles, u-sorted b columns, units).  The plan depends
 // only on the grids (units table), rows per lane and the device, so handles with the same key share it.
@@ -245,7 +289,9 @@ struct alp_s {
   DBuf<int> d_opts, d_pfeas;
   DBuf<double> d_plat, d_pthr;
   DBuf<long long> d_punits;
-  cudaStream_t stream = nullptr;
+  StreamCtx ctx;                      // pooled stream + events (see ctx_acquire)
+  cudaStream_t stream = nullptr;      // == ctx.stream
+  cudaStream_t last_stream = nullptr; // last stream a search/finalize ran on (for alp_destroy)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool ev_pending = false;
   float last_ms = 0.f;
@@ -264,6 +310,9 @@ struct alp_s {
   }
 
   ~alp_s() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (ctx.stream && cur != device) cudaSetDevice(device);
     for (auto *b : {&g_targets, &g_term, &g_b, &d_plat, &d_pthr}) b->release();
     for (auto *b : {&d_opts, &d_pfeas, &g_qb}) b->release();
     g_tau.release();
@@ -274,13 +323,15 @@ struct alp_s {
     g_fbest.release();
     g_fdone.release();
     d_punits.release();
+    // stream-ordered release: after the last work on the handle's stream and on the last caller
+    // stream (alp_search_shard may run on a caller's stream), without a host synchronisation
+    if (stream && last_stream && last_stream != stream) {
+      cudaEventRecord(ctx.last, last_stream);
+      cudaStreamWaitEvent(stream, ctx.last, 0);
+    }
     if (d_arena) cudaFreeAsync(d_arena, stream);
-    if (stream) cudaStreamSynchronize(stream);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (evs0) cudaEventDestroy(evs0);
-    if (evs1) cudaEventDestroy(evs1);
-    if (stream) cudaStreamDestroy(stream);
+    ctx_release(ctx);
+    if (cur >= 0 && cur != device) cudaSetDevice(cur);
   }
 };
 
@@ -463,6 +514,7 @@ alp_status get_plan(alp_s *h) {
     A.add(h->dv, &P->d_dv);
     A.add(h->dcnt, &P->d_dcnt);
     CU(A.commit(&P->dev->mem, h->h2d, h->stream));
+    CU(cudaStreamSynchronize(h->stream));  // shared by handles on other streams (cold path only)
     P->N = h->N; P->a_llm = h->a_llm; P->b_llm = h->b_llm; P->Ka = h->Ka; P->Kb = h->Kb; P->g0 = h->g0;
     P->g1 = h->g1; P->ng = h->ng; P->dig_bits = h->dig_bits; P->umax_a = h->umax_a; P->umax_b = h->umax_b;
     P->L = h->L; P->n_chunks = h->n_chunks; P->n_groups = h->n_groups; P->nQ = h->nQ; P->A = h->A;
@@ -506,6 +558,16 @@ alp_status upload_all(alp_s *h) {
   }
   A.add(h->T, &h->d_T);
   A.add(h->R, &h->d_R);
+  // self-resetting scratch, initialised through the copied section (rest state), packed in one
+  // section: [fbest | fz keys x8 | fz counts x8 | fz work x64 | fdone, fz ticket (u32 pair)]
+  static const std::vector<unsigned long long> rest = [] {
+    std::vector<unsigned long long> v(1 + 2 * kInlineTargets + kArenaWork + 1, 0ull);
+    v[0] = ~0ull;
+    for (int i = 0; i < kInlineTargets; ++i) v[1 + i] = ~0ull;
+    return v;
+  }();
+  unsigned long long *d_rest = nullptr;
+  A.add(rest, &d_rest);
   A.scratch(1, &h->a_targets);
   A.scratch(MK, &h->a_tau);
   A.scratch(MK, &h->a_term);
@@ -515,17 +577,21 @@ alp_status upload_all(alp_s *h) {
   A.scratch(1, &h->a_counts);
   A.scratch(1, &h->a_qb);
   A.scratch(kArenaWork, &h->a_work);
-  // self-resetting scratch, initialised through the copied section (rest state)
-  static const std::vector<unsigned long long> ones1(1, ~0ull), onesT(kInlineTargets, ~0ull),
-      zerosT(kInlineTargets, 0ull), zerosW(kArenaWork, 0ull);
-  static const std::vector<unsigned> zero1(1, 0u);
-  A.add(ones1, &h->a_fbest);
-  A.add(zero1, &h->a_fdone);
-  A.add(onesT, &h->a_fzkeys);
-  A.add(zerosT, &h->a_fzcounts);
-  A.add(zerosW, &h->a_fzwork);
-  A.add(zero1, &h->a_fzticket);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
+  h->a_fbest = d_rest;
+  h->a_fzkeys = d_rest + 1;
+  h->a_fzcounts = d_rest + 1 + kInlineTargets;
+  h->a_fzwork = d_rest + 1 + 2 * kInlineTargets;
+  h->a_fdone = reinterpret_cast<unsigned *>(d_rest + 1 + 2 * kInlineTargets + kArenaWork);
+  h->a_fzticket = h->a_fdone + 1;
+  CU(cudaEventRecord(h->ctx.ready, h->stream));  // searches on other streams wait for the upload
+  return ALP_OK;
+}
+
+// Order a caller's stream after the handle's upload; remember it for alp_destroy.
+alp_status use_stream(alp_s *h, cudaStream_t st) {
+  if (st != h->stream) CU(cudaStreamWaitEvent(st, h->ctx.ready, 0));
+  h->last_stream = st;
   return ALP_OK;
 }
 
@@ -537,18 +603,18 @@ alp_status init_device(alp_s *h) {
   if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = std::min(4, std::max(2, atoi(v)));
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
-  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  {  // keep freed handle memory in the default pool so the next alp_build reuses it cheaply
+  CU(ctx_acquire(h->device, h->ctx));
+  h->stream = h->ctx.stream;
+  h->ev0 = h->ctx.ev0; h->ev1 = h->ctx.ev1; h->evs0 = h->ctx.evs0; h->evs1 = h->ctx.evs1;
+  static std::once_flag pool_once[64];
+  std::call_once(pool_once[h->device & 63], [&] {
+    // keep freed handle memory in the default pool so the next alp_build reuses it cheaply
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-  }
-  CU(cudaEventCreate(&h->ev0));
-  CU(cudaEventCreate(&h->ev1));
-  CU(cudaEventCreate(&h->evs0));
-  CU(cudaEventCreate(&h->evs1));
+  });
   return ALP_OK;
 }
 
@@ -786,6 +852,8 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
+  s = use_stream(h, st);
+  if (s != ALP_OK) return s;
   CU(cudaEventRecord(h->evs0, st));
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
@@ -888,7 +956,9 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
                          alp_result *out) {
   if (!out) return fail(ALP_EINVAL, "out is NULL");
   CU(cudaSetDevice(h->device));
-  alp_status s = ensure_scratch(h, n);
+  alp_status s = use_stream(h, st);
+  if (s != ALP_OK) return s;
+  s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   if (budgets) {
     s = prepare_budgets(h, budgets, n, st, &budget);
