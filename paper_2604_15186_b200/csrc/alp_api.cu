@@ -247,6 +247,7 @@ struct alp_s {
   std::vector<int> tile_s, bperm, bu, dv, dcnt;
   std::vector<uint32_t> tile_e, tile_off;
   int rows_per_lane = 8;
+  int nq_force = 0;    // ALP_NQ: a-ranges per row (tuning), 0 = automatic
   int min_blocks = 0;  // 0: per rows-per-lane default (T = 8: 3 blocks/SM, T = 16: 2); ALP_BLOCKS_PER_SM overrides
   int umax_a = 0, umax_b = 0;
   long long umax_total = 0;
@@ -268,7 +269,7 @@ struct alp_s {
   DBuf<double> g_targets, g_term, g_b;
   DBuf<float> g_tau;
   DBuf<alp_result> g_res;
-  DBuf<unsigned long long> g_keys, g_counts, g_work;
+  DBuf<unsigned long long> g_keys, g_counts, g_work, g_dbg;
   int *a_qb = nullptr;
   unsigned long long *a_fbest = nullptr;  // finalize scratch (1 target), ~0 / 0 between calls
   unsigned *a_fdone = nullptr;
@@ -320,6 +321,7 @@ struct alp_s {
     g_keys.release();
     g_counts.release();
     g_work.release();
+    g_dbg.release();
     g_fbest.release();
     g_fdone.release();
     d_punits.release();
@@ -454,6 +456,7 @@ alp_status make_plan(alp_s *h) {
   const uint64_t want = (uint64_t)h->sm_count * 24 * 24;
   uint32_t nQ = 1;
   while ((uint64_t)h->n_chunks * h->n_groups * nQ < want && nQ < (uint32_t)h->Ka) ++nQ;
+  if (h->nq_force > 0) nQ = (uint32_t)std::min(h->nq_force, h->Ka);  // ALP_NQ (tuning)
   h->A = (uint32_t)((h->Ka + nQ - 1) / nQ);
   h->nQ = (uint32_t)((h->Ka + h->A - 1) / h->A);
   while ((uint64_t)h->n_chunks * h->L * h->nQ >= (1ull << 32)) {
@@ -483,7 +486,7 @@ std::map<std::string, std::shared_ptr<PlanSnap>> g_plans;
 std::string plan_key(const alp_s *h) {
   std::string k;
   auto put = [&](const void *p, size_t n) { k.append(static_cast<const char *>(p), n); };
-  const int hdr[5] = {h->device, h->sm_count, h->M, h->K, h->rows_per_lane};
+  const int hdr[6] = {h->device, h->sm_count, h->M, h->K, h->rows_per_lane, h->nq_force};
   put(hdr, sizeof(hdr));
   put(h->u.data(), h->u.size() * sizeof(int));
   return k;
@@ -601,6 +604,7 @@ alp_status init_device(alp_s *h) {
   h->rows_per_lane = (h->K >= 64) ? 16 : 8;
   if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 16) ? 16 : 8;
   if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = std::min(4, std::max(2, atoi(v)));
+  if (const char *v = getenv("ALP_NQ")) h->nq_force = std::max(0, atoi(v));
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   CU(ctx_acquire(h->device, h->ctx));
@@ -671,7 +675,7 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
     a.off_u = off; off = align16(off + h->g0 * h->K * 4);
     a.off_a = off; off = align16(off + h->Ka * 8);
     a.off_lut = off; off = align16(off + (a.budget + 2) * 8);
-    a.off_tmp = off; off = align16(off + (2 * h->Kb + 3) * 4);
+    a.off_tmp = off; off = align16(off + (3 * h->Kb + 3 + h->Ka) * 4);  // dv, dcnt, bperm, ua
     a.off_btab = off; off = align16(off + rows * a.row_stride * 4);
     a.off_pfx = -1;
     if (h->g0 > 0 && h->n_chunks <= kPfxTableMax) {
@@ -911,14 +915,36 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   if (hi > lo || fused) {  // the fused launch also computes the terms and writes keys/counts
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
     g.a.work = work;
-    // ~16 grabs per warp; the last ~1/8 of the items go in grabs a quarter that size (tail balance)
+    // ~16 grabs per warp; the last ~1/8 of the items go in grabs a quarter that size (tail balance;
+    // finer a-ranges balance the tail better but cost more in the bulk: measured)
     const uint64_t warps = (uint64_t)g.grid * (kThreads / 32);
     const uint64_t n_items = hi - lo;
     g.a.grab = (int)std::max<uint64_t>(1, std::min<uint64_t>(1u << 20, n_items / (warps * 16)));
     g.a.grab2 = std::max(1, g.a.grab / 4);
     g.a.grab_t1 = (n_items - n_items / 8) / (uint64_t)g.a.grab;
+    static const bool dbg = getenv("ALP_DBG_TS") != nullptr;  // per-block timeline (diagnostics)
+    if (dbg) {
+      CU(h->g_dbg.ensure((size_t)g.grid * 8));
+      CU(cudaMemsetAsync(h->g_dbg.p, 0, (size_t)g.grid * 8 * sizeof(unsigned long long), st));
+      g.a.dbg_ts = h->g_dbg.p;
+    }
     CU(launch_search(g.a, g.grid, st));
     launches += 1;
+    if (dbg) {
+      std::vector<unsigned long long> ts((size_t)g.grid * 8);
+      CU(cudaMemcpyAsync(ts.data(), h->g_dbg.p, ts.size() * 8, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < g.grid; ++b) t0 = std::min(t0, ts[b * 8]);
+      std::vector<double> v[5];
+      for (int b = 0; b < g.grid; ++b)
+        for (int i = 0; i < 5; ++i) v[i].push_back(ts[b * 8 + i] ? (ts[b * 8 + i] - t0) * 1e-3 : 0.0);
+      for (auto &x : v) std::sort(x.begin(), x.end());
+      auto q = [&](int i, double f) { return v[i][(size_t)(f * (v[i].size() - 1))]; };
+      fprintf(stderr, "[alp dbg] grid %d us: start med %.1f max %.1f | terms med %.1f max %.1f | tables med %.1f "
+              "max %.1f | loop-end min %.1f med %.1f max %.1f | end max %.1f\n", g.grid, q(0, .5), q(0, 1), q(4, .5),
+              q(4, 1), q(1, .5), q(1, 1), q(2, 0), q(2, .5), q(2, 1), q(3, 1));
+    }
   }
   CU(cudaEventRecord(h->ev1, st));
   h->ev_pending = true;
@@ -1190,11 +1216,12 @@ alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, i
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (world < 1 || rank < 0 || rank >= world) return fail(ALP_EINVAL, "need 0 <= rank < world");
   if (!lo || !hi) return fail(ALP_EINVAL, "lo/hi is NULL");
-  const uint64_t n = alp_num_items(h, budget_units);
-  // contiguous, balanced to +-1 item; computed without overflow for n < 2^63
-  const uint64_t q = n / (uint64_t)world, r = n % (uint64_t)world;
-  *lo = q * (uint64_t)rank + std::min<uint64_t>((uint64_t)rank, r);
-  *hi = *lo + q + ((uint64_t)rank < r ? 1 : 0);
+  // contiguous, balanced to +-1 row of nQ items (a lane tile's a-ranges stay on one rank, so
+  // bulk work grabs start tile-aligned); computed without overflow for n < 2^63
+  const uint64_t nq = h->nQ, rows = alp_num_items(h, budget_units) / nq;
+  const uint64_t q = rows / (uint64_t)world, r = rows % (uint64_t)world;
+  *lo = (q * (uint64_t)rank + std::min<uint64_t>((uint64_t)rank, r)) * nq;
+  *hi = *lo + (q + ((uint64_t)rank < r ? 1 : 0)) * nq;
   return ALP_OK;
 }
 

@@ -56,6 +56,7 @@ struct OptionArgs {
   int n_work;
 };
 
+
 // Finalize inputs/outputs (K3, or the fused search's last block).
 struct FinalizeExtra {
   const double *term;    // [n_t][M][K] FP64 Eq. 1 terms
@@ -128,6 +129,7 @@ struct SearchArgs {
   unsigned long long *counts;
   FusedArgs fz;
   FinalizeExtra fin;
+  unsigned long long *dbg_ts;  // [grid][8] %globaltimer stamps per block (ALP_DBG_TS) or nullptr
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
   int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it

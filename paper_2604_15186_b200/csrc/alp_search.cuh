@@ -48,6 +48,8 @@ struct Smem {
   int2 *lut;       // [R+2] {shared address of the masked row, #finite entries in it} for r = -1..R
   int *dv;         // [D] distinct b unit values <= R, ascending
   int *dcnt;       // [D+1] #u-sorted columns with u <= dv[i-1]
+  int *bperm;      // [Kb] canonical b option of u-sorted column j
+  int *ua;         // [Ka] units of the a options
   float *btab;     // [rows][row_stride] masked rows
   float2 *pfx;     // [n_chunks] {prefix partial sum, bits(prefix units)} when P.off_pfx >= 0
   float *opt;      // [M*K] option terms of the phase's target (fused mode)
@@ -56,16 +58,16 @@ struct Smem {
 constexpr int kBigUnits = 1 << 28;
 
 // a-table entry for option a (infeasible a gets +inf units -> maps to the all-+inf row)
-__device__ __forceinline__ float2 a_entry(const SearchArgs &P, const float *tau_t, int a) {
+__device__ __forceinline__ float2 a_entry(const SearchArgs &P, const float *tau_t, const int *ua, int a) {
   if (P.a_llm < 0) return make_float2(0.f, __int_as_float(0));
   const float ta = tau_t[P.a_llm * P.K + a];
-  return make_float2(ta, __int_as_float(ta < __int_as_float(0x7f800000) ? -P.u[P.a_llm * P.K + a] : -kBigUnits));
+  return make_float2(ta, __int_as_float(ta < __int_as_float(0x7f800000) ? -ua[a] : -kBigUnits));
 }
 // masked-row element (row, j) of b-chunk [c0, c1): tau_b of the j-th u-sorted column if it fits
-__device__ __forceinline__ float btab_entry(const SearchArgs &P, const float *tau_t, const int *dcnt, int row, int j,
-                                            int c0, int c1) {
+__device__ __forceinline__ float btab_entry(const SearchArgs &P, const float *tau_t, const int *dcnt,
+                                            const int *bperm, int row, int j, int c0, int c1) {
   const int len = min(max(dcnt[row], c0), c1) - c0;
-  return (j < len) ? tau_t[P.b_llm * P.K + P.bperm[c0 + j]] : __int_as_float(0x7f800000);
+  return (j < len) ? tau_t[P.b_llm * P.K + bperm[c0 + j]] : __int_as_float(0x7f800000);
 }
 // masked-row index for remaining budget r: #{distinct b unit values <= r}
 __device__ __forceinline__ int row_of(const int *dv, int D, int r) {
@@ -102,6 +104,8 @@ __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *
   s.lut = reinterpret_cast<int2 *>(base + P.off_lut);
   s.dv = reinterpret_cast<int *>(base + P.off_tmp);
   s.dcnt = s.dv + (P.Kb + 1);
+  s.bperm = s.dcnt + (P.Kb + 2);
+  s.ua = s.bperm + P.Kb;
   s.btab = reinterpret_cast<float *>(base + P.off_btab);
   s.pfx = reinterpret_cast<float2 *>(base + (P.off_pfx >= 0 ? P.off_pfx : 0));
   s.opt = reinterpret_cast<float *>(base + (P.fz.on ? P.fz.off_opt : 0));
@@ -109,9 +113,31 @@ __device__ __forceinline__ Smem smem_layout(const SearchArgs &P, unsigned char *
 }
 
 // Build the per-(target, b-chunk) tables in shared memory.  All threads participate.
+// The target-independent tables (static plan) in shared memory, once per block, before the
+// option terms exist: one wave of global loads (no dependency on K1 / the fused prologue).
+// Asynchronous copies (cp.async, no register staging): the thread goes on to the option terms
+// while they land; cp_async_wait() + a barrier make them visible.
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ inline void load_static(const SearchArgs &P, const Smem &s) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < P.g0 * P.K; i += nt) cp_async4(s.u + i, P.u + i);
+  for (int i = tid; i < P.D; i += nt) cp_async4(s.dv + i, P.dv + i);
+  for (int i = tid; i <= P.D; i += nt) cp_async4(s.dcnt + i, P.dcnt + i);
+  for (int i = tid; i < P.Kb; i += nt) cp_async4(s.bperm + i, P.bperm + i);
+  if (P.a_llm >= 0)
+    for (int i = tid; i < P.Ka; i += nt) cp_async4(s.ua + i, P.u + P.a_llm * P.K + i);
+}
+
+// Build the per-(target, b-chunk) tables in shared memory.  All threads participate; the static
+// tables (load_static) are visible (a barrier separates them).
 __device__ inline void build_tables(const SearchArgs &P, const Smem &s, const float *tau_t, int c, int R) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int K = P.K, D = row_of(P.dv, P.D, R);
+  const int K = P.K, D = row_of(s.dv, P.D, R);
   const int c0 = c * P.bchunk_w;
   const int c1 = min(c0 + P.bchunk_w, P.Kb);
   for (int i = tid; i < P.g1 * K; i += nt) s.tau[i] = tau_t[i];
@@ -119,16 +145,12 @@ __device__ inline void build_tables(const SearchArgs &P, const Smem &s, const fl
     s.tau[P.g1 * K] = 0.f;         // unused sort-group digit slot: x + 0 = x exactly
     s.tau[P.g1 * K + 1] = finf();  // padded (dummy) row
   }
-  for (int i = tid; i < P.g0 * K; i += nt) s.u[i] = P.u[i];
-  for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, a);
-  for (int i = tid; i < D; i += nt) s.dv[i] = P.dv[i];
-  for (int i = tid; i <= D; i += nt) s.dcnt[i] = P.dcnt[i];
-  __syncthreads();
+  for (int a = tid; a < P.Ka; a += nt) s.a[a] = a_entry(P, tau_t, s.ua, a);
   // masked row i holds the u-sorted columns [c0, c1) with u <= dv[i-1] (row 0: none), +inf elsewhere
   const int rows = D + 1;
   for (int i = tid; i < rows * P.bchunk_wpad; i += nt) {
     const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
-    s.btab[row * P.row_stride + j] = btab_entry(P, tau_t, s.dcnt, row, j, c0, c1);
+    s.btab[row * P.row_stride + j] = btab_entry(P, tau_t, s.dcnt, s.bperm, row, j, c0, c1);
   }
   __syncthreads();
   // finite entries per masked row (feasible b count), kept in the row's padding column
@@ -360,6 +382,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
 __device__ inline void fused_terms(const SearchArgs &P, const Smem &s, int t, bool publish) {
   const int MK = P.M * P.K;
   const bool wr = publish && blockIdx.x == 0;
+  const DevProfiles &sp = P.fz.prof;
   for (int i = threadIdx.x; i < MK; i += blockDim.x) {
     float tau;
     if (P.fz.tau_fixed) {
@@ -367,7 +390,7 @@ __device__ inline void fused_terms(const SearchArgs &P, const Smem &s, int t, bo
     } else {
       double term, b;
       int u;
-      option_terms(P.fz.prof, P.fz.tgt[t], i / P.K, i % P.K, &tau, &term, &b, &u);
+      option_terms(sp, P.fz.tgt[t], i / P.K, i % P.K, &tau, &term, &b, &u);
       if (wr) {
         P.fz.o_term[(size_t)t * MK + i] = term;
         P.fz.o_b[(size_t)t * MK + i] = b;
@@ -415,22 +438,37 @@ __global__ void __launch_bounds__(kThreads, MB)
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long red_key[kThreads / 32], red_cnt[kThreads / 32];
   const Smem s = smem_layout(P, smem);
-  pdl_wait();  // option terms, zeroed work counters and keys come from K1
+  auto stamp = [&](int i) {
+    if (P.dbg_ts && threadIdx.x == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      P.dbg_ts[blockIdx.x * 8 + i] = g;
+    }
+  };
+  stamp(0);
+  load_static(P, s);  // static plan tables: independent of K1, in flight during the option terms
+  pdl_wait();         // option terms, zeroed work counters and keys come from K1
   for (int t = P.t_begin; t < P.t_end; ++t) {
     float best = finf();
     uint32_t best_seg = 0xffffffffu;
     unsigned long long cnt = 0ull;
     for (int c = P.c_begin; c < P.c_end; ++c) {
-      __syncthreads();
+      const bool first = (t == P.t_begin && c == P.c_begin);
+      if (!first) __syncthreads();  // the previous phase is done with the shared tables
       const int R = qbudget(P, t);
       const float *tau_t = P.tau + (size_t)t * P.M * P.K;
-      if (P.fz.on) {
-        if (c == P.c_begin) fused_terms(P, s, t, true);  // kept in shared memory across b-chunks
-        tau_t = s.opt;
+      if (P.fz.on && c == P.c_begin) fused_terms(P, s, t, true);  // kept in shared memory across b-chunks
+      if (first) {
+        cp_async_wait();
+        __syncthreads();  // static tables (and the fused option terms) visible
+        stamp(4);
       }
+      if (P.fz.on) tau_t = s.opt;
       build_tables(P, s, tau_t, c, R);
+      if (t == P.t_begin && c == P.c_begin) stamp(1);
       process_items<T, NB4, TAIL2>(P, s, smem, best, best_seg, cnt, R, t * P.n_bchunks + c);
     }
+    if (t + 1 == P.t_end) stamp(2);
     if (t + 1 == P.t_end) pdl_trigger();  // K3 may launch; it waits for this grid to complete
     unsigned long long key = (best < finf()) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
 #pragma unroll
@@ -459,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, MB)
     }
   }
   if (P.fz.on) fused_epilogue(P);
+  stamp(3);
 }
 
 // Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
