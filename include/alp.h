@@ -20,7 +20,9 @@
  *    No C++ exception crosses this boundary.
  *  - alp_build copies every input array; the caller may free them on return.  The handle owns
  *    host copies plus device tables on the device current at build time.  A handle may be used
- *    by one host thread at a time.
+ *    by one host thread at a time; its calls are ordered on the device even across streams (a
+ *    call on another stream waits for the handle's previous work), and alp_destroy releases
+ *    device memory stream-ordered after that work (no host synchronisation).
  *  - Budgets are integer GPU units (1 unit = 1/F GPU); targets are workflow requests/second.
  *  - All results are bit-identical for any rank count / grid shape (see alp_search_shard).
  */

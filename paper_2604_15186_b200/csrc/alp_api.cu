@@ -591,9 +591,14 @@ alp_status upload_all(alp_s *h) {
   return ALP_OK;
 }
 
-// Order a caller's stream after the handle's upload; remember it for alp_destroy.
+// Order a caller's stream after the handle's upload and after the handle's previous work on
+// another stream (the per-handle scratch is reused by every call); remember it for alp_destroy.
 alp_status use_stream(alp_s *h, cudaStream_t st) {
   if (st != h->stream) CU(cudaStreamWaitEvent(st, h->ctx.ready, 0));
+  if (h->last_stream && h->last_stream != st) {
+    CU(cudaEventRecord(h->ctx.last, h->last_stream));
+    CU(cudaStreamWaitEvent(st, h->ctx.last, 0));
+  }
   h->last_stream = st;
   return ALP_OK;
 }
@@ -1158,6 +1163,8 @@ alp_status alp_option_table(alp_t *h, double lambda, float *tau, double *term, d
   alp_status s = check_targets(&lambda, 1);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
+  s = use_stream(h, h->stream);
+  if (s != ALP_OK) return s;
   s = ensure_scratch(h, 1);
   if (s != ALP_OK) return s;
   s = option_tables(h, &lambda, 1, h->stream, nullptr, nullptr);
@@ -1181,6 +1188,8 @@ alp_status alp_predict(alp_t *h, const int32_t *opts, int32_t n, double lambda, 
   for (long long i = 0; i < (long long)n * h->M; ++i)
     if (opts[i] < 0 || opts[i] >= h->K) return fail(ALP_EINVAL, "opts[%lld] out of range 0..K-1", i);
   CU(cudaSetDevice(h->device));
+  s = use_stream(h, h->stream);
+  if (s != ALP_OK) return s;
   CU(h->d_opts.ensure((size_t)n * h->M));
   CU(h->d_plat.ensure(n));
   CU(h->d_pthr.ensure(n));

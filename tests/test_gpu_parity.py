@@ -399,3 +399,31 @@ def test_fused_empty_shard_and_uneven_world(P):
     c = counts.sum(dim=0).contiguous()
     r = alp.finalize(lam, I.budget, k.data_ptr(), c.data_ptr())[0]
     assert (r.index, r.feasible_count, r.latency_key) == (ref.index, ref.feasible_count, ref.latency_key)
+
+
+def test_cross_stream_calls_are_ordered(P):
+    """An async shard search on a caller stream followed at once by a search on the handle's own
+    stream: the second call waits for the first (they share the handle's scratch)."""
+    import torch
+    d = generate.load("C4")
+    B = d["budget_units"]
+    lam = d["targets"][0]
+    alp = P.Alp.from_instance(d)
+    lo, hi = alp.shard_range(B, 0, 1)
+    keys = torch.empty(1, dtype=torch.int64, device="cuda")
+    counts = torch.empty(1, dtype=torch.int64, device="cuda")
+    st = torch.cuda.Stream()
+    alp.search_shard([lam], B, lo, hi, keys.data_ptr(), counts.data_ptr(), st.cuda_stream)
+    st.synchronize()
+    ref_key, ref_cnt = int(keys[0]), int(counts[0])
+    ref_half = alp.search(lam * 0.5, B)
+    for _ in range(3):
+        keys.fill_(0)
+        counts.fill_(0)
+        torch.cuda.synchronize()
+        alp.search_shard([lam], B, lo, hi, keys.data_ptr(), counts.data_ptr(), st.cuda_stream)  # async
+        r = alp.search(lam * 0.5, B)  # handle stream, issued while the shard search may still run
+        st.synchronize()
+        assert (int(keys[0]), int(counts[0])) == (ref_key, ref_cnt)
+        assert (r.index, r.feasible_count, r.latency_key) == (ref_half.index, ref_half.feasible_count,
+                                                              ref_half.latency_key)
