@@ -1,16 +1,29 @@
 #!/bin/bash
-# Round-end measurement set (one GPU): tests, smoke, C4 bench (+ ncu), C5 and C3 bench lines.
+# Round-end measurement set (one GPU): tests, smoke, bench lines (C4 headline with CPU oracle leg,
+# C3, C5, reference arm), device timeline, shard timing, 2-rank gloo path, ncu launch list and a
+# full ncu capture of the search kernel on C4 (plus C3), microbenchmark.
+set -u
 mkdir -p gpurun_out
-bash tools/gpu_check.sh
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu_info.txt 2>&1
+lscpu | grep -E "Model name|^CPU\(s\)|Socket|Core" > gpurun_out/host_cpu.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
+timeout 600 python bench.py > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err
+timeout 600 python bench.py --workload C3 --steps 50 --warmup 3 --e2e-steps 3 > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err
 timeout 600 python bench.py --workload C5 --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
-timeout 600 python bench.py --workload C3 --steps 50 --warmup 3 --e2e-steps 2 > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err
-ALP_TRACE=1 timeout 120 python -c "
-import time, sys; sys.path.insert(0, '.')
-import paper_2604_15186_b200 as P
-from workloads import generate
-d = generate.load('C4'); desc = P.Desc(d)
-for i in range(5):
-    t0 = time.perf_counter(); a = P.Alp.build(desc); t1 = time.perf_counter()
-    r = a.search(d['targets'][0], d['budget_units']); t2 = time.perf_counter(); a.close(); t3 = time.perf_counter()
-    print(f'build {1e3*(t1-t0):.3f} ms search {1e3*(t2-t1):.3f} ms destroy {1e3*(t3-t2):.3f} ms')
-" > gpurun_out/trace_e2e.txt 2>&1
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+python tools/step_timeline.py --workload C4 --mode search > gpurun_out/timeline_C4_search.txt 2>/dev/null
+python tools/step_timeline.py --workload C4 --mode shard > gpurun_out/timeline_C4_shard.txt 2>/dev/null
+(python tools/shard_timing.py C4; python tools/shard_timing.py C3) > gpurun_out/shard_timing.jsonl 2>&1
+ALP_DBG_TS=1 python tools/shard_timing.py C4 2>&1 | grep "alp dbg" | awk 'NR%20==10' > gpurun_out/block_timeline_C4.txt
+bash tools/multirank_check.sh > gpurun_out/multirank.txt 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pipes5 tools/microbench/pipes5.cu && /tmp/pipes5 > gpurun_out/mb_pipes5.txt 2>&1
+if [ "${NCU:-1}" = "1" ]; then
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+   python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launch_bench.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_search -s 3 -c 1 -f -o gpurun_out/prof_search \
+   python bench.py --steps 1 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_full.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_search -s 3 -c 1 -f -o gpurun_out/prof_search_C3 \
+   python bench.py --workload C3 --steps 1 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_full_C3.txt 2>&1
+fi
+tail -2 gpurun_out/pytest_gpu.txt; cat gpurun_out/smoke.txt; head -c 400 gpurun_out/bench_C4.json; echo
