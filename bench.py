@@ -295,7 +295,9 @@ def run_ours(args):
                        "feasible_count": res.feasible_count},
             "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcandidates/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_search (K2)", "kernel_ms": kern_max / len(kern_ms),
+                         "kernel": ("k_search (fused: option terms + search + finalize)" if world == 1
+                                    else "k_search (shard: option terms + search)"),
+                         "kernel_ms": kern_max / len(kern_ms),
                          "peak_def": f"{sm_count} SMs x 128 issue lanes/clk x {f_max / 1e6:.0f} MHz / 1 instr per candidate"},
             "e2e": {"value": N * nt * len(e2e_ms) / (e2e_tot * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(P.ctypes.sizeof(P._Result)),
