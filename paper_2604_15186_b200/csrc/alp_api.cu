@@ -604,10 +604,13 @@ alp_status use_stream(alp_s *h, cudaStream_t st) {
 }
 
 alp_status init_device(alp_s *h) {
-  // rows per lane: 16 when the b rows are long (more candidates per lane tile), else 8 (tuned on
-  // C3 / C4, profiles/r01_variant_sweep.txt); ALP_ROWS_PER_LANE overrides.
-  h->rows_per_lane = (h->K >= 64) ? 16 : 8;
-  if (const char *v = getenv("ALP_ROWS_PER_LANE")) h->rows_per_lane = (atoi(v) == 16) ? 16 : 8;
+  // rows per lane: 12 at 2 blocks/SM (no register cap) beats 8 at 3 blocks/SM and 16 on both C4
+  // and C3 (profiles/r01_rows_per_lane.txt); ALP_ROWS_PER_LANE (8 / 12 / 16) overrides.
+  h->rows_per_lane = 12;
+  if (const char *v = getenv("ALP_ROWS_PER_LANE")) {
+    const int t = atoi(v);
+    h->rows_per_lane = (t == 16 || t == 12) ? t : 8;
+  }
   if (const char *v = getenv("ALP_BLOCKS_PER_SM")) h->min_blocks = std::min(4, std::max(2, atoi(v)));
   if (const char *v = getenv("ALP_NQ")) h->nq_force = std::max(0, atoi(v));
   CU(cudaGetDevice(&h->device));

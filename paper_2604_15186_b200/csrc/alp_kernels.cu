@@ -73,15 +73,21 @@ __global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts
 // The kernel templates live in alp_search.cuh; each rows-per-lane value is its own translation unit.
 cudaError_t launch_search_t8(const SearchArgs &a, int grid, cudaStream_t st);
 cudaError_t launch_search_t16(const SearchArgs &a, int grid, cudaStream_t st);
+cudaError_t launch_search_t12(const SearchArgs &a, int grid, cudaStream_t st);
+int occ_search_t12(const SearchArgs &a);
 int occ_search_t8(const SearchArgs &a);
 int occ_search_t16(const SearchArgs &a);
 
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st) {
-  return a.rows_per_lane == 16 ? launch_search_t16(a, grid, st) : launch_search_t8(a, grid, st);
+  if (a.rows_per_lane == 16) return launch_search_t16(a, grid, st);
+  if (a.rows_per_lane == 12) return launch_search_t12(a, grid, st);
+  return launch_search_t8(a, grid, st);
 }
 
 int search_max_blocks_per_sm(const SearchArgs &a) {
-  return a.rows_per_lane == 16 ? occ_search_t16(a) : occ_search_t8(a);
+  if (a.rows_per_lane == 16) return occ_search_t16(a);
+  if (a.rows_per_lane == 12) return occ_search_t12(a);
+  return occ_search_t8(a);
 }
 
 // ------------------------------------------------------------------ finalize (K3)

@@ -501,7 +501,8 @@ __global__ void __launch_bounds__(kThreads, MB)
 }
 
 // Host-side dispatch over rows per lane (T) and the b-chunk width specialisations.
-// Register-cap variants: T = 8 -> 3 (default) or 4 blocks/SM; T = 16 -> 2 (default) or 3
+// Register-cap variants: T = 8 -> 3 (default) or 4 blocks/SM; T = 12 and T = 16 -> 2 (default)
+// or 3 (T = 12 under the 3-block cap spills and is 4 % slower on C4)
 // (min_blocks 0 = the default).
 template <int T, int NB4, bool TAIL2>
 static auto pick(const SearchArgs &a) {
