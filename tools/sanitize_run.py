@@ -1,18 +1,27 @@
-"""Small searches for compute-sanitizer (memcheck / racecheck / synccheck): hand case, C1, a
-two-LLM slice of the C3 grid (K = 512: b-chunked masked tables, 16 rows per lane) and a target batch."""
+"""Small searches for compute-sanitizer (memcheck / racecheck / synccheck): hand case, C1 (fused
+single launch and, with ALP_NO_FUSED, K1 + K2 + K3), a two-LLM slice of the C3 grid (K = 512:
+b-chunked masked tables), a target batch, budget queries, a sharded search on a caller stream
+with a device finalize, injected terms, and (SANITIZE_C4=1) the full C4 headline search."""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import json  # noqa: E402
 
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
 import paper_2604_15186_b200 as P  # noqa: E402
 from workloads import generate  # noqa: E402
 
-for name in ("hand", "C1"):
-    d = generate.load(name)
-    r = P.Alp.from_instance(d).search(d["targets"][0], d["budget_units"])
-    print(name, r.index, r.feasible_count)
+for fused in (True, False):
+    if not fused:
+        os.environ["ALP_NO_FUSED"] = "1"
+    for name in ("hand", "C1"):
+        d = generate.load(name)
+        r = P.Alp.from_instance(d).search(d["targets"][0], d["budget_units"])
+        print(name, "fused" if fused else "classic", r.index, r.feasible_count)
+    os.environ.pop("ALP_NO_FUSED", None)
 d = json.loads(json.dumps(generate.load("C3")))
 for k in ("n", "p", "profiles"):
     d[k] = d[k][:2]
@@ -20,3 +29,24 @@ d["M"] = 2
 alp = P.Alp.from_instance(d)
 print("C3x2", alp.search(d["targets"][0], 128).index, alp.search_batch([d["targets"][0], 1.0, 3.0], 64)[0].index)
 print("queries", [r.index for r in alp.search_queries([d["targets"][0]] * 3, [0, 40, 128])])
+# shard path on a caller stream: 3 shards, torch-side reduction, device finalize (PDL K3)
+d = generate.load("C1")
+alp = P.Alp.from_instance(d)
+B, lam = d["budget_units"], [d["targets"][0]]
+st = torch.cuda.Stream()
+keys = torch.empty((3, 1), dtype=torch.int64, device="cuda")
+cnts = torch.empty((3, 1), dtype=torch.int64, device="cuda")
+for rank in range(3):
+    lo, hi = alp.shard_range(B, rank, 3)
+    alp.search_shard(lam, B, lo, hi, keys[rank].data_ptr(), cnts[rank].data_ptr(), st.cuda_stream)
+st.synchronize()
+k = keys.min(dim=0).values.contiguous()
+c = cnts.sum(dim=0).contiguous()
+print("shards", alp.finalize(lam, B, k.data_ptr(), c.data_ptr())[0].index)
+tau = (np.arange(24, dtype=np.float32).reshape(3, 8) % 5 + 1) / 8
+u = (np.arange(24, dtype=np.int32).reshape(3, 8) % 3)
+print("terms", P.Alp.from_terms(tau, u).search(1.0, 4).index)
+if os.environ.get("SANITIZE_C4"):
+    d = generate.load("C4")
+    r = P.Alp.from_instance(d).search(d["targets"][0], d["budget_units"])
+    print("C4", r.index, r.feasible_count)
