@@ -414,7 +414,7 @@ alp_status make_plan(alp_s *h) {
   // smem byte offsets of each row's sort-group terms (tau of LLM g0+j lives at ((g0+j)*K + d)*4;
   // slot g1*K holds 0.0f for unused digits, slot g1*K+1 holds +inf for padded rows)
   const uint32_t zero_off = (uint32_t)(h->g1 * K) * 4u, inf_off = zero_off + 4u;
-  h->tile_off.assign(h->tile_e.size() * 2, 0u);
+  h->tile_off.assign(h->tile_e.size() * 4, 0u);
   for (size_t i = 0; i < h->tile_e.size(); ++i) {
     uint32_t off[4] = {zero_off, zero_off, zero_off, zero_off};
     if (h->tile_e[i] == kDummy) {
@@ -426,8 +426,7 @@ alp_status make_plan(alp_s *h) {
         rem /= (uint32_t)K;
       }
     }
-    h->tile_off[2 * i] = off[0] | (off[1] << 16);
-    h->tile_off[2 * i + 1] = off[2] | (off[3] << 16);
+    for (int j = 0; j < 4; ++j) h->tile_off[4 * i + j] = off[j];
   }
   // b columns sorted by units (stable): the feasible set for a remaining budget is a prefix.
   h->bperm.resize(K);

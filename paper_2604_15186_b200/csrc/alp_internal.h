@@ -116,7 +116,7 @@ struct SearchArgs {
   const int *u;          // [M][K]
   const int *tile_s;     // [n_tiles] units of the lane tile's sort-group options
   const uint32_t *tile_e;// [n_tiles][T] canonical sort-group entry index (kDummy = padding)
-  const uint32_t *tile_off;// [n_tiles][T][2] smem byte offsets of the row's sort-group terms (4 x 16 bit)
+  const uint32_t *tile_off;// [n_tiles][T][4] smem byte offsets of the row's sort-group terms
   int rows_per_lane;     // T (8 or 16)
   int min_blocks;        // launch-bounds variant for T = 8 (3 or 4 blocks/SM)
   int t_begin, t_end, c_begin, c_end;  // phases (target, b-chunk) evaluated by this launch

@@ -241,19 +241,26 @@ __device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], floa
 template <int T>
 __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[T], uint32_t tile, uint32_t chunk,
                                           uint32_t q0, float &best, uint32_t &best_seg) {
-  bool any = false;
+  // tile minimum first (FMNMX3 tree); the rows' canonical indices are read only when it can
+  // improve the best (value, segment)
+  float m = acc[0];
 #pragma unroll
-  for (int i = 0; i < T; ++i) any |= (acc[i] <= best) && (acc[i] < finf());
-  if (!any) return;
+  for (int i = 1; i + 1 < T; i += 2) m = min3(m, acc[i], acc[i + 1]);
+  if (T % 2 == 0) m = fminf(m, acc[T - 1]);
+  if (!(m <= best) || !(m < finf())) return;
+  uint32_t bs = 0xffffffffu;
+#pragma unroll
   for (int i = 0; i < T; ++i) {
-    if (acc[i] <= best && acc[i] < finf()) {
+    if (acc[i] == m) {
       const uint32_t ec = __ldg(P.tile_e + (size_t)tile * T + i);  // canonical within-group index
-      const uint32_t seg = (chunk * P.L + ec) * P.nQ + q0;
-      if (acc[i] < best || seg < best_seg) {
-        best = acc[i];
-        best_seg = seg;
-      }
+      bs = min(bs, (chunk * P.L + ec) * P.nQ + q0);
     }
+  }
+  if (m < best) {
+    best = m;
+    best_seg = bs;
+  } else if (bs < best_seg) {  // m == best: lowest segment wins
+    best_seg = bs;
   }
 }
 
@@ -319,25 +326,21 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
       const uint32_t tile = grp * kWarpTiles + lane;
       const int stile = __ldg(P.tile_s + tile);
-      // per row: 4 smem byte offsets (16 bits each) of the sort-group terms, in LLM order;
-      // unused digits point at 0.0f, padded rows at +inf
-      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * (T / 2);
+      // per row: 4 smem byte offsets of the sort-group terms, in LLM order; unused digits point
+      // at 0.0f, padded rows at +inf
+      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
       nfin = 0;
 #pragma unroll
-      for (int v = 0; v < T / 2; ++v) {
+      for (int v = 0; v < T; ++v) {
         const uint4 o = __ldg(op + v);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t w0 = h ? o.z : o.x, w1 = h ? o.w : o.y;
-          float qv = Pfx;
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w0 & 0xffffu)));
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w0 >> 16)));
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w1 & 0xffffu)));
-          qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + (w1 >> 16)));
-          Qr[2 * v + h] = qv;
-          nfin += (qv < finf()) ? 1u : 0u;
-          acc[2 * v + h] = finf();
-        }
+        float qv = Pfx;
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
+        Qr[v] = qv;
+        nfin += (qv < finf()) ? 1u : 0u;
+        acc[v] = finf();
       }
       r_tile = R - Upfx - stile;
       q0 = q;
