@@ -25,6 +25,7 @@ using namespace alp;
 namespace {
 
 thread_local std::string g_err = "no error";
+constexpr size_t kPinnedStageMax = 256 * 1024;  // larger arena uploads skip the pinned staging buffer
 constexpr size_t kArenaWork = 64;  // work counters kept in the handle arena (phases of one search)
 
 // Small pinned host buffer per host thread (allocated once, shared by all handles the thread uses)
@@ -119,7 +120,12 @@ struct Arena {
     // stream-ordered allocation from the device's default memory pool (kept warm across handles)
     cudaError_t e = cudaMallocAsync(base, total ? total : 1, st);
     if (e != cudaSuccess) return e;
-    if (copied) {
+    if (copied > kPinnedStageMax) {
+      // large, rare uploads (static plans): a pageable copy beats growing the pinned staging
+      // buffer (page-locking megabytes costs more than the copy); the call returns once the
+      // driver has staged the source, the DMA is ordered on st
+      e = cudaMemcpyAsync(*base, host.data(), copied, cudaMemcpyHostToDevice, st);
+    } else if (copied) {
       std::lock_guard<std::mutex> lock(mu);
       if (pinned_bytes < copied) {
         if (pinned) cudaFreeHost(pinned);
