@@ -179,11 +179,6 @@ FastDiv make_fastdiv(uint32_t d) {
   return f;
 }
 
-int ceil_log2(int k) {
-  int b = 0;
-  while ((1 << b) < k) ++b;
-  return b ? b : 1;
-}
 
 }  // namespace
 
@@ -247,7 +242,7 @@ struct alp_s {
   std::vector<double> term_fixed, b_fixed;
   uint64_t N = 0;
   // static plan
-  int a_llm = -1, b_llm = 0, Ka = 1, Kb = 1, g0 = 0, g1 = 0, ng = 0, dig_bits = 1;
+  int a_llm = -1, b_llm = 0, Ka = 1, Kb = 1, g0 = 0, g1 = 0, ng = 0;
   uint32_t L = 1, n_chunks = 1, n_groups = 1, nQ = 1, A = 1;
   uint32_t pw[ALP_MAX_M] = {0};
   std::vector<int> tile_s, bperm, bu, dv, dcnt;
@@ -358,10 +353,9 @@ alp_status make_plan(alp_s *h) {
   h->Kb = K;
   h->Ka = h->a_llm >= 0 ? K : 1;
   h->g1 = h->a_llm >= 0 ? h->a_llm : 0;
-  h->dig_bits = ceil_log2(K);
   int ng = 0;
   uint64_t L = 1;
-  while (ng < std::min(4, h->g1) && L * (uint64_t)K <= (1ull << 18) && (ng + 1) * h->dig_bits <= 31) {
+  while (ng < std::min(4, h->g1) && L * (uint64_t)K <= (1ull << 18)) {
     ++ng;
     L *= (uint64_t)K;
   }
@@ -475,7 +469,7 @@ alp_status make_plan(alp_s *h) {
 // Snapshot of a built plan (everything make_plan produces that the searches need).
 struct PlanSnap {
   uint64_t N;
-  int a_llm, b_llm, Ka, Kb, g0, g1, ng, dig_bits, umax_a, umax_b;
+  int a_llm, b_llm, Ka, Kb, g0, g1, ng, umax_a, umax_b;
   uint32_t L, n_chunks, n_groups, nQ, A;
   uint32_t pw[ALP_MAX_M];
   long long umax_total;
@@ -524,7 +518,7 @@ alp_status get_plan(alp_s *h) {
     CU(A.commit(&P->dev->mem, h->h2d, h->stream));
     CU(cudaStreamSynchronize(h->stream));  // shared by handles on other streams (cold path only)
     P->N = h->N; P->a_llm = h->a_llm; P->b_llm = h->b_llm; P->Ka = h->Ka; P->Kb = h->Kb; P->g0 = h->g0;
-    P->g1 = h->g1; P->ng = h->ng; P->dig_bits = h->dig_bits; P->umax_a = h->umax_a; P->umax_b = h->umax_b;
+    P->g1 = h->g1; P->ng = h->ng; P->umax_a = h->umax_a; P->umax_b = h->umax_b;
     P->L = h->L; P->n_chunks = h->n_chunks; P->n_groups = h->n_groups; P->nQ = h->nQ; P->A = h->A;
     memcpy(P->pw, h->pw, sizeof(P->pw));
     P->umax_total = h->umax_total;
@@ -533,7 +527,7 @@ alp_status get_plan(alp_s *h) {
     h->tile_s.clear(); h->tile_e.clear(); h->tile_off.clear(); h->bperm.clear(); h->bu.clear(); h->dcnt.clear();
   }
   h->N = P->N; h->a_llm = P->a_llm; h->b_llm = P->b_llm; h->Ka = P->Ka; h->Kb = P->Kb; h->g0 = P->g0;
-  h->g1 = P->g1; h->ng = P->ng; h->dig_bits = P->dig_bits; h->umax_a = P->umax_a; h->umax_b = P->umax_b;
+  h->g1 = P->g1; h->ng = P->ng; h->umax_a = P->umax_a; h->umax_b = P->umax_b;
   h->L = P->L; h->n_chunks = P->n_chunks; h->n_groups = P->n_groups; h->nQ = P->nQ; h->A = P->A;
   memcpy(h->pw, P->pw, sizeof(h->pw));
   h->umax_total = P->umax_total;
@@ -666,7 +660,7 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   SearchArgs &a = g.a;
   memset(&a, 0, sizeof(a));
   a.M = h->M; a.K = h->K; a.g0 = h->g0; a.g1 = h->g1; a.a_llm = h->a_llm; a.b_llm = h->b_llm;
-  a.Ka = h->Ka; a.Kb = h->Kb; a.ng = h->ng; a.dig_bits = h->dig_bits; a.L = h->L; a.n_chunks = h->n_chunks;
+  a.Ka = h->Ka; a.Kb = h->Kb; a.ng = h->ng; a.L = h->L; a.n_chunks = h->n_chunks;
   a.n_groups = h->n_groups; a.nQ = h->nQ; a.A = h->A; a.item_lo = lo; a.item_hi = hi;
   a.fd_nQ = make_fastdiv(h->nQ);
   a.fd_ng = make_fastdiv(h->n_groups);

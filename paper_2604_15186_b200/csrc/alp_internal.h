@@ -95,7 +95,7 @@ struct SearchArgs {
   int g0, g1;            // prefix LLMs [0,g0), sort-group LLMs [g0,g1)
   int a_llm, b_llm;      // a = LLM M-2 (or -1: virtual single zero option), b = LLM M-1
   int Ka, Kb;
-  int ng, dig_bits;      // sort group size, bits per packed digit
+  int ng;                // sort group size (LLMs)
   uint32_t L;            // sort-list length K^ng
   uint32_t n_chunks;     // K^g0
   uint32_t n_groups;     // warp groups of 32 lane tiles
