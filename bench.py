@@ -114,9 +114,10 @@ def oracle_rate(d, seconds=12.0, threads=None):
     dt = time.perf_counter() - t0
     n2 = int(min(I.N, max(n, n * seconds / max(dt, 1e-3))))
     t0 = time.perf_counter()
-    oracle.search(I, lam, I.budget, lo=0, hi=n2, threads=threads)
+    o = oracle.search(I, lam, I.budget, lo=0, hi=n2, threads=threads)
     dt = time.perf_counter() - t0
-    return n2 / dt, threads, f"canonical indices [0, {n2}) of {d['name']} (N={I.N}), {threads} threads", dt
+    full = o if n2 == I.N else None  # the whole space: the oracle's answer for a parity check
+    return n2 / dt, threads, f"canonical indices [0, {n2}) of {d['name']} (N={I.N}), {threads} threads", dt, full
 
 
 def run_reference(args):
@@ -309,8 +310,13 @@ def run_ours(args):
             "clocks": cs,
         }
         if world == 1 and not args.no_cpu_baseline:
-            v, cores, sample, _dt = oracle_rate(d, seconds=args.cpu_seconds)
+            v, cores, sample, _dt, full = oracle_rate(d, seconds=args.cpu_seconds)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+            if full is not None and nt == 1:
+                # the sample was the whole space: the timed GPU result vs the oracle's, bit for bit
+                line["cpu_baseline"]["parity"] = bool(
+                    full.found == res.found and full.count == res.feasible_count
+                    and (not full.found or (full.index == res.index and full.latency_key == res.latency_key)))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -427,3 +427,17 @@ def test_cross_stream_calls_are_ordered(P):
         assert (int(keys[0]), int(counts[0])) == (ref_key, ref_cnt)
         assert (r.index, r.feasible_count, r.latency_key) == (ref_half.index, ref_half.feasible_count,
                                                               ref_half.latency_key)
+
+
+@pytest.mark.parametrize("rows", [8, 16])
+@pytest.mark.parametrize("name", ["hand", "C1", "C2"])
+def test_rows_per_lane_variants_agree(P, name, rows, monkeypatch):
+    """The tuning variants (8 / 16 rows per lane; the default is 12) give identical results."""
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    lam = d["targets"][0]
+    ref = P.Alp.from_instance(d).search(lam, I.budget)
+    monkeypatch.setenv("ALP_ROWS_PER_LANE", str(rows))
+    r = P.Alp.from_instance(d).search(lam, I.budget)
+    assert (r.found, r.index, r.feasible_count, r.latency_key) == (ref.found, ref.index, ref.feasible_count,
+                                                                    ref.latency_key)
