@@ -1,7 +1,10 @@
 // Host side of the C ABI declared in include/alp.h: validation, the static search plan (sort
 // list, u-sorted b columns), per-search launch geometry, and the kernel launches.  All ALP
-// arithmetic (option terms, objective sums, mins, counts, FP64 winner prediction) runs in the
-// kernels of alp_kernels.cu; this file only moves integers and pointers.
+// arithmetic of the search path (option terms, objective sums, mins, counts, FP64 winner
+// prediction) runs in the kernels (alp_kernels.cu, alp_search.cuh with alp_terms.cuh and
+// alp_finalize.cuh); for the search this file only moves integers and pointers.  The two steps
+// around the path, alp_workflow_stats (before alp_build) and alp_place (after the search), are
+// small host computations here.
 #include <cuda_runtime.h>
 
 #include <algorithm>
