@@ -1,4 +1,7 @@
-for i in 1 2; do for nq in 0 2 3; do
-  ALP_NQ=$nq timeout 300 python bench.py --workload C4 --steps 100 --warmup 5 --e2e-steps 1 --no-cpu-baseline > gpurun_out/sw.json 2>gpurun_out/sw.err
-  python -c "import json; d=json.load(open('gpurun_out/sw.json')); print('nQ=$nq', 'k', round(d['roofline']['kernel_ms'],4), 'step', round(d['ms_per_step'],4), d['result']['index'], d['result']['feasible_count'])"
-done; done
+for cfg in "0 0" "3 0" "3 1" "2 1" "0 0" "3 1"; do
+  set -- $cfg
+  if [ $2 = 1 ]; then export ALP_ALIGN_GRABS=1; else unset ALP_ALIGN_GRABS; fi
+  echo "nQ=$1 align=$2 $(ALP_NQ=$1 python tools/shard_timing.py C4 | python -c "
+import sys, json
+print(' '.join('w%d:%.4f' % (d['world'], d['kernel_ms']) for d in map(json.loads, sys.stdin)))")"
+done
