@@ -15,39 +15,63 @@ namespace alp {
 // finish (ticket) assembles the result and resets the target's scratch.  Called by every thread
 // of a block (K3, or the last block of the fused search).
 __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long long key, unsigned long long count,
-                                       int part, int nparts) {
+                                       int part, int nparts, const float *tau_s = nullptr) {
   const FinalizeExtra &F = P.fin;
-  __shared__ unsigned long long s_best;
   const int K = P.K;
-  const float *tau_t = P.tau + (size_t)t * P.M * K;
+  // option terms of target t: the caller's shared-memory copy (fused kernel) or the global table
+  const float *tau_g = P.tau + (size_t)t * P.M * K;
+  auto tau = [&](int i) { return tau_s ? tau_s[i] : __ldcg(tau_g + i); };
+  __shared__ unsigned long long s_best;
+  __shared__ int s_k[ALP_MAX_M], s_u[ALP_MAX_M], s_grid[3][ALP_MAX_M];
+  __shared__ float s_tq[ALP_MAX_M];
+  __shared__ double s_term[ALP_MAX_M], s_bterm[ALP_MAX_M];
+  __shared__ float s_Q;
+  __shared__ int s_U;
+  __shared__ alp_result s_res;
   const uint32_t seg = (uint32_t)(key & 0xffffffffull);
   const float val = __uint_as_float((uint32_t)(key >> 32));
   const bool found = key != kKeyNone && val < __int_as_float(0x7f800000);
   uint32_t q = 0, chunk = 0, e = 0;
-  float Qrow = 0.f;
-  int Urow = 0;
   if (found) {
     q = seg % P.nQ;
     const uint32_t row = seg / P.nQ;
     chunk = row / P.L;
     e = row % P.L;
-    // canonical partial sum over LLMs 0..g1-1 (digits of chunk then e, most significant first)
-    int kd[ALP_MAX_M];
-    uint32_t rem = chunk;
-    for (int m = P.g0 - 1; m >= 0; --m) { kd[m] = (int)(rem % (uint32_t)K); rem /= (uint32_t)K; }
-    rem = e;
-    for (int j = P.ng - 1; j >= 0; --j) { kd[P.g0 + j] = (int)(rem % (uint32_t)K); rem /= (uint32_t)K; }
-    for (int m = 0; m < P.g1; ++m) {
-      Qrow = __fadd_rn(Qrow, __ldcg(tau_t + m * K + kd[m]));
-      Urow += P.u[m * K + kd[m]];
+    // digits of the row's LLMs 0..g1-1 (chunk digits, then sort-group digits; LLM 0 most
+    // significant), one thread per LLM, with their terms and units
+    const int m = threadIdx.x;
+    if (m < P.g1) {
+      uint32_t d;
+      if (m < P.g0) {
+        d = (chunk / P.pw[m]) % (uint32_t)K;
+      } else {
+        uint32_t pw = 1;
+        for (int j = m - P.g0 + 1; j < P.ng; ++j) pw *= (uint32_t)K;
+        d = (e / pw) % (uint32_t)K;
+      }
+      s_k[m] = (int)d;
+      s_tq[m] = tau(m * K + (int)d);
+      s_u[m] = P.u[m * K + (int)d];
     }
   }
-  if (threadIdx.x == 0) {
-    s_best = ~0ull;
+  if (threadIdx.x == 0) s_best = ~0ull;
+  __syncthreads();
+  if (found && threadIdx.x == 0) {
+    // canonical partial sum over LLMs 0..g1-1: ((0 + tau_0) + tau_1) + ...
+    float Q = 0.f;
+    int U = 0;
+    for (int m = 0; m < P.g1; ++m) {
+      Q = __fadd_rn(Q, s_tq[m]);
+      U += s_u[m];
+    }
+    s_Q = Q;
+    s_U = U;
   }
   __syncthreads();
   if (found) {
     // the segment starts at a-range q and runs to the end of the row (see fold_rows)
+    const float Qrow = s_Q;
+    const int Urow = s_U;
     const int a0 = (int)(q * P.A), a1 = P.Ka;
     const unsigned long long n = (unsigned long long)(a1 - a0) * P.Kb;
     unsigned long long mine = ~0ull;
@@ -58,10 +82,10 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
       float ta = 0.f;
       int ua = 0;
       if (P.a_llm >= 0) {
-        ta = __ldcg(tau_t + P.a_llm * K + a);
+        ta = tau(P.a_llm * K + a);
         ua = P.u[P.a_llm * K + a];
       }
-      const float v = __fadd_rn(__fadd_rn(Qrow, ta), __ldcg(tau_t + P.b_llm * K + b));
+      const float v = __fadd_rn(__fadd_rn(Qrow, ta), tau(P.b_llm * K + b));
       const int units = Urow + ua + P.u[P.b_llm * K + b];
       if (v == val && units <= qbudget(P, t)) {
         mine = li;
@@ -89,24 +113,10 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
     }
     __syncthreads();
   }
-  // winner digits, then the per-LLM FP64 terms gathered in parallel (one thread per LLM)
-  __shared__ int s_k[ALP_MAX_M];
-  __shared__ double s_term[ALP_MAX_M], s_bterm[ALP_MAX_M];
-  __shared__ int s_u[ALP_MAX_M], s_grid[3][ALP_MAX_M];
+  // the winner's a and b digits, then its per-LLM FP64 terms gathered in parallel (one thread per LLM)
   const bool win = found && s_best != ~0ull;
-  if (threadIdx.x == 0 && win) {
-    const int a0 = (int)(q * P.A);
-    const int a = a0 + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
-    uint32_t rem = chunk;
-    for (int m = P.g0 - 1; m >= 0; --m) {
-      s_k[m] = (int)(rem % (uint32_t)K);
-      rem /= (uint32_t)K;
-    }
-    rem = e;
-    for (int j = P.ng - 1; j >= 0; --j) {
-      s_k[P.g0 + j] = (int)(rem % (uint32_t)K);
-      rem /= (uint32_t)K;
-    }
+  if (win && threadIdx.x == 0) {
+    const int a = (int)(q * P.A) + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
     if (P.a_llm >= 0) s_k[P.a_llm] = a;
     s_k[P.b_llm] = b;
   }
@@ -124,40 +134,45 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-  alp_result r;
-  memset(&r, 0, sizeof(r));
-  r.M = P.M;
-  r.feasible_count = count;
-  r.candidates = F.N;
-  r.index = ~0ull;
-  r.latency_key = __int_as_float(0x7f800000);
-  if (win) {
-    unsigned long long idx = 0;
-    double L = 0.0, Tw = CUDART_INF;
-    long long U = 0;
-    for (int m = 0; m < P.M; ++m) {
-      idx = idx * (unsigned long long)K + (unsigned long long)s_k[m];
-      L = (m == 0) ? s_term[m] : __dadd_rn(L, s_term[m]);  // Eq. 1 in canonical order (FP64)
-      Tw = s_bterm[m] < Tw ? s_bterm[m] : Tw;               // Eq. 2
-      U += s_u[m];
-      if (F.S) {
-        r.share_units[m] = s_grid[0][m];
-        r.tp[m] = s_grid[1][m];
-        r.replicas[m] = s_grid[2][m];
+    alp_result &r = s_res;
+    memset(&r, 0, sizeof(r));
+    r.M = P.M;
+    r.feasible_count = count;
+    r.candidates = F.N;
+    r.index = ~0ull;
+    r.latency_key = __int_as_float(0x7f800000);
+    if (win) {
+      unsigned long long idx = 0;
+      double L = 0.0, Tw = CUDART_INF;
+      long long U = 0;
+      for (int m = 0; m < P.M; ++m) {
+        idx = idx * (unsigned long long)K + (unsigned long long)s_k[m];
+        L = (m == 0) ? s_term[m] : __dadd_rn(L, s_term[m]);  // Eq. 1 in canonical order (FP64)
+        Tw = s_bterm[m] < Tw ? s_bterm[m] : Tw;               // Eq. 2
+        U += s_u[m];
+        if (F.S) {
+          r.share_units[m] = s_grid[0][m];
+          r.tp[m] = s_grid[1][m];
+          r.replicas[m] = s_grid[2][m];
+        }
       }
+      r.found = 1;
+      r.index = idx;
+      r.latency_key = val;
+      r.latency = L;
+      r.throughput = Tw;
+      r.units = U;
+    } else {
+      r.latency = CUDART_INF;
+      r.throughput = 0.0;
     }
-    r.found = 1;
-    r.index = idx;
-    r.latency_key = val;
-    r.latency = L;
-    r.throughput = Tw;
-    r.units = U;
-  } else {
-    r.latency = CUDART_INF;
-    r.throughput = 0.0;
   }
-  F.out[t] = r;
-  }
+  __syncthreads();
+  // one coalesced copy of the result (device memory, or mapped host memory for the fused search)
+  static_assert(sizeof(alp_result) % 4 == 0, "alp_result is copied as 32-bit words");
+  const uint32_t *src = reinterpret_cast<const uint32_t *>(&s_res);
+  uint32_t *dst = reinterpret_cast<uint32_t *>(F.out + t);
+  for (int i = threadIdx.x; i < (int)(sizeof(alp_result) / 4); i += blockDim.x) dst[i] = src[i];
   __syncthreads();  // shared scratch reused by the next target
 }
 

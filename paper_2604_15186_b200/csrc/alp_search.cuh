@@ -407,7 +407,7 @@ __device__ inline void fused_terms(const SearchArgs &P, const Smem &s, int t, bo
 
 // Fused epilogue: the last block to finish writes the reduced (key, count) of every target, resets
 // the scratch to its rest state and (fz.finalize) finalizes every target.
-__device__ inline void fused_epilogue(const SearchArgs &P) {
+__device__ inline void fused_epilogue(const SearchArgs &P, const float *tau_last) {
   __shared__ unsigned s_last;
   __shared__ unsigned long long s_key[kInlineTargets], s_cnt[kInlineTargets];
   __syncthreads();
@@ -430,8 +430,9 @@ __device__ inline void fused_epilogue(const SearchArgs &P) {
   for (int i = threadIdx.x; i < P.n_targets * P.n_bchunks; i += blockDim.x) P.fz.work[i] = 0ull;
   if (threadIdx.x == 0) atomicExch(P.fz.ticket, 0u);
   __syncthreads();
-  if (P.fz.finalize)
-    for (int t = 0; t < P.n_targets; ++t) finalize_target(P, t, s_key[t], s_cnt[t], 0, 1);
+  if (P.fz.finalize)  // the last target's option terms are still in shared memory (tau_last)
+    for (int t = 0; t < P.n_targets; ++t)
+      finalize_target(P, t, s_key[t], s_cnt[t], 0, 1, t + 1 == P.n_targets ? tau_last : nullptr);
 }
 
 // T = rows per lane; MB = minimum resident blocks per SM (register cap 65536 / (256 * MB)).
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, MB)
       if (n) atomicAdd(cd + t, n);
     }
   }
-  if (P.fz.on) fused_epilogue(P);
+  if (P.fz.on) fused_epilogue(P, s.opt);
   stamp(3);
 }
 

@@ -1,7 +1,7 @@
-for cfg in "0 0" "3 0" "3 1" "2 1" "0 0" "3 1"; do
-  set -- $cfg
-  if [ $2 = 1 ]; then export ALP_ALIGN_GRABS=1; else unset ALP_ALIGN_GRABS; fi
-  echo "nQ=$1 align=$2 $(ALP_NQ=$1 python tools/shard_timing.py C4 | python -c "
-import sys, json
-print(' '.join('w%d:%.4f' % (d['world'], d['kernel_ms']) for d in map(json.loads, sys.stdin)))")"
-done
+ALP_DBG_TS=1 python - <<'PY' 2>&1 | grep "alp dbg" | tail -3
+import sys; sys.path.insert(0, '.')
+import paper_2604_15186_b200 as P
+from workloads import generate
+d = generate.load('C4'); a = P.Alp.from_instance(d)
+for i in range(10): a.search(d['targets'][0], d['budget_units'])
+PY
