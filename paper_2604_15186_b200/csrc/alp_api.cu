@@ -964,9 +964,32 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
 }
 
 // D2H of the n results (pinned staging), step-end event, sync; status from the results.
-alp_status collect_results(alp_s *h, int n, cudaStream_t st, alp_result *out) {
-  void *pin = (n * sizeof(alp_result) <= kPinHalf) ? pinned_scratch(2 * kPinHalf) : nullptr;
-  if (pin) {
+// Device pointer into this thread's mapped pinned scratch (upper half) for n results, written by
+// the finalizing kernel itself (zero-copy: no D2H copy op, whose start after a kernel costs
+// ~5-10 us); nullptr when n results do not fit or mapping is unavailable.
+alp_result *zero_copy_out(int n, alp_result **host) {
+  *host = nullptr;
+  if (n * sizeof(alp_result) > kPinHalf) return nullptr;
+  auto *pin = static_cast<unsigned char *>(pinned_scratch(2 * kPinHalf));
+  if (!pin) return nullptr;
+  alp_result *hres = reinterpret_cast<alp_result *>(pin + kPinHalf), *dres = nullptr;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&dres), hres, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  *host = hres;
+  return dres;
+}
+
+// The n results on the host (zero-copy results already written by the kernel into host_zc, else a
+// D2H copy through pinned staging), step-end event, sync; status from the results.
+alp_status collect_results(alp_s *h, int n, cudaStream_t st, alp_result *out, const alp_result *host_zc = nullptr) {
+  void *pin = (!host_zc && n * sizeof(alp_result) <= kPinHalf) ? pinned_scratch(2 * kPinHalf) : nullptr;
+  if (host_zc) {
+    CU(cudaEventRecord(h->evs1, st));
+    CU(cudaStreamSynchronize(st));
+    memcpy(out, host_zc, n * sizeof(alp_result));
+  } else if (pin) {
     pin = static_cast<unsigned char *>(pin) + kPinHalf;
     CU(cudaMemcpyAsync(pin, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(h->evs1, st));
@@ -1014,9 +1037,11 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
   fill_finalize(h, g.a);
   g.a.fin.keys = keys;
   g.a.fin.counts = counts;
+  alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);
+  if (zc) g.a.fin.out = zc;
   CU(launch_finalize(g.a, st));
   h->last_launches += 1;
-  return collect_results(h, n, st, out);
+  return collect_results(h, n, st, out, hzc);
 }
 
 }  // namespace
@@ -1270,26 +1295,11 @@ static alp_status search_queries(alp_t *h, const double *targets, const int64_t 
   if (s != ALP_OK) return s;
   const uint64_t items = alp_num_items(h, budget_units);
   if (use_fused(h, n, budgets)) {  // one launch: terms + search + finalize
-    // the kernel's last block stores the results into mapped pinned memory (no D2H copy)
-    auto *pin = static_cast<unsigned char *>(pinned_scratch(2 * kPinHalf));
-    alp_result *hres = pin ? reinterpret_cast<alp_result *>(pin + kPinHalf) : nullptr, *dres = nullptr;
-    if (hres && cudaHostGetDevicePointer(reinterpret_cast<void **>(&dres), hres, 0) != cudaSuccess) {
-      cudaGetLastError();
-      dres = nullptr;
-    }
+    alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);  // the last block stores the results
     s = search_shard_impl(h, targets, nullptr, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts, true,
-                          dres);
+                          zc);
     if (s != ALP_OK) return s;
-    if (!dres) return collect_results(h, n, h->stream, out);
-    CU(cudaEventRecord(h->evs1, h->stream));
-    CU(cudaStreamSynchronize(h->stream));
-    memcpy(out, hres, n * sizeof(alp_result));
-    CU(cudaEventElapsedTime(&h->last_step_ms, h->evs0, h->evs1));
-    CU(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
-    h->ev_pending = false;
-    int any = 0;
-    for (int i = 0; i < n; ++i) any |= out[i].found;
-    return any ? ALP_OK : ALP_EINFEASIBLE;
+    return collect_results(h, n, h->stream, out, hzc);
   }
   s = search_shard_impl(h, targets, budgets, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts);
   if (s != ALP_OK) return s;
