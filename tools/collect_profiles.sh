@@ -1,0 +1,37 @@
+#!/bin/bash
+# Copy the outputs of tools/run_final.sh (gpurun_out/) into profiles/ under the round prefix.
+set -e
+R=${1:-r01}
+G=gpurun_out
+cp $G/bench_C4.json profiles/${R}_bench_C4.json
+cp $G/bench_C3.json profiles/${R}_bench_C3.json
+cp $G/bench_C5.json profiles/${R}_bench_C5.json
+cp $G/bench_reference.json profiles/${R}_bench_reference.json
+cp $G/bench_2rank_gloo.json profiles/${R}_bench_C4_2rank_gloo_1gpu.json
+cp $G/launches.csv profiles/${R}_C4_launches.csv
+ncu -i $G/prof_search.ncu-rep --page raw --csv > profiles/${R}_C4_k_search_ncu_raw.csv 2>/dev/null
+ncu -i $G/prof_search_C3.ncu-rep --page raw --csv > profiles/${R}_C3_k_search_ncu_raw.csv 2>/dev/null
+ncu -i $G/prof_search.ncu-rep --page source --csv --print-source sass > $G/sass_C4.csv 2>/dev/null
+python tools/sass_blocks.py $G/sass_C4.csv --candidates 11019960576 --top 30 > profiles/${R}_C4_k_search_sass_blocks.txt
+(echo "# fused single-GPU search (alp_search): one kernel, zero-copy result"; cat $G/timeline_C4_search.txt; echo
+ echo "# shard path (alp_search_shard + alp_finalize), world 1, no all-reduce; K3 writes the result zero-copy"
+ cat $G/timeline_C4_shard.txt) > profiles/${R}_step_timeline_C4.txt
+(echo "# per-block %globaltimer stamps of k_search (ALP_DBG_TS=1), rank-0 shard of world 1/2/4/8/8; us from the first block start"
+ cat $G/block_timeline_C4.txt) > profiles/${R}_block_timeline_C4.txt
+cp $G/shard_timing.jsonl profiles/${R}_shard_scaling.jsonl
+cp $G/mb_pipes5.txt profiles/${R}_microbench_pipes5.txt
+cp $G/pytest_gpu.txt profiles/${R}_pytest_gpu.txt
+python - <<PY
+import csv, json
+out = {"_note": "dram__bytes_read.sum + dram__bytes_write.sum of one k_search launch (ncu --set full; profiles/${R}_C4_k_search_ncu_raw.csv, ${R}_C3_k_search_ncu_raw.csv)"}
+for w in ("C4", "C3"):
+    rows = list(csv.reader(open(f"profiles/${R}_{w}_k_search_ncu_raw.csv")))
+    h, u, v = rows[0], rows[1], rows[2]
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        x = float(v[h.index(k)]); unit = u[h.index(k)]
+        tot += x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+    out[w] = int(round(tot))
+json.dump(out, open("profiles/ncu_traffic.json", "w"))
+print(out)
+PY
