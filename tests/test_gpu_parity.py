@@ -441,3 +441,18 @@ def test_rows_per_lane_variants_agree(P, name, rows, monkeypatch):
     r = P.Alp.from_instance(d).search(lam, I.budget)
     assert (r.found, r.index, r.feasible_count, r.latency_key) == (ref.found, ref.index, ref.feasible_count,
                                                                     ref.latency_key)
+
+
+@pytest.mark.parametrize("M,S,T,R,budget", [(10, [1, 2], [1], [1, 2], 14), (12, [1], [1, 2], [1, 2], 20),
+                                             (16, [1, 2], [1], [1], 22), (9, [1, 2, 4], [1], [1, 2], 17)])
+def test_many_llms_vs_bruteforce(P, M, S, T, R, budget):
+    """Many LLMs (up to ALP_MAX_M = 16): several prefix LLMs above the sort group, the prefix-chunk
+    table and multi-digit chunk decode, against the brute-force oracle over the whole space."""
+    d = generate.random_instance(900 + M, M=M, F=4, S=S, T=T, R=R, budget=budget)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (0.05, 0.3):
+        r = alp.search(lam, budget)
+        o = oracle.search(I, lam, budget, threads=8)
+        _same(r, o.found, o.latency_key, o.index, o.count, (M, lam))
+        _check_winner(P, alp, I, lam, budget, r)
