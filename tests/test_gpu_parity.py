@@ -444,7 +444,8 @@ def test_rows_per_lane_variants_agree(P, name, rows, monkeypatch):
 
 
 @pytest.mark.parametrize("M,S,T,R,budget", [(10, [1, 2], [1], [1, 2], 14), (12, [1], [1, 2], [1, 2], 20),
-                                             (16, [1, 2], [1], [1], 22), (9, [1, 2, 4], [1], [1, 2], 17)])
+                                             (16, [1, 2], [1], [1], 22), (9, [1, 2, 4], [1], [1, 2], 17),
+                                             (16, [1], [1], [1, 2, 3], 30)])
 def test_many_llms_vs_bruteforce(P, M, S, T, R, budget):
     """Many LLMs (up to ALP_MAX_M = 16): several prefix LLMs above the sort group, the prefix-chunk
     table and multi-digit chunk decode, against the brute-force oracle over the whole space."""
@@ -456,3 +457,19 @@ def test_many_llms_vs_bruteforce(P, M, S, T, R, budget):
         o = oracle.search(I, lam, budget, threads=8)
         _same(r, o.found, o.latency_key, o.index, o.count, (M, lam))
         _check_winner(P, alp, I, lam, budget, r)
+
+
+def test_max_options_per_llm_vs_bruteforce(P):
+    """K = 1024 options per LLM (ALP_MAX_K): a one-LLM sort group, b rows split into chunks."""
+    S = [1, 2, 3, 4]
+    T = [1, 2, 4, 8]
+    R = list(range(1, 65))
+    d = generate.random_instance(4242, M=3, F=4, S=S, T=T, R=R, budget=600)
+    I = oracle.from_json(d)
+    assert I.K == 1024
+    alp = P.Alp.from_instance(d)
+    for lam in (0.05, 0.5):
+        r = alp.search(lam, 600)
+        o = oracle.search(I, lam, 600, threads=16)
+        _same(r, o.found, o.latency_key, o.index, o.count, lam)
+        _check_winner(P, alp, I, lam, 600, r)
