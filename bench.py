@@ -3,9 +3,9 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
 
-A step = one full search of the workload: option-term kernel, exhaustive evaluation of all N
-candidates (sharded over ranks), NCCL all-reduce of the (key, count) pairs, device finalize and
-the D2H of the result.  value = candidates evaluated per second for the whole job (max over
+A step = one full search of the workload: at N=1 one fused kernel (option terms, exhaustive
+evaluation of all N candidates, finalize; result stored zero-copy); at N>1 the sharded search
+kernel on every rank, ONE NCCL all-gather of the 16-byte (key, count) pairs, device finalize.  value = candidates evaluated per second for the whole job (max over
 ranks of the device time); inputs (profile tables) are resident in HBM before the timed region.
 e2e = the same metric through the C ABI from HOST buffers: alp_build (H2D of the profiles and the
 plan) + search + D2H of the result + alp_destroy, per step.
@@ -153,7 +153,7 @@ def _config(d, N, world):
     return {"workload": f"{d['name']}: {d['description']}", "candidates": N * len(d["targets"]), "M": d["M"],
             "options_per_llm": len(d["share_units"]) * len(d["tp"]) * len(d["replicas"]),
             "budget_units": d["budget_units"], "F": d["F"], "target_req_s": d["targets"][0],
-            "n_targets": len(d["targets"]), "parallelism": f"index-space shard x{world} + NCCL allreduce-min",
+            "n_targets": len(d["targets"]), "parallelism": f"index-space shard x{world} + NCCL all-gather of (key, count) pairs",
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -182,7 +182,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     import paper_2604_15186_b200 as P
-    from paper_2604_15186_b200.dist import reduce_keys
+    from paper_2604_15186_b200.dist import gather_pairs
 
     d = load_workload(args.workload)
     B = int(d["budget_units"])
@@ -192,8 +192,8 @@ def run_ours(args):
     N = alp.num_candidates
     lo, hi = alp.shard_range(B, rank, world)
     stream = torch.cuda.Stream(device=dev)
-    keys = torch.empty(nt, dtype=torch.int64, device=dev)
-    counts = torch.empty(nt, dtype=torch.int64, device=dev)
+    pairs = torch.empty(2 * nt, dtype=torch.int64, device=dev)             # this rank's (keys, counts)
+    gathered = torch.empty(world * 2 * nt, dtype=torch.int64, device=dev)  # every rank's pairs
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def run_step(a, lo_, hi_):
@@ -203,9 +203,9 @@ def run_ours(args):
         if world == 1:
             return a.search_batch(targets, B)[-1]
         with torch.cuda.stream(stream):
-            a.search_shard(targets, B, lo_, hi_, keys.data_ptr(), counts.data_ptr(), stream.cuda_stream)
-            reduce_keys(keys, counts)
-            return a.finalize(targets, B, keys.data_ptr(), counts.data_ptr(), stream.cuda_stream)[-1]
+            a.search_shard(targets, B, lo_, hi_, pairs.data_ptr(), pairs.data_ptr() + 8 * nt, stream.cuda_stream)
+            w = gather_pairs(pairs, gathered)  # ONE all-gather of the 16-byte (key, count) pairs
+            return a.finalize_gathered(targets, B, gathered.data_ptr(), w, stream.cuda_stream)[-1]
 
     def step():
         return run_step(alp, lo, hi)

@@ -179,6 +179,12 @@ alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t 
  * of the winner) and copy n results to the host (synchronises `stream`). */
 alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
                         const int64_t *d_keys, const int64_t *d_counts, void *stream, alp_result *out);
+/* Same, from the per-rank pairs gathered by ONE all-gather instead of two all-reduces: every rank
+ * searches with d_keys = buf, d_counts = buf + n (a contiguous int64[2n] buffer), all-gathers buf
+ * into d_gathered = int64[world][2][n], and the finalize kernel takes the MIN of the keys and the
+ * SUM of the counts itself (the result equals alp_finalize's on the all-reduced pair). */
+alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
+                                 const int64_t *d_gathered, int32_t world, void *stream, alp_result *out);
 
 /* Device time (ms) of the last search kernel launched through this handle (CUDA events on the
  * launching stream), and the number of kernels the last search/finalize launched.  Searches of at

@@ -50,10 +50,9 @@ class _Result(ctypes.Structure):
 
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
-           "alp_search_shard", "alp_finalize", "alp_last_kernel_ms", "alp_last_launches", "alp_last_step_ms",
-           "alp_last_error",
-           "alp_plan_cache_clear", "alp_search_queries", "alp_schedule_egalitarian", "alp_workflow_stats",
-           "alp_place"]
+           "alp_search_shard", "alp_finalize", "alp_finalize_gathered", "alp_last_kernel_ms", "alp_last_launches",
+           "alp_last_step_ms", "alp_last_error", "alp_plan_cache_clear", "alp_search_queries",
+           "alp_schedule_egalitarian", "alp_workflow_stats", "alp_place"]
 
 _lib = None
 
@@ -76,6 +75,7 @@ def lib():
             "alp_num_items": (u64, [vp, i64]), "alp_shard_range": (i32, [vp, i64, i32, i32, vp, vp]),
             "alp_search_shard": (i32, [vp, vp, i32, i64, u64, u64, vp, vp, vp]),
             "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp]),
+            "alp_finalize_gathered": (i32, [vp, vp, i32, i64, vp, i32, vp, vp]),
             "alp_last_kernel_ms": (ctypes.c_float, [vp]), "alp_last_launches": (i32, [vp]),
             "alp_last_step_ms": (ctypes.c_float, [vp]),
             "alp_last_error": (ctypes.c_char_p, []), "alp_plan_cache_clear": (None, []),
@@ -90,6 +90,15 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def _stream(stream_ptr: int | None):
+    """cudaStream_t for the C ABI: None -> NULL (the handle's own stream); a torch stream handle of
+    0 (the legacy default stream) -> cudaStreamLegacy, so the call is ordered with torch's default
+    stream instead of silently running on the handle's stream."""
+    if stream_ptr is None:
+        return None
+    return stream_ptr or 1  # 0x1 = cudaStreamLegacy
 
 
 def plan_cache_clear() -> None:
@@ -330,15 +339,26 @@ class Alp:
                      stream_ptr: int | None = None) -> None:
         """Async: evaluate items [lo, hi) for every target into device int64 keys/counts."""
         t = _arr(targets, np.float64)
-        _check(lib().alp_search_shard(self._h, t.ctypes.data, len(t), budget, lo, hi, stream_ptr, keys_ptr,
+        _check(lib().alp_search_shard(self._h, t.ctypes.data, len(t), budget, lo, hi, _stream(stream_ptr), keys_ptr,
                                       counts_ptr))
 
     def finalize(self, targets: Sequence[float], budget: int, keys_ptr: int, counts_ptr: int,
                  stream_ptr: int | None = None) -> list[Result]:
         t = _arr(targets, np.float64)
         out = (_Result * len(t))()
-        _check(lib().alp_finalize(self._h, t.ctypes.data, len(t), budget, keys_ptr, counts_ptr, stream_ptr, out),
+        _check(lib().alp_finalize(self._h, t.ctypes.data, len(t), budget, keys_ptr, counts_ptr, _stream(stream_ptr),
+                                  out),
                (ALP_OK, ALP_EINFEASIBLE))
+        return [Result._from(x) for x in out]
+
+    def finalize_gathered(self, targets: Sequence[float], budget: int, gathered_ptr: int, world: int,
+                          stream_ptr: int | None = None) -> list[Result]:
+        """alp_finalize_gathered: finalize from all-gathered per-rank int64[world][2][n] pairs."""
+        t = _arr(targets, np.float64)
+        out = (_Result * len(t))()
+        _check(lib().alp_finalize_gathered(self._h, t.ctypes.data, len(t), budget, gathered_ptr, world,
+                                           _stream(stream_ptr),
+                                           out), (ALP_OK, ALP_EINFEASIBLE))
         return [Result._from(x) for x in out]
 
     @property

@@ -1012,7 +1012,7 @@ alp_status collect_results(alp_s *h, int n, cudaStream_t st, alp_result *out, co
 
 alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
                          const unsigned long long *keys, const unsigned long long *counts, cudaStream_t st,
-                         alp_result *out) {
+                         alp_result *out, int world = 0) {
   if (!out) return fail(ALP_EINVAL, "out is NULL");
   CU(cudaSetDevice(h->device));
   alp_status s = use_stream(h, st);
@@ -1037,6 +1037,7 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
   fill_finalize(h, g.a);
   g.a.fin.keys = keys;
   g.a.fin.counts = counts;
+  g.a.fin.world = world;
   alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);
   if (zc) g.a.fin.out = zc;
   CU(launch_finalize(g.a, st));
@@ -1282,6 +1283,17 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
   return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
                        reinterpret_cast<const unsigned long long *>(d_counts),
                        stream ? (cudaStream_t)stream : h->stream, out);
+}
+
+alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
+                                 const int64_t *d_gathered, int32_t world, void *stream, alp_result *out) {
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (!d_gathered) return fail(ALP_EINVAL, "d_gathered is NULL");
+  if (world < 1) return fail(ALP_EINVAL, "world must be >= 1");
+  alp_status s = check_targets(targets, n);
+  if (s != ALP_OK) return s;
+  return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_gathered),
+                       nullptr, stream ? (cudaStream_t)stream : h->stream, out, world);
 }
 
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,

@@ -64,8 +64,9 @@ struct FinalizeExtra {
   const int *S, *T, *R;  // grids (for the winner's (share, tp, replicas)); S == nullptr: injected terms
   int nS, nT, nR;
   uint64_t N;
-  const unsigned long long *keys;    // [n_t] reduced keys (K3 input)
-  const unsigned long long *counts;  // [n_t] reduced counts (K3 input)
+  const unsigned long long *keys;    // [n_t] reduced keys (K3 input); world > 0: [world][2][n_t] gathered pairs
+  const unsigned long long *counts;  // [n_t] reduced counts (K3 input; unused when world > 0)
+  int world;                         // > 0: K3 reduces the gathered per-rank (keys, counts) itself
   alp_result *out;       // [n_t] device
   unsigned long long *best;  // [n_t] scratch: ~0 between calls (self-resetting)
   unsigned *done;            // [n_t] scratch: 0 between calls (self-resetting)

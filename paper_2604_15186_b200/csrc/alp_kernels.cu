@@ -95,7 +95,22 @@ int search_max_blocks_per_sm(const SearchArgs &a) {
 __global__ void k_finalize(const __grid_constant__ SearchArgs P) {
   pdl_wait();  // keys/counts/terms come from K2 (or the all-reduce after it)
   const int t = blockIdx.y;
-  finalize_target(P, t, P.fin.keys[t], P.fin.counts[t], blockIdx.x, gridDim.x);
+  unsigned long long key = 0, count = 0;
+  if (P.fin.world > 0) {
+    // per-rank (keys, counts) gathered as [world][2][n_t]: MIN of keys (lowest value, then lowest
+    // global segment), SUM of counts
+    const size_t stride = 2 * (size_t)P.n_targets;
+    key = ~0ull;
+    for (int r = 0; r < P.fin.world; ++r) {
+      const unsigned long long k = P.fin.keys[r * stride + t];
+      key = k < key ? k : key;
+      count += P.fin.keys[r * stride + P.n_targets + t];
+    }
+  } else {
+    key = P.fin.keys[t];
+    count = P.fin.counts[t];
+  }
+  finalize_target(P, t, key, count, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------ multi-workflow split (NEXT-1)

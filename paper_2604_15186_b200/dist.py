@@ -1,8 +1,10 @@
 """Multi-GPU search: the candidate work items are split into contiguous per-rank ranges
-(alp_shard_range), every rank runs the search kernel on its range, and ONE grouped all-reduce
-(MIN over int64 keys, SUM over int64 counts; every key < 2^63) combines them over NCCL /
-NVLink.  PyTorch owns the device memory, the stream and the process group; the kernels are the
-library's.  Keys carry the global segment id, so the result is independent of the split.
+(alp_shard_range), every rank runs the search kernel on its range, and the per-rank (key, count)
+pairs are combined over NCCL / NVLink: by ONE all-gather of the 16-byte pairs (the finalize
+kernel takes MIN of the keys and SUM of the counts itself, alp_finalize_gathered), or by two
+all-reduces (MIN over int64 keys, SUM over int64 counts; every key < 2^63) and alp_finalize.
+PyTorch owns the device memory, the stream and the process group; the kernels are the library's.
+Keys carry the global segment id, so the result is independent of the split.
 """
 from __future__ import annotations
 
@@ -22,16 +24,32 @@ def reduce_keys(keys: torch.Tensor, counts: torch.Tensor, group=None) -> None:
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
 
 
+def gather_pairs(pairs: torch.Tensor, gathered: torch.Tensor, group=None) -> int:
+    """One all-gather of this rank's int64[2n] (keys, counts) into int64[world][2n]; returns world.
+    Without a process group (or world size 1) the pairs are copied through."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        gathered[: pairs.numel()].copy_(pairs)
+        return 1
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, pairs, group=group)
+    else:  # gloo (CPU tests, several ranks on one GPU): list form
+        dist.all_gather(list(gathered[: world * pairs.numel()].view(world, -1).unbind(0)), pairs, group=group)
+    return world
+
+
 def search_distributed(alp: Alp, targets: Sequence[float], budget: int, group=None,
                        stream: torch.cuda.Stream | None = None) -> list[Result]:
+    """Every rank searches its shard, one all-gather exchanges the (key, count) pairs, every rank
+    finalizes (identical results on all ranks)."""
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     lo, hi = alp.shard_range(budget, rank, world)
     st = stream or torch.cuda.current_stream()
     n = len(targets)
-    keys = torch.empty(n, dtype=torch.int64, device="cuda")
-    counts = torch.empty(n, dtype=torch.int64, device="cuda")
+    pairs = torch.empty(2 * n, dtype=torch.int64, device="cuda")
+    gathered = torch.empty(world * 2 * n, dtype=torch.int64, device="cuda")
     with torch.cuda.stream(st):
-        alp.search_shard(targets, budget, lo, hi, keys.data_ptr(), counts.data_ptr(), st.cuda_stream)
-        reduce_keys(keys, counts, group)
-        return alp.finalize(targets, budget, keys.data_ptr(), counts.data_ptr(), st.cuda_stream)
+        alp.search_shard(targets, budget, lo, hi, pairs.data_ptr(), pairs.data_ptr() + 8 * n, st.cuda_stream)
+        w = gather_pairs(pairs, gathered, group)
+        return alp.finalize_gathered(targets, budget, gathered.data_ptr(), w, st.cuda_stream)

@@ -83,8 +83,12 @@ def _gloo_worker(rank, world, port, q):
         keys.append(0x7FFFFFFFFFFFFFFF if not np.isfinite(v) else (int(v.view(np.uint32)) << 32) | s)
     k = torch.tensor(keys, dtype=torch.int64)
     c = torch.tensor([rank + 1, 5, 0], dtype=torch.int64)
+    pairs = torch.cat([k, c])
     reduce_keys(k, c)
-    q.put((rank, k.tolist(), c.tolist()))
+    from paper_2604_15186_b200.dist import gather_pairs
+    gathered = torch.empty(world * pairs.numel(), dtype=torch.int64)
+    w = gather_pairs(pairs, gathered)
+    q.put((rank, k.tolist(), c.tolist(), w, gathered.tolist(), pairs.tolist()))
     dist.destroy_process_group()
 
 
@@ -102,6 +106,13 @@ def test_gloo_two_rank_key_reduction():
         p.join(timeout=60)
     exp0 = (int(np.float32(1.5).view(np.uint32)) << 32) | 10       # lower value wins
     exp1 = (int(np.float32(2.0).view(np.uint32)) << 32) | 99       # equal values: lower segment wins
-    for _rank, k, c in out:
+    for _rank, k, c, _w, _g, _p in out:
         assert k == [exp0, exp1, 0x7FFFFFFFFFFFFFFF]
         assert c == [3, 10, 0]
+    # one all-gather: rank r's (keys, counts) land in row r; MIN / SUM over rows = the all-reduces
+    own = {r: p for r, _k, _c, _w, _g, p in out}
+    for _rank, k, c, w, g, _p in out:
+        assert w == 2 and g == own[0] + own[1]
+        rows = [g[0:6], g[6:12]]
+        assert [min(rows[0][i], rows[1][i]) for i in range(3)] == k
+        assert [rows[0][3 + i] + rows[1][3 + i] for i in range(3)] == c

@@ -243,6 +243,28 @@ def test_partition_independence(P):
         assert (r.index, r.feasible_count, r.latency_key) == (ref.index, ref.feasible_count, ref.latency_key)
 
 
+def test_finalize_gathered_matches_allreduce(P):
+    """The one-all-gather exchange: per-rank int64[2n] (keys, counts) rows, reduced inside K3."""
+    import torch
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = [d["targets"][0], d["targets"][0] * 2.0, d["targets"][0] * 40.0]  # incl. an infeasible target
+    ref = alp.search_batch(lam, I.budget)
+    n = len(lam)
+    for world in (1, 3, 8):
+        gathered = torch.empty(world * 2 * n, dtype=torch.int64, device="cuda")
+        for rank in range(world):
+            lo, hi = alp.shard_range(I.budget, rank, world)
+            row = gathered[rank * 2 * n:(rank + 1) * 2 * n]
+            alp.search_shard(lam, I.budget, lo, hi, row.data_ptr(), row.data_ptr() + 8 * n)
+            torch.cuda.synchronize()
+        res = alp.finalize_gathered(lam, I.budget, gathered.data_ptr(), world)
+        for r, e in zip(res, ref):
+            assert (r.found, r.index, r.feasible_count, r.latency_key, r.units) == (e.found, e.index, e.feasible_count,
+                                                                                   e.latency_key, e.units)
+
+
 def test_infeasible_and_zero_budget(P):
     d = generate.load("C1")
     alp = P.Alp.from_instance(d)
@@ -473,3 +495,16 @@ def test_max_options_per_llm_vs_bruteforce(P):
         o = oracle.search(I, lam, 600, threads=16)
         _same(r, o.found, o.latency_key, o.index, o.count, lam)
         _check_winner(P, alp, I, lam, 600, r)
+
+
+def test_search_distributed_single_process(P):
+    """dist.search_distributed without a process group (world 1) on torch's default stream: the
+    gather-based exchange and the finalize must be ordered with the search."""
+    from paper_2604_15186_b200.dist import search_distributed
+    d = generate.load("C4")
+    alp = P.Alp.from_instance(d)
+    lam = [d["targets"][0], d["targets"][0] * 3.0]
+    ref = alp.search_batch(lam, d["budget_units"])
+    for _ in range(3):
+        res = search_distributed(alp, lam, d["budget_units"])
+        assert [(r.index, r.feasible_count) for r in res] == [(e.index, e.feasible_count) for e in ref]
