@@ -30,6 +30,9 @@ namespace {
 thread_local std::string g_err = "no error";
 constexpr size_t kPinnedStageMax = 256 * 1024;  // larger arena uploads skip the pinned staging buffer
 constexpr size_t kArenaWork = 64;  // work counters kept in the handle arena (phases of one search)
+// fused-launch work counters: <= kInlineTargets targets x <= 16 b-chunks (b columns are split in
+// chunks of >= 64 and K <= 1024)
+constexpr size_t kFusedWork = (size_t)kInlineTargets * 16;
 
 // Small pinned host buffer per host thread (allocated once, shared by all handles the thread uses)
 // for the per-search H2D of targets and D2H of results: pageable copies cost a staging hop each.
@@ -564,9 +567,9 @@ alp_status upload_all(alp_s *h) {
   A.add(h->T, &h->d_T);
   A.add(h->R, &h->d_R);
   // self-resetting scratch, initialised through the copied section (rest state), packed in one
-  // section: [fbest | fz keys x8 | fz counts x8 | fz work x64 | fdone, fz ticket (u32 pair)]
+  // section: [fbest | fz keys x8 | fz counts x8 | fz work x128 | fdone, fz ticket (u32 pair)]
   static const std::vector<unsigned long long> rest = [] {
-    std::vector<unsigned long long> v(1 + 2 * kInlineTargets + kArenaWork + 1, 0ull);
+    std::vector<unsigned long long> v(1 + 2 * kInlineTargets + kFusedWork + 1, 0ull);
     v[0] = ~0ull;
     for (int i = 0; i < kInlineTargets; ++i) v[1 + i] = ~0ull;
     return v;
@@ -587,7 +590,7 @@ alp_status upload_all(alp_s *h) {
   h->a_fzkeys = d_rest + 1;
   h->a_fzcounts = d_rest + 1 + kInlineTargets;
   h->a_fzwork = d_rest + 1 + 2 * kInlineTargets;
-  h->a_fdone = reinterpret_cast<unsigned *>(d_rest + 1 + 2 * kInlineTargets + kArenaWork);
+  h->a_fdone = reinterpret_cast<unsigned *>(d_rest + 1 + 2 * kInlineTargets + kFusedWork);
   h->a_fzticket = h->a_fdone + 1;
   CU(cudaEventRecord(h->ctx.ready, h->stream));  // searches on other streams wait for the upload
   return ALP_OK;
@@ -884,7 +887,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   int launches = 0;
   unsigned long long *work = h->a_work;
   if (fused) {
-    if (nctr > kArenaWork) return fail(ALP_EINTERNAL, "fused search: %zu work counters", nctr);
+    if (nctr > kFusedWork) return fail(ALP_EINTERNAL, "fused search: %zu work counters", nctr);
     FusedArgs &z = g.a.fz;
     z.on = 1;
     z.finalize = fuse_finalize ? 1 : 0;

@@ -508,3 +508,20 @@ def test_search_distributed_single_process(P):
     for _ in range(3):
         res = search_distributed(alp, lam, d["budget_units"])
         assert [(r.index, r.feasible_count) for r in res] == [(e.index, e.feasible_count) for e in ref]
+
+
+def test_fused_many_b_chunks_eight_targets(P):
+    """One LLM with K = 1024 options (b columns split in several chunks) and 8 targets: the fused
+    launch's work counters cover targets x chunks phases."""
+    S = [1, 2, 3, 4]
+    T = [1, 2, 4, 8]
+    R = list(range(1, 65))
+    d = generate.random_instance(77, M=1, F=4, S=S, T=T, R=R, budget=300)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lams = [0.02 * (i + 1) for i in range(8)]
+    res = alp.search_batch(lams, 300)
+    assert alp.last_launches == 1
+    for lam, r in zip(lams, res):
+        o = oracle.search(I, lam, 300)
+        _same(r, o.found, o.latency_key, o.index, o.count, lam)
