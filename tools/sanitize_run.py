@@ -43,6 +43,13 @@ st.synchronize()
 k = keys.min(dim=0).values.contiguous()
 c = cnts.sum(dim=0).contiguous()
 print("shards", alp.finalize(lam, B, k.data_ptr(), c.data_ptr())[0].index)
+# one-all-gather exchange layout: per-rank int64[2n] rows, reduced inside K3
+g = torch.empty(3 * 2, dtype=torch.int64, device="cuda")
+for rank in range(3):
+    lo, hi = alp.shard_range(B, rank, 3)
+    alp.search_shard(lam, B, lo, hi, g[2 * rank:].data_ptr(), g[2 * rank + 1:].data_ptr(), st.cuda_stream)
+st.synchronize()
+print("gathered", alp.finalize_gathered(lam, B, g.data_ptr(), 3)[0].index)
 tau = (np.arange(24, dtype=np.float32).reshape(3, 8) % 5 + 1) / 8
 u = (np.arange(24, dtype=np.int32).reshape(3, 8) % 3)
 print("terms", P.Alp.from_terms(tau, u).search(1.0, 4).index)
