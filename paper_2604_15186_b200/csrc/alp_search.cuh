@@ -269,7 +269,6 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
                               uint32_t &best_seg, unsigned long long &cnt, int R, int work_slot) {
   const int lane = threadIdx.x & 31;
   const uint64_t n = P.item_hi - P.item_lo;
-  const int K = P.K;
   const int ng4 = P.bchunk_wpad >> 2;
   // Dynamic work distribution: warps take runs of P.grab consecutive items from this phase's
   // counter (the result is independent of who evaluates what: keys carry (value, segment) and the
