@@ -252,6 +252,8 @@ struct alp_s {
   uint32_t L = 1, n_chunks = 1, n_groups = 1, nQ = 1, A = 1;
   uint32_t pw[ALP_MAX_M] = {0};
   std::vector<int> tile_s, bperm, bu, dv, dcnt;
+  std::vector<int> gsum;     // unit sum of each uniform warp group (groups [0, n_groups_u))
+  uint32_t n_groups_u = 0;
   std::vector<uint32_t> tile_e, tile_off;
   int rows_per_lane = 8;
   int nq_force = 0;    // ALP_NQ: a-ranges per row (tuning), 0 = automatic
@@ -412,9 +414,39 @@ alp_status make_plan(alp_s *h) {
       }
     }
   }
-  while (h->tile_s.size() % kWarpTiles) {
-    h->tile_s.push_back(h->tile_s.back());
-    for (int r = 0; r < T; ++r) h->tile_e.push_back(kDummy);
+  // warp groups of 32 lane tiles: first every group whose 32 tiles share one unit sum (a
+  // warp-uniform remaining budget), then the leftover tiles of all sums (mixed groups), padded
+  {
+    const size_t nt = h->tile_s.size();
+    std::vector<int> ts;
+    std::vector<uint32_t> te;
+    std::vector<size_t> rest;
+    ts.reserve(nt + kWarpTiles);
+    te.reserve((nt + kWarpTiles) * T);
+    h->gsum.clear();
+    for (size_t i = 0; i < nt;) {
+      size_t j = i;
+      while (j < nt && h->tile_s[j] == h->tile_s[i]) ++j;  // tiles of one sum are consecutive
+      const size_t full = (j - i) / kWarpTiles * kWarpTiles;
+      for (size_t k = i; k < i + full; ++k) {
+        ts.push_back(h->tile_s[k]);
+        te.insert(te.end(), h->tile_e.begin() + k * T, h->tile_e.begin() + (k + 1) * T);
+      }
+      for (size_t g = 0; g < full / kWarpTiles; ++g) h->gsum.push_back(h->tile_s[i]);
+      for (size_t k = i + full; k < j; ++k) rest.push_back(k);
+      i = j;
+    }
+    h->n_groups_u = (uint32_t)h->gsum.size();
+    for (size_t k : rest) {
+      ts.push_back(h->tile_s[k]);
+      te.insert(te.end(), h->tile_e.begin() + k * T, h->tile_e.begin() + (k + 1) * T);
+    }
+    while (ts.size() % kWarpTiles) {
+      ts.push_back(ts.back());
+      for (int r = 0; r < T; ++r) te.push_back(kDummy);
+    }
+    h->tile_s.swap(ts);
+    h->tile_e.swap(te);
   }
   h->n_groups = (uint32_t)(h->tile_s.size() / kWarpTiles);
   // smem byte offsets of each row's sort-group terms (tau of LLM g0+j lives at ((g0+j)*K + d)*4;
@@ -479,7 +511,8 @@ struct PlanSnap {
   uint32_t L, n_chunks, n_groups, nQ, A;
   uint32_t pw[ALP_MAX_M];
   long long umax_total;
-  std::vector<int> dv;
+  std::vector<int> dv, gsum;
+  uint32_t n_groups_u;
   int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt;
   uint32_t *d_tile_e, *d_tile_off;
   std::shared_ptr<PlanDev> dev;
@@ -529,6 +562,8 @@ alp_status get_plan(alp_s *h) {
     memcpy(P->pw, h->pw, sizeof(P->pw));
     P->umax_total = h->umax_total;
     P->dv = h->dv;
+    P->gsum = h->gsum;
+    P->n_groups_u = h->n_groups_u;
     g_plans[key] = P;
     h->tile_s.clear(); h->tile_e.clear(); h->tile_off.clear(); h->bperm.clear(); h->bu.clear(); h->dcnt.clear();
   }
@@ -538,6 +573,8 @@ alp_status get_plan(alp_s *h) {
   memcpy(h->pw, P->pw, sizeof(h->pw));
   h->umax_total = P->umax_total;
   h->dv = P->dv;
+  h->gsum = P->gsum;
+  h->n_groups_u = P->n_groups_u;
   h->d_u = P->d_u; h->d_tile_s = P->d_tile_s; h->d_tile_e = P->d_tile_e; h->d_tile_off = P->d_tile_off;
   h->d_bperm = P->d_bperm; h->d_dv = P->d_dv; h->d_dcnt = P->d_dcnt;
   h->plan_dev = P->dev;
