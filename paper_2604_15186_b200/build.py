@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libscepsy_alp.so")
-SOURCES = ["alp_api.cu", "alp_kernels.cu", "alp_search_t8.cu", "alp_search_t12.cu", "alp_search_t16.cu"]
+SOURCES = ["alp_api.cu", "alp_kernels.cu", "alp_search_t8.cu", "alp_search_t12.cu", "alp_search_t16.cu",
+           "alp_search_u.cu"]
 HEADERS = ["alp_internal.h", "alp_search.cuh", os.path.join("..", "..", "include", "alp.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

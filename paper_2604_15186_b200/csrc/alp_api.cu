@@ -266,7 +266,7 @@ struct alp_s {
   void *d_arena = nullptr;  // every static table + single-target scratch (one allocation)
   double *d_n = nullptr, *d_p = nullptr, *d_rate = nullptr, *d_lat = nullptr, *d_tmax = nullptr;
   int *d_S = nullptr, *d_T = nullptr, *d_R = nullptr, *d_off = nullptr, *d_minu = nullptr, *d_u = nullptr;
-  int *d_tile_s = nullptr, *d_bperm = nullptr, *d_dv = nullptr, *d_dcnt = nullptr;
+  int *d_tile_s = nullptr, *d_bperm = nullptr, *d_dv = nullptr, *d_dcnt = nullptr, *d_gsum = nullptr;
   uint32_t *d_tile_e = nullptr, *d_tile_off = nullptr;
   float *d_tau_fixed = nullptr;
   double *d_term_fixed = nullptr, *d_b_fixed = nullptr;
@@ -513,7 +513,7 @@ struct PlanSnap {
   long long umax_total;
   std::vector<int> dv, gsum;
   uint32_t n_groups_u;
-  int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt;
+  int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt, *d_gsum;
   uint32_t *d_tile_e, *d_tile_off;
   std::shared_ptr<PlanDev> dev;
 };
@@ -554,6 +554,7 @@ alp_status get_plan(alp_s *h) {
     A.add(h->bperm, &P->d_bperm);
     A.add(h->dv, &P->d_dv);
     A.add(h->dcnt, &P->d_dcnt);
+    A.add(h->gsum, &P->d_gsum);
     CU(A.commit(&P->dev->mem, h->h2d, h->stream));
     CU(cudaStreamSynchronize(h->stream));  // shared by handles on other streams (cold path only)
     P->N = h->N; P->a_llm = h->a_llm; P->b_llm = h->b_llm; P->Ka = h->Ka; P->Kb = h->Kb; P->g0 = h->g0;
@@ -576,7 +577,7 @@ alp_status get_plan(alp_s *h) {
   h->gsum = P->gsum;
   h->n_groups_u = P->n_groups_u;
   h->d_u = P->d_u; h->d_tile_s = P->d_tile_s; h->d_tile_e = P->d_tile_e; h->d_tile_off = P->d_tile_off;
-  h->d_bperm = P->d_bperm; h->d_dv = P->d_dv; h->d_dcnt = P->d_dcnt;
+  h->d_bperm = P->d_bperm; h->d_dv = P->d_dv; h->d_dcnt = P->d_dcnt; h->d_gsum = P->d_gsum;
   h->plan_dev = P->dev;
   return ALP_OK;
 }
@@ -748,6 +749,7 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.rows_per_lane = h->rows_per_lane;
   a.min_blocks = h->min_blocks;
   a.dv = h->d_dv; a.dcnt = h->d_dcnt;
+  a.n_groups_u = h->n_groups_u; a.gsum = h->d_gsum;
   a.t_begin = 0; a.t_end = n_targets; a.c_begin = 0; a.c_end = a.n_bchunks;
   // occupancy per kernel variant and smem size (cached: the query costs microseconds per search)
   const long long okey = ((long long)a.smem_bytes << 24) | ((long long)a.bchunk_wpad << 8) |
@@ -897,6 +899,40 @@ alp_status ensure_finalize_scratch(alp_s *h, int n, cudaStream_t st) {
   return ALP_OK;
 }
 
+// Uniform-register path (alp_search_u.cu) for single-target searches with short b rows: the
+// arguments with its shared-memory layout, lut geometry and grid; false when not applicable.
+bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, int &grid) {
+  if (getenv("ALP_NO_UR") || n != 1 || a.q_budget || h->from_terms || h->rows_per_lane != 12 ||
+      a.n_bchunks != 1 || a.bchunk_wpad > 34 || hi >= (1ull << 31) || h->M * h->K > 1024)
+    return false;
+  auto umax = [&](int m) {
+    int x = 0;
+    for (int k = 0; k < h->K; ++k) x = std::max(x, h->u[(size_t)m * h->K + k]);
+    return x;
+  };
+  int lb = 0;
+  for (int m = 0; m < h->g1; ++m) lb += umax(m);  // prefix + sort-group LLMs
+  if (h->a_llm >= 0) lb += umax(h->a_llm);
+  ua = a;
+  ua.lut_base = lb;
+  ua.lut_n = lb + 1;
+  const int rows = a.D + 1;
+  if (!utables_fit((int)h->n_chunks, h->Ka, ua.lut_n, rows * a.row_stride, (int)h->n_groups_u)) return false;
+  auto align16 = [](int x) { return (x + 15) & ~15; };
+  int off = align16((h->g1 * h->K + 2) * 4);
+  ua.off_lut = off;
+  off = align16(off + ua.lut_n * 8);
+  ua.off_btab = off;
+  off = align16(off + rows * a.row_stride * 4);
+  ua.smem_bytes = off;
+  const long long okey = (1ll << 60) | ((long long)ua.smem_bytes << 8) | ua.bchunk_wpad;
+  auto oit = h->occ_cache.find(okey);
+  const int bps = (oit != h->occ_cache.end()) ? oit->second : (h->occ_cache[okey] = search_u_max_blocks_per_sm(ua));
+  if (bps < 1) return false;
+  grid = h->sm_count * bps;
+  return true;
+}
+
 // K2 over work items [lo, hi) (classic: after K1; fused: alone, finalize optional).  Writes the
 // per-target (key, count) of this shard to keys/counts; async on st.
 alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
@@ -978,8 +1014,15 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
       CU(cudaMemsetAsync(h->g_dbg.p, 0, (size_t)g.grid * 8 * sizeof(unsigned long long), st));
       g.a.dbg_ts = h->g_dbg.p;
     }
-    CU(launch_search(g.a, g.grid, st));
-    launches += 1;
+    SearchArgs ua;
+    int ugrid = 0;
+    if (fused && ur_path(h, g.a, n, hi, ua, ugrid)) {  // option terms + tables, then the UR search
+      CU(launch_search_u(ua, ugrid, st));
+      launches += 2;
+    } else {
+      CU(launch_search(g.a, g.grid, st));
+      launches += 1;
+    }
     if (dbg) {
       std::vector<unsigned long long> ts((size_t)g.grid * 8);
       CU(cudaMemcpyAsync(ts.data(), h->g_dbg.p, ts.size() * 8, cudaMemcpyDeviceToHost, st));

@@ -131,6 +131,11 @@ struct SearchArgs {
   FusedArgs fz;
   FinalizeExtra fin;
   unsigned long long *dbg_ts;  // [grid][8] %globaltimer stamps per block (ALP_DBG_TS) or nullptr
+  // uniform-register path (k_uprep + k_search_u): tables in the constant bank
+  uint32_t n_groups_u;   // warp groups [0, n_groups_u) have one unit sum (uniform remaining budget)
+  const int *gsum;       // [n_groups_u] their unit sums (device, plan)
+  int lut_base;          // lut index of remaining budget r = r + lut_base - R (>= 0 for every r reached)
+  int lut_n;             // lut entries (lut_base + 1)
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
   int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it
@@ -172,6 +177,10 @@ cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st);
 cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
                              int n_work, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
+// uniform-register path: prep (option terms + constant-bank tables, one block) and search
+cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st);
+int search_u_max_blocks_per_sm(const SearchArgs &a);
+bool utables_fit(int n_chunks, int Ka, int lut_n, int btab_floats, int n_groups_u);
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
 int search_max_blocks_per_sm(const SearchArgs &a);

@@ -1,0 +1,269 @@
+// Uniform-register variant of the search (k_uprep + k_search_u), for single-target searches with
+// short b rows (C4-like).  The per-search tables — prefix-chunk partial sums, a-options, the
+// remaining-budget -> masked-row lookup and the masked rows — live in the constant bank, and the
+// search kernel runs one warp per block with a blockIdx-derived (uniform) item schedule, so for
+// the warp groups whose 32 lane tiles share one unit sum the masked-row index is warp-uniform:
+// ptxas loads the b values with LDCU into uniform registers and FADD2 reads them from there
+// (tools/microbench/pipes6: 92 vs 80 candidates/clk/SM).  Mixed groups read their lanes' rows
+// with ordinary (divergent) constant loads.  Same arithmetic, same keys and counts as k_search.
+#include "alp_search.cuh"
+
+#include <mutex>
+
+namespace alp {
+
+constexpr int kUChunks = 1024, kUA = 64, kULut = 1024, kUBtab = 4096, kUGroups = 1024;
+struct UTables {
+  float2 pfx[kUChunks];   // {canonical prefix partial sum, bits(prefix units)} per chunk
+  int gsum[kUGroups];     // unit sum of each uniform warp group
+  float4 a[kUA];          // {tau_a, bits(u_a), bits(feasible), 0}
+  int2 lut[kULut];        // lut[lut_base - U] = {masked-row float offset, #finite entries}
+  float btab[kUBtab];     // masked rows
+};
+__constant__ UTables cu;
+
+// ------------------------------------------------------------------ prep: one block
+// Option terms of the (single) target into global (finalize inputs) and shared memory, then the
+// constant-bank tables written through the symbol's global address (the constant cache is
+// refilled at the next kernel launch).
+__global__ void k_uprep(const __grid_constant__ SearchArgs P, UTables *T) {
+  extern __shared__ float s_t[];  // [M*K] option terms
+  const int MK = P.M * P.K, K = P.K, tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < MK; i += nt) {
+    float tau;
+    double term, b;
+    int u;
+    option_terms(P.fz.prof, P.fz.tgt[0], i / K, i % K, &tau, &term, &b, &u);
+    s_t[i] = tau;
+    P.fz.o_tau[i] = tau;
+    P.fz.o_term[i] = term;
+    P.fz.o_b[i] = b;
+  }
+  __syncthreads();
+  // prefix chunks: canonical sum over LLMs 0..g0-1
+  for (uint32_t c = tid; c < P.n_chunks; c += nt) {
+    float pa = 0.f;
+    int U = 0;
+    for (int m = 0; m < P.g0; ++m) {
+      const uint32_t d = (c / P.pw[m]) % (uint32_t)K;
+      pa = __fadd_rn(pa, s_t[m * K + d]);
+      U += P.u[m * K + d];
+    }
+    T->pfx[c] = make_float2(pa, __int_as_float(U));
+  }
+  for (uint32_t g = tid; g < P.n_groups_u; g += nt) T->gsum[g] = P.gsum[g];
+  for (int a = tid; a < P.Ka; a += nt) {
+    const float ta = P.a_llm >= 0 ? s_t[P.a_llm * K + a] : 0.f;
+    const int ua = P.a_llm >= 0 ? P.u[P.a_llm * K + a] : 0;
+    const int feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
+    T->a[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), 0.f);
+  }
+  // masked rows: row i holds the u-sorted b columns with u <= dv[i-1] (row 0 none), +inf elsewhere
+  const int R = P.budget, D = P.D;
+  for (int i = tid; i < (D + 1) * P.bchunk_wpad; i += nt) {
+    const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
+    const int len = min(P.dcnt[row], P.Kb);
+    T->btab[row * P.row_stride + j] = (j < len) ? s_t[P.b_llm * K + P.bperm[j]] : __int_as_float(0x7f800000);
+  }
+  // lut: index x <-> remaining budget r = R - lut_base + x; row = #{distinct b unit values <= r}
+  for (int x = tid; x < P.lut_n; x += nt) {
+    const int r = R - P.lut_base + x;
+    int row = 0;
+    while (row < D && P.dv[row] <= r) ++row;
+    int n = 0;  // finite entries of the row
+    const int len = min(P.dcnt[row], P.Kb);
+    for (int j = 0; j < len; ++j) n += (s_t[P.b_llm * K + P.bperm[j]] < __int_as_float(0x7f800000)) ? 1 : 0;
+    T->lut[x] = make_int2(row * P.row_stride, n);
+  }
+}
+
+template <int NB4, bool TAIL2>
+__device__ __forceinline__ void eval_row_u(const float *rb, const float (&Qa)[12], float (&acc)[12]) {
+#pragma unroll
+  for (int j = 0; j < 4 * NB4 + (TAIL2 ? 2 : 0); j += 2) {
+    const float b0 = rb[j], b1 = rb[j + 1];
+#pragma unroll
+    for (int i = 0; i < 12; i += 2) {
+      float x0, y0, x1, y1;
+      add2b(x0, y0, Qa[i], Qa[i + 1], b0);
+      add2b(x1, y1, Qa[i], Qa[i + 1], b1);
+      acc[i] = min3(acc[i], x0, x1);
+      acc[i + 1] = min3(acc[i + 1], y0, y1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ search: one warp per block
+template <int NB4, bool TAIL2>
+__global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchArgs P, const UTables *ug) {
+  constexpr int T = 12;
+  extern __shared__ __align__(16) unsigned char smem[];
+  // [g1*K + 2] terms of LLMs 0..g1-1 then {0, +inf} | lut [lut_n] int2 | masked rows
+  float *s_tau = reinterpret_cast<float *>(smem);
+  int2 *s_lut = reinterpret_cast<int2 *>(smem + P.off_lut);
+  float *s_btab = reinterpret_cast<float *>(smem + P.off_btab);
+  const int lane = threadIdx.x;
+  pdl_wait();
+  for (int i = lane; i < P.g1 * P.K; i += 32) s_tau[i] = __ldcg(P.tau + i);
+  if (lane == 0) {
+    s_tau[P.g1 * P.K] = 0.f;
+    s_tau[P.g1 * P.K + 1] = __int_as_float(0x7f800000);
+  }
+  // shared-memory copies of the lut and masked rows for the mixed groups (lane-varying rows)
+  for (int i = lane; i < P.lut_n; i += 32) s_lut[i] = __ldcg(&ug->lut[i]);
+  for (int i = lane; i < (P.D + 1) * P.row_stride; i += 32) s_btab[i] = __ldcg(&ug->btab[i]);
+  __syncwarp();
+  const unsigned char *tau_b = smem;
+  float best = __int_as_float(0x7f800000);
+  uint32_t best_seg = 0xffffffffu;
+  unsigned long long cnt = 0ull;
+  float Qr[T], acc[T];
+  const uint32_t n = (uint32_t)(P.item_hi - P.item_lo);
+  for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {  // uniform item schedule
+    const uint32_t it = (uint32_t)P.item_lo + k;
+    const uint32_t tq = fdiv(it, P.fd_nQ);
+    const uint32_t q = it - tq * P.nQ;           // a-range of the row
+    const uint32_t chunk = fdiv(tq, P.fd_ng);
+    const uint32_t grp = tq - chunk * P.n_groups;
+    const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
+    const float2 pf = cu.pfx[chunk];
+    const int upfx = __float_as_int(pf.y);
+    const uint32_t tile = grp * kWarpTiles + lane;
+    const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
+    unsigned nfin = 0;
+#pragma unroll
+    for (int v = 0; v < T; ++v) {
+      const uint4 o = __ldg(op + v);
+      float qv = pf.x;
+      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
+      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
+      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
+      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
+      Qr[v] = qv;
+      nfin += (qv < __int_as_float(0x7f800000)) ? 1u : 0u;
+      acc[v] = __int_as_float(0x7f800000);
+    }
+    unsigned c32 = 0;
+    if (grp < P.n_groups_u) {
+      // warp-uniform remaining budget: uniform-register b operands
+      const int xg = P.lut_base - upfx - cu.gsum[grp];
+#pragma unroll 2
+      for (int a = a0; a < a1; ++a) {
+        const float4 av = cu.a[a];
+        const int2 lu = cu.lut[xg - __float_as_int(av.y)];
+        c32 += (unsigned)(lu.y * __float_as_int(av.z));
+        float Qa[T];
+#pragma unroll
+        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+        eval_row_u<NB4, TAIL2>(cu.btab + lu.x, Qa, acc);
+      }
+    } else {
+      // mixed group: the lanes' own remaining budgets, rows from the shared-memory copies
+      const int xl = P.lut_base - upfx - __ldg(P.tile_s + tile);
+      const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
+#pragma unroll 2
+      for (int a = a0; a < a1; ++a) {
+        const float4 av = cu.a[a];
+        const int2 lu = s_lut[xl - __float_as_int(av.y)];
+        c32 += (unsigned)(lu.y * __float_as_int(av.z));
+        float Qa[T];
+#pragma unroll
+        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+        eval_row<T, NB4, TAIL2>(bbase + 4u * (uint32_t)lu.x, Qa, acc, 0);
+      }
+    }
+    cnt += (unsigned long long)c32 * nfin;
+    fold_rows<T>(P, acc, tile, chunk, q, best, best_seg);  // segment: from a-range q to the row's end
+  }
+  pdl_trigger();
+  unsigned long long key = (best < __int_as_float(0x7f800000)) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg
+                                                               : kKeyNone;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+    const unsigned long long oc = __shfl_xor_sync(0xffffffffu, cnt, o);
+    key = ok < key ? ok : key;
+    cnt += oc;
+  }
+  if (lane == 0) {
+    if (key != kKeyNone) atomicMin(P.fz.acc_keys, key);
+    if (cnt) atomicAdd(P.fz.acc_counts, cnt);
+  }
+  fused_epilogue(P, nullptr);
+}
+
+// ------------------------------------------------------------------ launch
+// Per-device staging copy of the tables (k_uprep writes it; one D2D copy moves it into the
+// constant bank; the mixed groups' shared-memory copies read it) and the ordering event that keeps
+// concurrent searches on other streams from overwriting the constant bank in use.
+struct UState {
+  UTables *staging = nullptr;
+  cudaEvent_t done = nullptr;
+};
+static std::mutex g_u_mu;
+static UState &ustate() {
+  static UState s[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  UState &u = s[dev & 63];
+  if (!u.staging) {
+    cudaMalloc(reinterpret_cast<void **>(&u.staging), sizeof(UTables));
+    cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming);
+  }
+  return u;
+}
+
+template <int NB4, bool TAIL2>
+static cudaError_t launch_u(const SearchArgs &a, int grid, cudaStream_t st) {
+  const int smem = a.smem_bytes;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  const UTables *ug = ustate().staging;
+  return cudaLaunchKernelEx(&cfg, k_search_u<NB4, TAIL2>, a, ug);
+}
+
+template <int NB4, bool TAIL2>
+static int occ_u(const SearchArgs &a) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_search_u<NB4, TAIL2>, 32, a.smem_bytes) != cudaSuccess)
+    return 0;
+  return n;
+}
+
+
+static cudaError_t launch_u_search(const SearchArgs &a, int grid, cudaStream_t st) {
+#define CALL(T_, N, T2) launch_u<N, T2>(a, grid, st)
+  ALP_DISPATCH_W(CALL, 12);
+#undef CALL
+}
+
+cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_u_mu);
+  UState &u = ustate();
+  if (!u.staging) return cudaErrorMemoryAllocation;
+  const int MK = a.M * a.K;
+  const int threads = MK >= 512 ? 1024 : (MK >= 256 ? 512 : 256);
+  cudaError_t e = cudaStreamWaitEvent(st, u.done, 0);  // the previous search using the constant bank
+  if (e != cudaSuccess) return e;
+  k_uprep<<<1, threads, (size_t)MK * 4, st>>>(a, u.staging);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbolAsync(cu, u.staging, sizeof(UTables), 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    return e;
+  if ((e = launch_u_search(a, grid, st)) != cudaSuccess) return e;
+  return cudaEventRecord(u.done, st);
+}
+
+int search_u_max_blocks_per_sm(const SearchArgs &a) {
+#define CALL(T_, N, T2) occ_u<N, T2>(a)
+  ALP_DISPATCH_W(CALL, 12);
+#undef CALL
+}
+
+bool utables_fit(int n_chunks, int Ka, int lut_n, int btab_floats, int n_groups_u) {
+  return n_chunks <= kUChunks && Ka <= kUA && lut_n <= kULut && btab_floats <= kUBtab && n_groups_u <= kUGroups;
+}
+
+}  // namespace alp

@@ -525,3 +525,47 @@ def test_fused_many_b_chunks_eight_targets(P):
     for lam, r in zip(lams, res):
         o = oracle.search(I, lam, 300)
         _same(r, o.found, o.latency_key, o.index, o.count, lam)
+
+
+@pytest.mark.parametrize("name", ["hand", "C4"])
+def test_uniform_register_path_matches_fused(P, name, monkeypatch):
+    """Single-target searches with short b rows run the uniform-register pair (k_uprep: option
+    terms + constant-bank tables; k_search_u: one warp per block, warp-uniform masked rows from the
+    constant bank, mixed groups from shared memory); ALP_NO_UR forces the fused kernel."""
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (d["targets"][0], d["targets"][0] * 0.3, d["targets"][0] * 2.5):
+        u = alp.search(lam, I.budget)
+        assert alp.last_launches == 2
+        monkeypatch.setenv("ALP_NO_UR", "1")
+        f = alp.search(lam, I.budget)
+        assert alp.last_launches == 1
+        monkeypatch.delenv("ALP_NO_UR")
+        assert (u.found, u.index, u.feasible_count, u.units) == (f.found, f.index, f.feasible_count, f.units)
+        assert u.latency_key == f.latency_key and (u.latency == f.latency or not u.found)
+        if name == "hand":
+            o = oracle.search(I, lam, I.budget)
+            _same(u, o.found, o.latency_key, o.index, o.count, lam)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_uniform_register_path_random_vs_bruteforce(P, seed):
+    """Random instances whose b rows fit the uniform-register path (<= 34 options per LLM)."""
+    rng = np.random.default_rng(5000 + seed)
+    M = int(rng.integers(2, 6))
+    S = sorted(set(int(x) for x in rng.integers(1, 5, size=int(rng.integers(1, 3)))))
+    T = [1, 2, 4][: int(rng.integers(1, 4))]
+    R = list(range(1, int(rng.integers(2, 4))))
+    K = len(S) * len(T) * len(R)
+    while K ** M > 2_000_000:
+        M -= 1
+    budget = int(rng.integers(2, 40))
+    d = generate.random_instance(5000 + seed, M=M, F=4, S=S, T=T, R=R, budget=budget, min_units=bool(seed % 3 == 1))
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (0.02, 0.3, 1.5):
+        r = alp.search(lam, budget)
+        o = oracle.search(I, lam, budget, threads=4)
+        _same(r, o.found, o.latency_key, o.index, o.count, (seed, lam))
+        _check_winner(P, alp, I, lam, budget, r)
