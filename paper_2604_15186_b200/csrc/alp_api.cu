@@ -929,7 +929,9 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   auto oit = h->occ_cache.find(okey);
   const int bps = (oit != h->occ_cache.end()) ? oit->second : (h->occ_cache[okey] = search_u_max_blocks_per_sm(ua));
   if (bps < 1) return false;
-  grid = h->sm_count * bps;
+  int use = bps;
+  if (const char *v = getenv("ALP_U_BPS")) use = std::max(1, std::min(bps, atoi(v)));  // tuning knob
+  grid = h->sm_count * use;
   return true;
 }
 

@@ -27,8 +27,24 @@ __constant__ UTables cu;
 // constant-bank tables written through the symbol's global address (the constant cache is
 // refilled at the next kernel launch).
 __global__ void k_uprep(const __grid_constant__ SearchArgs P, UTables *T) {
-  extern __shared__ float s_t[];  // [M*K] option terms
+  extern __shared__ __align__(16) float s_t[];  // [M*K] option terms, then the staged plan tables
   const int MK = P.M * P.K, K = P.K, tid = threadIdx.x, nt = blockDim.x;
+  const int R = P.budget, D = P.D, Kb = P.Kb;
+  float *s_bs = s_t + MK;                                   // [Kb] u-sorted b terms
+  int *s_dv = reinterpret_cast<int *>(s_bs + Kb);           // [D]
+  int *s_len = s_dv + D;                                    // [D+1] masked-row lengths (dcnt)
+  int *s_fin = s_len + (D + 1);                             // [D+1] finite entries per row
+  int *s_bp = s_fin + (D + 1);                              // [Kb] bperm
+  int *s_u = s_bp + Kb;                                     // [g0*K] prefix units
+  int *s_ua = s_u + P.g0 * K;                               // [Ka] a units
+  // static plan tables first (cp.async: in flight while the FP64 option terms are computed)
+  for (int i = tid; i < D; i += nt) cp_async4(s_dv + i, P.dv + i);
+  for (int i = tid; i <= D; i += nt) cp_async4(s_len + i, P.dcnt + i);
+  for (int i = tid; i < Kb; i += nt) cp_async4(s_bp + i, P.bperm + i);
+  for (int i = tid; i < P.g0 * K; i += nt) cp_async4(s_u + i, P.u + i);
+  if (P.a_llm >= 0)
+    for (int i = tid; i < P.Ka; i += nt) cp_async4(s_ua + i, P.u + P.a_llm * K + i);
+  for (uint32_t g = tid; g < P.n_groups_u; g += nt) T->gsum[g] = P.gsum[g];
   for (int i = tid; i < MK; i += nt) {
     float tau;
     double term, b;
@@ -39,6 +55,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, UTables *T) {
     P.fz.o_term[i] = term;
     P.fz.o_b[i] = b;
   }
+  cp_async_wait();
   __syncthreads();
   // prefix chunks: canonical sum over LLMs 0..g0-1
   for (uint32_t c = tid; c < P.n_chunks; c += nt) {
@@ -47,33 +64,39 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, UTables *T) {
     for (int m = 0; m < P.g0; ++m) {
       const uint32_t d = (c / P.pw[m]) % (uint32_t)K;
       pa = __fadd_rn(pa, s_t[m * K + d]);
-      U += P.u[m * K + d];
+      U += s_u[m * K + d];
     }
     T->pfx[c] = make_float2(pa, __int_as_float(U));
   }
-  for (uint32_t g = tid; g < P.n_groups_u; g += nt) T->gsum[g] = P.gsum[g];
   for (int a = tid; a < P.Ka; a += nt) {
     const float ta = P.a_llm >= 0 ? s_t[P.a_llm * K + a] : 0.f;
-    const int ua = P.a_llm >= 0 ? P.u[P.a_llm * K + a] : 0;
+    const int ua = P.a_llm >= 0 ? s_ua[a] : 0;
     const int feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
     T->a[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), 0.f);
   }
   // masked rows: row i holds the u-sorted b columns with u <= dv[i-1] (row 0 none), +inf elsewhere
-  const int R = P.budget, D = P.D;
+  for (int j = tid; j < Kb; j += nt) s_bs[j] = s_t[P.b_llm * K + s_bp[j]];
+  for (int i = tid; i <= D; i += nt) s_len[i] = min(s_len[i], Kb);
+  __syncthreads();
+  for (int row = tid; row <= D; row += nt) {
+    int f = 0;
+    for (int j = 0; j < s_len[row]; ++j) f += (s_bs[j] < __int_as_float(0x7f800000)) ? 1 : 0;
+    s_fin[row] = f;
+  }
   for (int i = tid; i < (D + 1) * P.bchunk_wpad; i += nt) {
     const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
-    const int len = min(P.dcnt[row], P.Kb);
-    T->btab[row * P.row_stride + j] = (j < len) ? s_t[P.b_llm * K + P.bperm[j]] : __int_as_float(0x7f800000);
+    T->btab[row * P.row_stride + j] = (j < s_len[row]) ? s_bs[j] : __int_as_float(0x7f800000);
   }
+  __syncthreads();
   // lut: index x <-> remaining budget r = R - lut_base + x; row = #{distinct b unit values <= r}
   for (int x = tid; x < P.lut_n; x += nt) {
     const int r = R - P.lut_base + x;
-    int row = 0;
-    while (row < D && P.dv[row] <= r) ++row;
-    int n = 0;  // finite entries of the row
-    const int len = min(P.dcnt[row], P.Kb);
-    for (int j = 0; j < len; ++j) n += (s_t[P.b_llm * K + P.bperm[j]] < __int_as_float(0x7f800000)) ? 1 : 0;
-    T->lut[x] = make_int2(row * P.row_stride, n);
+    int lo = 0, hi = D;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
+    }
+    T->lut[x] = make_int2(lo * P.row_stride, s_fin[lo]);
   }
 }
 
@@ -248,7 +271,8 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st) {
   const int threads = MK >= 512 ? 1024 : (MK >= 256 ? 512 : 256);
   cudaError_t e = cudaStreamWaitEvent(st, u.done, 0);  // the previous search using the constant bank
   if (e != cudaSuccess) return e;
-  k_uprep<<<1, threads, (size_t)MK * 4, st>>>(a, u.staging);
+  const size_t prep_smem = (size_t)(MK + a.Kb) * 4 + (size_t)(3 * a.D + 2 + a.Kb + a.g0 * a.K + a.Ka) * 4;
+  k_uprep<<<1, threads, prep_smem, st>>>(a, u.staging);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbolAsync(cu, u.staging, sizeof(UTables), 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
     return e;
