@@ -296,8 +296,9 @@ def run_ours(args):
                        "feasible_count": res.feasible_count},
             "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcandidates/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("k_search (fused: option terms + search + finalize)" if world == 1
-                                    else "k_search (shard: option terms + search)"),
+                         "kernel": {"k_search_u": "k_search_u (uniform-register search; after k_uprep: option "
+                                                  "terms + constant-bank tables)",
+                                    "k_search": "k_search (fused option terms + search)"}[alp.last_path],
                          "kernel_ms": kern_max / len(kern_ms),
                          "peak_def": f"{sm_count} SMs x 128 issue lanes/clk x {f_max / 1e6:.0f} MHz / 1 instr per candidate"},
             "e2e": {"value": N * nt * len(e2e_ms) / (e2e_tot * 1e-3), "unit": UNIT,

@@ -197,6 +197,9 @@ int32_t alp_last_launches(const alp_t *h);
  * result D2H in alp_search* / alp_finalize (includes an all-reduce issued in between on that
  * stream; excludes the host's wake-up after the final synchronisation). */
 float alp_last_step_ms(const alp_t *h);
+/* Which search kernel the last search ran: 0 = k_search (shared-memory masked rows), 1 = the
+ * uniform-register pair k_uprep + k_search_u (single target, short b rows; ALP_NO_UR disables). */
+int32_t alp_last_path(const alp_t *h);
 
 /* Static search plans (sort-list tiles, u-sorted columns; they depend only on the grids) are cached
  * process-wide and shared by handles built on the same device with the same grids.  This drops the

@@ -51,7 +51,7 @@ class _Result(ctypes.Structure):
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
            "alp_search_shard", "alp_finalize", "alp_finalize_gathered", "alp_last_kernel_ms", "alp_last_launches",
-           "alp_last_step_ms", "alp_last_error", "alp_plan_cache_clear", "alp_search_queries",
+           "alp_last_step_ms", "alp_last_path", "alp_last_error", "alp_plan_cache_clear", "alp_search_queries",
            "alp_schedule_egalitarian", "alp_workflow_stats", "alp_place"]
 
 _lib = None
@@ -77,7 +77,7 @@ def lib():
             "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp]),
             "alp_finalize_gathered": (i32, [vp, vp, i32, i64, vp, i32, vp, vp]),
             "alp_last_kernel_ms": (ctypes.c_float, [vp]), "alp_last_launches": (i32, [vp]),
-            "alp_last_step_ms": (ctypes.c_float, [vp]),
+            "alp_last_step_ms": (ctypes.c_float, [vp]), "alp_last_path": (i32, [vp]),
             "alp_last_error": (ctypes.c_char_p, []), "alp_plan_cache_clear": (None, []),
             "alp_search_queries": (i32, [vp, vp, vp, i32, vp]),
             "alp_schedule_egalitarian": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp]),
@@ -369,6 +369,11 @@ class Alp:
     def last_step_ms(self) -> float:
         """Device time of the last complete search step (alp_last_step_ms)."""
         return float(lib().alp_last_step_ms(self._h))
+
+    @property
+    def last_path(self) -> str:
+        """Search kernel of the last search: "k_search" or "k_search_u" (alp_last_path)."""
+        return "k_search_u" if lib().alp_last_path(self._h) == 1 else "k_search"
 
     @property
     def last_launches(self) -> int:

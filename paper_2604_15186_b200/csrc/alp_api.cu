@@ -306,6 +306,7 @@ struct alp_s {
   bool ev_pending = false;
   float last_ms = 0.f;
   int last_launches = 0;
+  bool last_ur = false;  // the last search ran the uniform-register pair (k_uprep + k_search_u)
   uint64_t h2d = 0;
   SearchArgs last_args{};
   std::map<long long, int> occ_cache;  // (smem bytes, b width, T, MB) -> resident blocks per SM
@@ -1019,11 +1020,14 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     SearchArgs ua;
     int ugrid = 0;
     if (fused && ur_path(h, g.a, n, hi, ua, ugrid)) {  // option terms + tables, then the UR search
-      CU(launch_search_u(ua, ugrid, st));
+      // the kernel-time events bracket the search kernel itself (ev0 re-recorded after the prep)
+      CU(launch_search_u(ua, ugrid, st, h->ev0));
       launches += 2;
+      h->last_ur = true;
     } else {
       CU(launch_search(g.a, g.grid, st));
       launches += 1;
+      h->last_ur = false;
     }
     if (dbg) {
       std::vector<unsigned long long> ts((size_t)g.grid * 8);
@@ -1650,6 +1654,8 @@ float alp_last_kernel_ms(const alp_t *h) {
 }
 
 int32_t alp_last_launches(const alp_t *h) { return h ? h->last_launches : 0; }
+
+int32_t alp_last_path(const alp_t *h) { return h ? (h->last_ur ? 1 : 0) : -1; }
 
 float alp_last_step_ms(const alp_t *h) { return h ? h->last_step_ms : 0.f; }
 

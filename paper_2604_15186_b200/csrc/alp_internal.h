@@ -178,7 +178,8 @@ cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *count
                              int n_work, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 // uniform-register path: prep (option terms + constant-bank tables, one block) and search
-cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st);
+// (before_search, if set, is recorded on st between the prep and the search kernel)
+cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search);
 int search_u_max_blocks_per_sm(const SearchArgs &a);
 bool utables_fit(int n_chunks, int Ka, int lut_n, int btab_floats, int n_groups_u);
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);

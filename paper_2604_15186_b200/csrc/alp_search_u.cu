@@ -263,7 +263,7 @@ static cudaError_t launch_u_search(const SearchArgs &a, int grid, cudaStream_t s
 #undef CALL
 }
 
-cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st) {
+cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search) {
   std::lock_guard<std::mutex> lock(g_u_mu);
   UState &u = ustate();
   if (!u.staging) return cudaErrorMemoryAllocation;
@@ -276,6 +276,7 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st) {
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbolAsync(cu, u.staging, sizeof(UTables), 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
     return e;
+  if (before_search && (e = cudaEventRecord(before_search, st)) != cudaSuccess) return e;
   if ((e = launch_u_search(a, grid, st)) != cudaSuccess) return e;
   return cudaEventRecord(u.done, st);
 }
