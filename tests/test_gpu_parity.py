@@ -569,3 +569,26 @@ def test_uniform_register_path_random_vs_bruteforce(P, seed):
         o = oracle.search(I, lam, budget, threads=4)
         _same(r, o.found, o.latency_key, o.index, o.count, (seed, lam))
         _check_winner(P, alp, I, lam, budget, r)
+
+
+def test_uniform_register_path_concurrent_streams(P):
+    """Two handles with different problems search on two streams at once through the shared
+    constant-bank tables: the ordering event keeps them from overwriting each other's tables."""
+    import torch
+    dA, dB = generate.load("C4"), generate.load("hand")
+    A, B = P.Alp.from_instance(dA), P.Alp.from_instance(dB)
+    la, lb = [dA["targets"][0]], [dB["targets"][0]]
+    refA, refB = A.search(la[0], dA["budget_units"]), B.search(lb[0], dB["budget_units"])
+    sA, sB = torch.cuda.Stream(), torch.cuda.Stream()
+    kA = torch.empty(2, dtype=torch.int64, device="cuda")
+    kB = torch.empty(2, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        loA, hiA = A.shard_range(dA["budget_units"], 0, 1)
+        loB, hiB = B.shard_range(dB["budget_units"], 0, 1)
+        A.search_shard(la, dA["budget_units"], loA, hiA, kA.data_ptr(), kA.data_ptr() + 8, sA.cuda_stream)
+        B.search_shard(lb, dB["budget_units"], loB, hiB, kB.data_ptr(), kB.data_ptr() + 8, sB.cuda_stream)
+        assert A.last_path == "k_search_u" and B.last_path == "k_search_u"
+        rA = A.finalize(la, dA["budget_units"], kA.data_ptr(), kA.data_ptr() + 8, sA.cuda_stream)[0]
+        rB = B.finalize(lb, dB["budget_units"], kB.data_ptr(), kB.data_ptr() + 8, sB.cuda_stream)[0]
+        assert (rA.index, rA.feasible_count, rA.latency_key) == (refA.index, refA.feasible_count, refA.latency_key)
+        assert (rB.index, rB.feasible_count, rB.latency_key) == (refB.index, refB.feasible_count, refB.latency_key)
