@@ -142,7 +142,15 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
   unsigned long long cnt = 0ull;
   float Qr[T], acc[T];
   const uint32_t n = (uint32_t)(P.item_hi - P.item_lo);
-  for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {  // uniform item schedule
+  // dynamic item tickets: lane 0 takes the next ticket while the current item is evaluated;
+  // redux.sync broadcasts it into a uniform register (ptxas keeps the derived indices uniform)
+  unsigned long long *ctr = P.work;
+  unsigned tnext = 0xffffffffu;
+  if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
+  for (;;) {
+    const uint32_t k = __reduce_min_sync(0xffffffffu, tnext);
+    if (k >= n) break;
+    if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
     const uint32_t it = (uint32_t)P.item_lo + k;
     const uint32_t tq = fdiv(it, P.fd_nQ);
     const uint32_t q = it - tq * P.nQ;           // a-range of the row
