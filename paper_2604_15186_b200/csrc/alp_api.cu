@@ -903,8 +903,9 @@ alp_status ensure_finalize_scratch(alp_s *h, int n, cudaStream_t st) {
 // Uniform-register path (alp_search_u.cu) for single-target searches with short b rows: the
 // arguments with its shared-memory layout, lut geometry and grid; false when not applicable.
 bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, int &grid) {
-  if (getenv("ALP_NO_UR") || n != 1 || a.q_budget || h->from_terms || h->rows_per_lane != 12 ||
-      a.n_bchunks != 1 || a.bchunk_wpad > 34 || hi >= (1ull << 31) || h->M * h->K > 1024)
+  if (getenv("ALP_NO_UR") || n < 1 || n > kInlineTargets || a.q_budget || h->from_terms ||
+      h->rows_per_lane != 12 || a.n_bchunks != 1 || a.bchunk_wpad > 34 || hi >= (1ull << 31) ||
+      n * h->M * h->K > 8192)
     return false;
   auto umax = [&](int m) {
     int x = 0;
@@ -918,14 +919,17 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   ua.lut_base = lb;
   ua.lut_n = lb + 1;
   const int rows = a.D + 1;
-  if (!utables_fit((int)h->n_chunks, h->Ka, ua.lut_n, rows * a.row_stride, (int)h->n_groups_u)) return false;
-  auto align16 = [](int x) { return (x + 15) & ~15; };
-  int off = align16((h->g1 * h->K + 2) * 4);
-  ua.off_lut = off;
-  off = align16(off + ua.lut_n * 8);
-  ua.off_btab = off;
-  off = align16(off + rows * a.row_stride * 4);
-  ua.smem_bytes = off;
+  auto a16 = [](int x) { return (x + 15) & ~15; };
+  // constant-bank layout: gsum, then one block per target (a-options, prefix chunks, lut, rows)
+  ua.u_tbase = a16((int)h->n_groups_u * 4);
+  ua.u_off_a = 0;
+  ua.u_off_pfx = a16(h->Ka * 16);
+  ua.u_off_lut = a16(ua.u_off_pfx + (int)h->n_chunks * 8);
+  ua.u_off_btab = a16(ua.u_off_lut + ua.lut_n * 8);
+  ua.u_tstride = a16(ua.u_off_btab + rows * a.row_stride * 4);
+  if ((long long)ua.u_tbase + (long long)n * ua.u_tstride > kUBytes) return false;
+  // shared memory: the option terms of LLMs 0..g1-1 (+ {0, +inf}) of every target
+  ua.smem_bytes = a16(n * (h->g1 * h->K + 2) * 4);
   const long long okey = (1ll << 60) | ((long long)ua.smem_bytes << 8) | ua.bchunk_wpad;
   auto oit = h->occ_cache.find(okey);
   const int bps = (oit != h->occ_cache.end()) ? oit->second : (h->occ_cache[okey] = search_u_max_blocks_per_sm(ua));

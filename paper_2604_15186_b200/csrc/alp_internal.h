@@ -136,6 +136,9 @@ struct SearchArgs {
   const int *gsum;       // [n_groups_u] their unit sums (device, plan)
   int lut_base;          // lut index of remaining budget r = r + lut_base - R (>= 0 for every r reached)
   int lut_n;             // lut entries (lut_base + 1)
+  // byte layout of the constant-bank tables: gsum at 0; target t's block at u_tbase + t*u_tstride
+  // with the a-options, prefix chunks, lut and masked rows at these offsets inside it
+  int u_tbase, u_tstride, u_off_a, u_off_pfx, u_off_lut, u_off_btab;
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
   int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it
@@ -181,7 +184,7 @@ cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 // (before_search, if set, is recorded on st between the prep and the search kernel)
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search);
 int search_u_max_blocks_per_sm(const SearchArgs &a);
-bool utables_fit(int n_chunks, int Ka, int lut_n, int btab_floats, int n_groups_u);
+constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
 int search_max_blocks_per_sm(const SearchArgs &a);

@@ -1,36 +1,40 @@
-// Uniform-register variant of the search (k_uprep + k_search_u), for single-target searches with
-// short b rows (C4-like).  The per-search tables — prefix-chunk partial sums, a-options, the
-// remaining-budget -> masked-row lookup and the masked rows — live in the constant bank, and the
-// search kernel runs one warp per block with a blockIdx-derived (uniform) item schedule, so for
-// the warp groups whose 32 lane tiles share one unit sum the masked-row index is warp-uniform:
+// Uniform-register variant of the search (k_uprep + k_search_u), for searches with short b rows
+// (C4-like) and up to 8 targets per launch.  The per-target tables — prefix-chunk partial sums,
+// a-options, the remaining-budget -> masked-row lookup and the masked rows — live in the constant
+// bank, and the search kernel runs one warp per block with item tickets broadcast by redux.sync, so
+// for the warp groups whose 32 lane tiles share one unit sum the masked-row index is warp-uniform:
 // ptxas loads the b values with LDCU into uniform registers and FADD2 reads them from there
-// (tools/microbench/pipes6: 92 vs 80 candidates/clk/SM).  Mixed groups read their lanes' rows
-// with ordinary (divergent) constant loads.  Same arithmetic, same keys and counts as k_search.
+// (tools/microbench/pipes6: 92 vs 80 candidates/clk/SM).  Mixed groups read their lanes' rows from
+// shared-memory copies.  Same arithmetic, same keys and counts as k_search.
 #include "alp_search.cuh"
 
 #include <mutex>
 
 namespace alp {
 
-constexpr int kUChunks = 1024, kUA = 64, kULut = 1024, kUBtab = 4096, kUGroups = 1024;
-struct UTables {
-  float2 pfx[kUChunks];   // {canonical prefix partial sum, bits(prefix units)} per chunk
-  int gsum[kUGroups];     // unit sum of each uniform warp group
-  float4 a[kUA];          // {tau_a, bits(u_a), bits(feasible), 0}
-  int2 lut[kULut];        // lut[lut_base - U] = {masked-row float offset, #finite entries}
-  float btab[kUBtab];     // masked rows
+__constant__ __align__(16) unsigned char cu_mem[kUBytes];  // tables (layout: SearchArgs u_*)
+
+// typed views of a target's block of the tables (constant bank or its global staging copy)
+struct UView {
+  const unsigned char *t;
+  const SearchArgs &P;
+  __device__ __forceinline__ const float4 &a(int i) const { return reinterpret_cast<const float4 *>(t + P.u_off_a)[i]; }
+  __device__ __forceinline__ const float2 &pfx(uint32_t c) const {
+    return reinterpret_cast<const float2 *>(t + P.u_off_pfx)[c];
+  }
+  __device__ __forceinline__ const int2 &lut(int x) const { return reinterpret_cast<const int2 *>(t + P.u_off_lut)[x]; }
+  __device__ __forceinline__ const float *btab() const { return reinterpret_cast<const float *>(t + P.u_off_btab); }
 };
-__constant__ UTables cu;
 
 // ------------------------------------------------------------------ prep: one block
 // Option terms of the (single) target into global (finalize inputs) and shared memory, then the
 // constant-bank tables written through the symbol's global address (the constant cache is
 // refilled at the next kernel launch).
-__global__ void k_uprep(const __grid_constant__ SearchArgs P, UTables *T) {
-  extern __shared__ __align__(16) float s_t[];  // [M*K] option terms, then the staged plan tables
-  const int MK = P.M * P.K, K = P.K, tid = threadIdx.x, nt = blockDim.x;
+__global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) {
+  extern __shared__ __align__(16) float s_t[];  // [n_t][M*K] option terms, then the staged plan tables
+  const int MK = P.M * P.K, K = P.K, tid = threadIdx.x, nt = blockDim.x, NT = P.n_targets;
   const int R = P.budget, D = P.D, Kb = P.Kb;
-  float *s_bs = s_t + MK;                                   // [Kb] u-sorted b terms
+  float *s_bs = s_t + NT * MK;                              // [Kb] u-sorted b terms (per target, reused)
   int *s_dv = reinterpret_cast<int *>(s_bs + Kb);           // [D]
   int *s_len = s_dv + D;                                    // [D+1] masked-row lengths (dcnt)
   int *s_fin = s_len + (D + 1);                             // [D+1] finite entries per row
@@ -44,59 +48,69 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, UTables *T) {
   for (int i = tid; i < P.g0 * K; i += nt) cp_async4(s_u + i, P.u + i);
   if (P.a_llm >= 0)
     for (int i = tid; i < P.Ka; i += nt) cp_async4(s_ua + i, P.u + P.a_llm * K + i);
-  for (uint32_t g = tid; g < P.n_groups_u; g += nt) T->gsum[g] = P.gsum[g];
-  for (int i = tid; i < MK; i += nt) {
+  for (uint32_t g = tid; g < P.n_groups_u; g += nt) reinterpret_cast<int *>(T)[g] = P.gsum[g];
+  for (int i = tid; i < NT * MK; i += nt) {
+    const int t = i / MK, j = i % MK;
     float tau;
     double term, b;
     int u;
-    option_terms(P.fz.prof, P.fz.tgt[0], i / K, i % K, &tau, &term, &b, &u);
+    option_terms(P.fz.prof, P.fz.tgt[t], j / K, j % K, &tau, &term, &b, &u);
     s_t[i] = tau;
     P.fz.o_tau[i] = tau;
     P.fz.o_term[i] = term;
     P.fz.o_b[i] = b;
   }
   cp_async_wait();
-  __syncthreads();
-  // prefix chunks: canonical sum over LLMs 0..g0-1
-  for (uint32_t c = tid; c < P.n_chunks; c += nt) {
-    float pa = 0.f;
-    int U = 0;
-    for (int m = 0; m < P.g0; ++m) {
-      const uint32_t d = (c / P.pw[m]) % (uint32_t)K;
-      pa = __fadd_rn(pa, s_t[m * K + d]);
-      U += s_u[m * K + d];
-    }
-    T->pfx[c] = make_float2(pa, __int_as_float(U));
-  }
-  for (int a = tid; a < P.Ka; a += nt) {
-    const float ta = P.a_llm >= 0 ? s_t[P.a_llm * K + a] : 0.f;
-    const int ua = P.a_llm >= 0 ? s_ua[a] : 0;
-    const int feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
-    T->a[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), 0.f);
-  }
-  // masked rows: row i holds the u-sorted b columns with u <= dv[i-1] (row 0 none), +inf elsewhere
-  for (int j = tid; j < Kb; j += nt) s_bs[j] = s_t[P.b_llm * K + s_bp[j]];
   for (int i = tid; i <= D; i += nt) s_len[i] = min(s_len[i], Kb);
   __syncthreads();
-  for (int row = tid; row <= D; row += nt) {
-    int f = 0;
-    for (int j = 0; j < s_len[row]; ++j) f += (s_bs[j] < __int_as_float(0x7f800000)) ? 1 : 0;
-    s_fin[row] = f;
-  }
-  for (int i = tid; i < (D + 1) * P.bchunk_wpad; i += nt) {
-    const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
-    T->btab[row * P.row_stride + j] = (j < s_len[row]) ? s_bs[j] : __int_as_float(0x7f800000);
-  }
-  __syncthreads();
-  // lut: index x <-> remaining budget r = R - lut_base + x; row = #{distinct b unit values <= r}
-  for (int x = tid; x < P.lut_n; x += nt) {
-    const int r = R - P.lut_base + x;
-    int lo = 0, hi = D;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
+  for (int t = 0; t < NT; ++t) {
+    const float *st = s_t + t * MK;
+    unsigned char *tb = T + P.u_tbase + t * P.u_tstride;
+    float2 *pfx = reinterpret_cast<float2 *>(tb + P.u_off_pfx);
+    float4 *ta4 = reinterpret_cast<float4 *>(tb + P.u_off_a);
+    int2 *lut = reinterpret_cast<int2 *>(tb + P.u_off_lut);
+    float *btab = reinterpret_cast<float *>(tb + P.u_off_btab);
+    // prefix chunks: canonical sum over LLMs 0..g0-1
+    for (uint32_t c = tid; c < P.n_chunks; c += nt) {
+      float pa = 0.f;
+      int U = 0;
+      for (int m = 0; m < P.g0; ++m) {
+        const uint32_t d = (c / P.pw[m]) % (uint32_t)K;
+        pa = __fadd_rn(pa, st[m * K + d]);
+        U += s_u[m * K + d];
+      }
+      pfx[c] = make_float2(pa, __int_as_float(U));
     }
-    T->lut[x] = make_int2(lo * P.row_stride, s_fin[lo]);
+    for (int a = tid; a < P.Ka; a += nt) {
+      const float ta = P.a_llm >= 0 ? st[P.a_llm * K + a] : 0.f;
+      const int ua = P.a_llm >= 0 ? s_ua[a] : 0;
+      const int feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
+      ta4[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), 0.f);
+    }
+    // masked rows: row i holds the u-sorted b columns with u <= dv[i-1] (row 0 none), +inf elsewhere
+    for (int j = tid; j < Kb; j += nt) s_bs[j] = st[P.b_llm * K + s_bp[j]];
+    __syncthreads();
+    for (int row = tid; row <= D; row += nt) {
+      int f = 0;
+      for (int j = 0; j < s_len[row]; ++j) f += (s_bs[j] < __int_as_float(0x7f800000)) ? 1 : 0;
+      s_fin[row] = f;
+    }
+    for (int i = tid; i < (D + 1) * P.bchunk_wpad; i += nt) {
+      const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
+      btab[row * P.row_stride + j] = (j < s_len[row]) ? s_bs[j] : __int_as_float(0x7f800000);
+    }
+    __syncthreads();
+    // lut: index x <-> remaining budget r = R - lut_base + x; row = #{distinct b unit values <= r}
+    for (int x = tid; x < P.lut_n; x += nt) {
+      const int r = R - P.lut_base + x;
+      int lo = 0, hi = D;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
+      }
+      lut[x] = make_int2(lo * P.row_stride, s_fin[lo]);
+    }
+    __syncthreads();  // s_bs / s_fin reused by the next target
   }
 }
 
@@ -118,108 +132,113 @@ __device__ __forceinline__ void eval_row_u(const float *rb, const float (&Qa)[12
 
 // ------------------------------------------------------------------ search: one warp per block
 template <int NB4, bool TAIL2>
-__global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchArgs P, const UTables *ug) {
+__global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchArgs P, const unsigned char *ug) {
   constexpr int T = 12;
   extern __shared__ __align__(16) unsigned char smem[];
-  // [g1*K + 2] terms of LLMs 0..g1-1 then {0, +inf} | lut [lut_n] int2 | masked rows
+  // per target [g1*K + 2] terms of LLMs 0..g1-1 then {0, +inf}, all targets copied up front: any
+  // lane-divergent code inside the target loop makes ptxas give up the uniform datapath there
+  const int tw = P.g1 * P.K + 2;
   float *s_tau = reinterpret_cast<float *>(smem);
-  int2 *s_lut = reinterpret_cast<int2 *>(smem + P.off_lut);
-  float *s_btab = reinterpret_cast<float *>(smem + P.off_btab);
   const int lane = threadIdx.x;
-  pdl_wait();
-  for (int i = lane; i < P.g1 * P.K; i += 32) s_tau[i] = __ldcg(P.tau + i);
-  if (lane == 0) {
-    s_tau[P.g1 * P.K] = 0.f;
-    s_tau[P.g1 * P.K + 1] = __int_as_float(0x7f800000);
-  }
-  // shared-memory copies of the lut and masked rows for the mixed groups (lane-varying rows)
-  for (int i = lane; i < P.lut_n; i += 32) s_lut[i] = __ldcg(&ug->lut[i]);
-  for (int i = lane; i < (P.D + 1) * P.row_stride; i += 32) s_btab[i] = __ldcg(&ug->btab[i]);
-  __syncwarp();
-  const unsigned char *tau_b = smem;
-  float best = __int_as_float(0x7f800000);
-  uint32_t best_seg = 0xffffffffu;
-  unsigned long long cnt = 0ull;
-  float Qr[T], acc[T];
   const uint32_t n = (uint32_t)(P.item_hi - P.item_lo);
-  // dynamic item tickets: lane 0 takes the next ticket while the current item is evaluated;
-  // redux.sync broadcasts it into a uniform register (ptxas keeps the derived indices uniform)
-  unsigned long long *ctr = P.work;
-  unsigned tnext = 0xffffffffu;
-  if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
-  for (;;) {
-    const uint32_t k = __reduce_min_sync(0xffffffffu, tnext);
-    if (k >= n) break;
+  const int *gsum = reinterpret_cast<const int *>(cu_mem);
+  pdl_wait();
+  for (int i = lane; i < P.n_targets * tw; i += 32) {
+    const int t = i / tw, j = i % tw;
+    s_tau[i] = j < tw - 2 ? __ldcg(P.tau + (size_t)t * P.M * P.K + j) : (j == tw - 2 ? 0.f : __int_as_float(0x7f800000));
+  }
+  __syncwarp();
+  for (int t = 0; t < P.n_targets; ++t) {  // target phases: the warp moves on when the tickets run out
+    const UView cv{cu_mem + P.u_tbase + t * P.u_tstride, P};
+    const UView gv{ug + P.u_tbase + t * P.u_tstride, P};
+    const unsigned char *tau_b = smem + (size_t)t * tw * 4;
+    float best = __int_as_float(0x7f800000);
+    uint32_t best_seg = 0xffffffffu;
+    unsigned long long cnt = 0ull;
+    float Qr[T], acc[T];
+    // dynamic item tickets: lane 0 takes the next ticket while the current item is evaluated;
+    // redux.sync broadcasts it into a uniform register (ptxas keeps the derived indices uniform)
+    unsigned long long *ctr = P.work + t;
+    unsigned tnext = 0xffffffffu;
     if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
-    const uint32_t it = (uint32_t)P.item_lo + k;
-    const uint32_t tq = fdiv(it, P.fd_nQ);
-    const uint32_t q = it - tq * P.nQ;           // a-range of the row
-    const uint32_t chunk = fdiv(tq, P.fd_ng);
-    const uint32_t grp = tq - chunk * P.n_groups;
-    const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
-    const float2 pf = cu.pfx[chunk];
-    const int upfx = __float_as_int(pf.y);
-    const uint32_t tile = grp * kWarpTiles + lane;
-    const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
-    unsigned nfin = 0;
+    for (;;) {
+      const uint32_t k = __reduce_min_sync(0xffffffffu, tnext);
+      if (k >= n) break;
+      if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
+      const uint32_t it = (uint32_t)P.item_lo + k;
+      const uint32_t tq = fdiv(it, P.fd_nQ);
+      const uint32_t q = it - tq * P.nQ;           // a-range of the row
+      const uint32_t chunk = fdiv(tq, P.fd_ng);
+      const uint32_t grp = tq - chunk * P.n_groups;
+      const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
+      const float2 pf = cv.pfx(chunk);
+      const int upfx = __float_as_int(pf.y);
+      const uint32_t tile = grp * kWarpTiles + lane;
+      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
+      unsigned nfin = 0;
 #pragma unroll
-    for (int v = 0; v < T; ++v) {
-      const uint4 o = __ldg(op + v);
-      float qv = pf.x;
-      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
-      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
-      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
-      qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
-      Qr[v] = qv;
-      nfin += (qv < __int_as_float(0x7f800000)) ? 1u : 0u;
-      acc[v] = __int_as_float(0x7f800000);
-    }
-    unsigned c32 = 0;
-    if (grp < P.n_groups_u) {
-      // warp-uniform remaining budget: uniform-register b operands
-      const int xg = P.lut_base - upfx - cu.gsum[grp];
-#pragma unroll 2
-      for (int a = a0; a < a1; ++a) {
-        const float4 av = cu.a[a];
-        const int2 lu = cu.lut[xg - __float_as_int(av.y)];
-        c32 += (unsigned)(lu.y * __float_as_int(av.z));
-        float Qa[T];
-#pragma unroll
-        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-        eval_row_u<NB4, TAIL2>(cu.btab + lu.x, Qa, acc);
+      for (int v = 0; v < T; ++v) {
+        const uint4 o = __ldg(op + v);
+        float qv = pf.x;
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
+        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
+        Qr[v] = qv;
+        nfin += (qv < __int_as_float(0x7f800000)) ? 1u : 0u;
+        acc[v] = __int_as_float(0x7f800000);
       }
-    } else {
-      // mixed group: the lanes' own remaining budgets, rows from the shared-memory copies
-      const int xl = P.lut_base - upfx - __ldg(P.tile_s + tile);
-      const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
+      unsigned c32 = 0;
+      if (grp < P.n_groups_u) {
+        // warp-uniform remaining budget: uniform-register b operands
+        const int xg = P.lut_base - upfx - gsum[grp];
 #pragma unroll 2
-      for (int a = a0; a < a1; ++a) {
-        const float4 av = cu.a[a];
-        const int2 lu = s_lut[xl - __float_as_int(av.y)];
-        c32 += (unsigned)(lu.y * __float_as_int(av.z));
-        float Qa[T];
+        for (int a = a0; a < a1; ++a) {
+          const float4 av = cv.a(a);
+          const int2 lu = cv.lut(xg - __float_as_int(av.y));
+          c32 += (unsigned)(lu.y * __float_as_int(av.z));
+          float Qa[T];
 #pragma unroll
-        for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-        eval_row<T, NB4, TAIL2>(bbase + 4u * (uint32_t)lu.x, Qa, acc, 0);
+          for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+          eval_row_u<NB4, TAIL2>(cv.btab() + lu.x, Qa, acc);
+        }
+      } else {
+        // mixed group: the lanes' own remaining budgets, rows from the global staging copy of the
+        // tables (L1-resident; a different memory space keeps the compiler from merging this loop
+        // with the uniform one into a single vector loop)
+        const int xl = P.lut_base - upfx - __ldg(P.tile_s + tile);
+#pragma unroll 2
+        for (int a = a0; a < a1; ++a) {
+          const float4 av = cv.a(a);
+          const int2 lu = __ldg(&gv.lut(xl - __float_as_int(av.y)));
+          c32 += (unsigned)(lu.y * __float_as_int(av.z));
+          float Qa[T];
+#pragma unroll
+          for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+          const float *rb = gv.btab() + lu.x;
+#pragma unroll
+          for (int g = 0; g < NB4; ++g) eval4<T>(__ldg(reinterpret_cast<const float4 *>(rb) + g), Qa, acc);
+          if constexpr (TAIL2) eval2<T>(__ldg(reinterpret_cast<const float2 *>(rb + 4 * NB4)), Qa, acc);
+        }
       }
+      cnt += (unsigned long long)c32 * nfin;
+      fold_rows<T>(P, acc, tile, chunk, q, best, best_seg);  // segment: from a-range q to the row's end
     }
-    cnt += (unsigned long long)c32 * nfin;
-    fold_rows<T>(P, acc, tile, chunk, q, best, best_seg);  // segment: from a-range q to the row's end
+    unsigned long long key = (best < __int_as_float(0x7f800000))
+                                 ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+      const unsigned long long oc = __shfl_xor_sync(0xffffffffu, cnt, o);
+      key = ok < key ? ok : key;
+      cnt += oc;
+    }
+    if (lane == 0) {
+      if (key != kKeyNone) atomicMin(P.fz.acc_keys + t, key);
+      if (cnt) atomicAdd(P.fz.acc_counts + t, cnt);
+    }
   }
   pdl_trigger();
-  unsigned long long key = (best < __int_as_float(0x7f800000)) ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg
-                                                               : kKeyNone;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
-    const unsigned long long oc = __shfl_xor_sync(0xffffffffu, cnt, o);
-    key = ok < key ? ok : key;
-    cnt += oc;
-  }
-  if (lane == 0) {
-    if (key != kKeyNone) atomicMin(P.fz.acc_keys, key);
-    if (cnt) atomicAdd(P.fz.acc_counts, cnt);
-  }
   fused_epilogue(P, nullptr);
 }
 
@@ -228,7 +247,7 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
 // constant bank; the mixed groups' shared-memory copies read it) and the ordering event that keeps
 // concurrent searches on other streams from overwriting the constant bank in use.
 struct UState {
-  UTables *staging = nullptr;
+  unsigned char *staging = nullptr;
   cudaEvent_t done = nullptr;
 };
 static std::mutex g_u_mu;
@@ -238,7 +257,7 @@ static UState &ustate() {
   cudaGetDevice(&dev);
   UState &u = s[dev & 63];
   if (!u.staging) {
-    cudaMalloc(reinterpret_cast<void **>(&u.staging), sizeof(UTables));
+    cudaMalloc(reinterpret_cast<void **>(&u.staging), kUBytes);
     cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming);
   }
   return u;
@@ -252,7 +271,7 @@ static cudaError_t launch_u(const SearchArgs &a, int grid, cudaStream_t st) {
   cfg.blockDim = dim3(32);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = st;
-  const UTables *ug = ustate().staging;
+  const unsigned char *ug = ustate().staging;
   return cudaLaunchKernelEx(&cfg, k_search_u<NB4, TAIL2>, a, ug);
 }
 
@@ -275,15 +294,19 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
   std::lock_guard<std::mutex> lock(g_u_mu);
   UState &u = ustate();
   if (!u.staging) return cudaErrorMemoryAllocation;
-  const int MK = a.M * a.K;
-  const int threads = MK >= 512 ? 1024 : (MK >= 256 ? 512 : 256);
+  const int MK = a.M * a.K, NTM = a.n_targets * MK;
+  const int threads = NTM >= 512 ? 1024 : (NTM >= 256 ? 512 : 256);
   cudaError_t e = cudaStreamWaitEvent(st, u.done, 0);  // the previous search using the constant bank
   if (e != cudaSuccess) return e;
-  const size_t prep_smem = (size_t)(MK + a.Kb) * 4 + (size_t)(3 * a.D + 2 + a.Kb + a.g0 * a.K + a.Ka) * 4;
+  const size_t prep_smem = (size_t)(NTM + a.Kb) * 4 + (size_t)(3 * a.D + 2 + a.Kb + a.g0 * a.K + a.Ka) * 4;
+  if (prep_smem > 48 * 1024) {
+    static std::once_flag f;
+    std::call_once(f, [] { cudaFuncSetAttribute(k_uprep, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+  }
   k_uprep<<<1, threads, prep_smem, st>>>(a, u.staging);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbolAsync(cu, u.staging, sizeof(UTables), 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-    return e;
+  const size_t used = (size_t)a.u_tbase + (size_t)a.n_targets * a.u_tstride;
+  if ((e = cudaMemcpyToSymbolAsync(cu_mem, u.staging, used, 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
   if (before_search && (e = cudaEventRecord(before_search, st)) != cudaSuccess) return e;
   if ((e = launch_u_search(a, grid, st)) != cudaSuccess) return e;
   return cudaEventRecord(u.done, st);
@@ -295,8 +318,5 @@ int search_u_max_blocks_per_sm(const SearchArgs &a) {
 #undef CALL
 }
 
-bool utables_fit(int n_chunks, int Ka, int lut_n, int btab_floats, int n_groups_u) {
-  return n_chunks <= kUChunks && Ka <= kUA && lut_n <= kULut && btab_floats <= kUBtab && n_groups_u <= kUGroups;
-}
 
 }  // namespace alp
