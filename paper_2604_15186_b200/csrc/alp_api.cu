@@ -928,8 +928,17 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   ua.u_off_btab = a16(ua.u_off_lut + ua.lut_n * 8);
   ua.u_tstride = a16(ua.u_off_btab + rows * a.row_stride * 4);
   if ((long long)ua.u_tbase + (long long)n * ua.u_tstride > kUBytes) return false;
-  // shared memory: the option terms of LLMs 0..g1-1 (+ {0, +inf}) of every target
-  ua.smem_bytes = a16(n * (h->g1 * h->K + 2) * 4);
+  // shared memory: the option terms of LLMs 0..g1-1 (+ {0, +inf}) of every target; for a single
+  // target also copies of its lut and masked rows (the mixed groups read them from there)
+  int off = a16(n * (h->g1 * h->K + 2) * 4);
+  ua.off_lut = off;
+  ua.off_btab = off;
+  if (n == 1) {
+    off = a16(off + ua.lut_n * 8);
+    ua.off_btab = off;
+    off = a16(off + rows * a.row_stride * 4);
+  }
+  ua.smem_bytes = off;
   const long long okey = (1ll << 60) | ((long long)ua.smem_bytes << 8) | ua.bchunk_wpad;
   auto oit = h->occ_cache.find(okey);
   const int bps = (oit != h->occ_cache.end()) ? oit->second : (h->occ_cache[okey] = search_u_max_blocks_per_sm(ua));

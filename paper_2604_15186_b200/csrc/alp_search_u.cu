@@ -147,6 +147,15 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
     const int t = i / tw, j = i % tw;
     s_tau[i] = j < tw - 2 ? __ldcg(P.tau + (size_t)t * P.M * P.K + j) : (j == tw - 2 ? 0.f : __int_as_float(0x7f800000));
   }
+  // single target: shared-memory copies of the lut and masked rows for the mixed groups
+  int2 *s_lut = reinterpret_cast<int2 *>(smem + P.off_lut);
+  float *s_btab = reinterpret_cast<float *>(smem + P.off_btab);
+  const bool smem_rows = P.n_targets == 1;
+  if (smem_rows) {
+    const UView gv0{ug + P.u_tbase, P};
+    for (int i = lane; i < P.lut_n; i += 32) s_lut[i] = __ldcg(&gv0.lut(i));
+    for (int i = lane; i < (P.D + 1) * P.row_stride; i += 32) s_btab[i] = __ldcg(gv0.btab() + i);
+  }
   __syncwarp();
   for (int t = 0; t < P.n_targets; ++t) {  // target phases: the warp moves on when the tickets run out
     const UView cv{cu_mem + P.u_tbase + t * P.u_tstride, P};
@@ -207,6 +216,19 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
         // tables (L1-resident; a different memory space keeps the compiler from merging this loop
         // with the uniform one into a single vector loop)
         const int xl = P.lut_base - upfx - __ldg(P.tile_s + tile);
+        if (smem_rows) {
+          const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
+#pragma unroll 2
+          for (int a = a0; a < a1; ++a) {
+            const float4 av = cv.a(a);
+            const int2 lu = s_lut[xl - __float_as_int(av.y)];
+            c32 += (unsigned)(lu.y * __float_as_int(av.z));
+            float Qa[T];
+#pragma unroll
+            for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
+            eval_row<T, NB4, TAIL2>(bbase + 4u * (uint32_t)lu.x, Qa, acc, 0);
+          }
+        } else
 #pragma unroll 2
         for (int a = a0; a < a1; ++a) {
           const float4 av = cv.a(a);
