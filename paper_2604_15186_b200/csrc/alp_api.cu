@@ -949,18 +949,34 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   return true;
 }
 
+// Targets per uniform-register launch for a large batch (0: the path does not apply): the most
+// (<= kInlineTargets) whose tables fit the constant bank.
+int ur_batch_group(alp_s *h, int64_t budget) {
+  if (getenv("ALP_NO_UR") || getenv("ALP_NO_FUSED")) return 0;
+  for (int g = kInlineTargets; g >= 1; g /= 2) {
+    if (!use_fused(h, g, nullptr)) continue;
+    Geometry geo;
+    if (make_geometry(h, g, budget, 0, 0, geo, true) != ALP_OK) return 0;
+    SearchArgs ua;
+    int grid = 0;
+    const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
+    if (ur_path(h, geo.a, g, items, ua, grid)) return g;
+  }
+  return 0;
+}
+
 // K2 over work items [lo, hi) (classic: after K1; fused: alone, finalize optional).  Writes the
 // per-target (key, count) of this shard to keys/counts; async on st.
 alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
                              uint64_t lo, uint64_t hi, cudaStream_t st, unsigned long long *keys,
                              unsigned long long *counts, bool fuse_finalize = false,
-                             alp_result *fused_out = nullptr) {
+                             alp_result *fused_out = nullptr, bool first_of_batch = true) {
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
   s = use_stream(h, st);
   if (s != ALP_OK) return s;
-  CU(cudaEventRecord(h->evs0, st));
+  if (first_of_batch) CU(cudaEventRecord(h->evs0, st));  // step start (a batch of launches: the first)
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   s = prepare_budgets(h, budgets, n, st, &budget);
@@ -1013,7 +1029,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   g.a.counts = counts;
   fill_finalize(h, g.a);
   if (fused_out) g.a.fin.out = fused_out;
-  CU(cudaEventRecord(h->ev0, st));
+  if (first_of_batch) CU(cudaEventRecord(h->ev0, st));
   if (hi > lo || fused) {  // the fused launch also computes the terms and writes keys/counts
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
     g.a.work = work;
@@ -1034,7 +1050,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     int ugrid = 0;
     if (fused && ur_path(h, g.a, n, hi, ua, ugrid)) {  // option terms + tables, then the UR search
       // the kernel-time events bracket the search kernel itself (ev0 re-recorded after the prep)
-      CU(launch_search_u(ua, ugrid, st, h->ev0));
+      CU(launch_search_u(ua, ugrid, st, first_of_batch ? h->ev0 : nullptr));
       launches += 2;
       h->last_ur = true;
     } else {
@@ -1071,15 +1087,33 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
 // ~5-10 us); nullptr when n results do not fit or mapping is unavailable.
 alp_result *zero_copy_out(int n, alp_result **host) {
   *host = nullptr;
-  if (n * sizeof(alp_result) > kPinHalf) return nullptr;
-  auto *pin = static_cast<unsigned char *>(pinned_scratch(2 * kPinHalf));
-  if (!pin) return nullptr;
-  alp_result *hres = reinterpret_cast<alp_result *>(pin + kPinHalf), *dres = nullptr;
-  if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&dres), hres, 0) != cudaSuccess) {
+  struct Buf {
+    alp_result *p = nullptr;
+    size_t n = 0;
+    ~Buf() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Buf b;  // mapped pinned results, grown on demand (per host thread)
+  if ((size_t)n > b.n) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    const size_t want = std::max<size_t>((size_t)n, 128);
+    if (cudaHostAlloc(reinterpret_cast<void **>(&b.p), want * sizeof(alp_result),
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+      cudaGetLastError();
+      b.p = nullptr;
+      return nullptr;
+    }
+    b.n = want;
+  }
+  alp_result *dres = nullptr;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&dres), b.p, 0) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  *host = hres;
+  *host = b.p;
   return dres;
 }
 
@@ -1408,6 +1442,23 @@ static alp_status search_queries(alp_t *h, const double *targets, const int64_t 
   s = ensure_scratch(h, n);
   if (s != ALP_OK) return s;
   const uint64_t items = alp_num_items(h, budget_units);
+  const int ug = budgets ? 0 : ur_batch_group(h, budget_units);
+  if (n > kInlineTargets && ug > 0) {
+    // large batches (C5) on the uniform-register path: groups of ug targets, each one k_uprep +
+    // k_search_u pair with the finalize fused; the results land zero-copy, one sync at the end
+    alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);
+    if (!zc) return fail(ALP_ECUDA, "no mapped pinned memory for %d results", n);
+    int launches = 0;
+    for (int i = 0; i < n; i += ug) {
+      const int g = std::min(ug, n - i);
+      s = search_shard_impl(h, targets + i, nullptr, g, budget_units, 0, items, h->stream, h->s_keys, h->s_counts,
+                            true, zc + i, i == 0);
+      if (s != ALP_OK) return s;
+      launches += h->last_launches;
+    }
+    h->last_launches = launches;
+    return collect_results(h, n, h->stream, out, hzc);
+  }
   if (use_fused(h, n, budgets)) {  // one launch: terms + search + finalize
     alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);  // the last block stores the results
     s = search_shard_impl(h, targets, nullptr, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts, true,
