@@ -187,9 +187,11 @@ alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int
                                  const int64_t *d_gathered, int32_t world, void *stream, alp_result *out);
 
 /* Device time (ms) of the last search kernel launched through this handle (CUDA events on the
- * launching stream), and the number of kernels the last search/finalize launched.  Searches of at
- * most 8 targets with a common budget run as ONE kernel (option terms, exhaustive search and
- * finalize fused); larger batches and per-query budgets run K1 + K2 + K3. */
+ * launching stream), and the number of kernels the last search/finalize launched.  Searches with
+ * short b rows and a common budget run the uniform-register pair (option terms + constant-bank
+ * tables, then the search with the finalize fused; batches in groups of 8 targets); other searches
+ * of at most 8 targets with a common budget run as ONE kernel (option terms, exhaustive search and
+ * finalize fused); the rest run K1 + K2 + K3. */
 float alp_last_kernel_ms(const alp_t *h);
 int32_t alp_last_launches(const alp_t *h);
 /* Device time (ms) of the last complete search step through this handle: CUDA events on the
