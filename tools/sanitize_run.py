@@ -53,6 +53,10 @@ print("gathered", alp.finalize_gathered(lam, B, g.data_ptr(), 3)[0].index)
 tau = (np.arange(24, dtype=np.float32).reshape(3, 8) % 5 + 1) / 8
 u = (np.arange(24, dtype=np.int32).reshape(3, 8) % 3)
 print("terms", P.Alp.from_terms(tau, u).search(1.0, 4).index)
+# uniform-register path: a batch of 12 targets on the hand case (groups of 8 + 4)
+d = generate.load("hand")
+alp = P.Alp.from_instance(d)
+print("ur batch", [r.index for r in alp.search_batch([0.125 * (i + 1) for i in range(12)], d["budget_units"])])
 if os.environ.get("SANITIZE_C4"):
     d = generate.load("C4")
     r = P.Alp.from_instance(d).search(d["targets"][0], d["budget_units"])
