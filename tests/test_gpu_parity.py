@@ -592,3 +592,18 @@ def test_uniform_register_path_concurrent_streams(P):
         rB = B.finalize(lb, dB["budget_units"], kB.data_ptr(), kB.data_ptr() + 8, sB.cuda_stream)[0]
         assert (rA.index, rA.feasible_count, rA.latency_key) == (refA.index, refA.feasible_count, refA.latency_key)
         assert (rB.index, rB.feasible_count, rB.latency_key) == (refB.index, refB.feasible_count, refB.latency_key)
+
+
+def test_uniform_register_batch_groups_vs_oracle(P):
+    """A 12-target batch runs as uniform-register groups of 8 + 4 (results zero-copy, one sync);
+    every target against the brute-force oracle, including infeasible ones."""
+    d = generate.load("hand")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lams = [0.125 * (i + 1) for i in range(10)] + [4.0, 5.0]
+    res = alp.search_batch(lams, I.budget)
+    assert alp.last_path == "k_search_u" and alp.last_launches == 4
+    for lam, r in zip(lams, res):
+        o = oracle.search(I, lam, I.budget)
+        _same(r, o.found, o.latency_key, o.index, o.count, lam)
+        _check_winner(P, alp, I, lam, I.budget, r)
