@@ -264,6 +264,30 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
   }
 }
 
+// Load a lane tile: the canonical partial sums Q_row = (((P + tau_g0) + ...) of its T rows from the
+// chunk prefix P and the sort-group terms in shared memory (4 byte offsets per row, in LLM order;
+// unused digits point at 0.0f, padded rows at +inf); resets the row minima.  Returns the number of
+// rows with a finite partial sum.
+template <int T>
+__device__ __forceinline__ unsigned load_tile(const SearchArgs &P, const unsigned char *tau_b, float pfx,
+                                              uint32_t tile, float (&Qr)[T], float (&acc)[T]) {
+  const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
+  unsigned nfin = 0;
+#pragma unroll
+  for (int v = 0; v < T; ++v) {
+    const uint4 o = __ldg(op + v);
+    float qv = pfx;
+    qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
+    qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
+    qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
+    qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
+    Qr[v] = qv;
+    nfin += (qv < finf()) ? 1u : 0u;
+    acc[v] = finf();
+  }
+  return nfin;
+}
+
 template <int T, int NB4, bool TAIL2>
 __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char *base, float &best,
                               uint32_t &best_seg, unsigned long long &cnt, int R, int work_slot) {
@@ -325,22 +349,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
       const uint32_t tile = grp * kWarpTiles + lane;
       const int stile = __ldg(P.tile_s + tile);
-      // per row: 4 smem byte offsets of the sort-group terms, in LLM order; unused digits point
-      // at 0.0f, padded rows at +inf
-      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
-      nfin = 0;
-#pragma unroll
-      for (int v = 0; v < T; ++v) {
-        const uint4 o = __ldg(op + v);
-        float qv = Pfx;
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
-        Qr[v] = qv;
-        nfin += (qv < finf()) ? 1u : 0u;
-        acc[v] = finf();
-      }
+      nfin = load_tile<T>(P, tau_b, Pfx, tile, Qr, acc);
       r_tile = R - Upfx - stile;
       q0 = q;
       tchunk = chunk;

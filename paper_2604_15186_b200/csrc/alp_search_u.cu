@@ -183,20 +183,7 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       const float2 pf = cv.pfx(chunk);
       const int upfx = __float_as_int(pf.y);
       const uint32_t tile = grp * kWarpTiles + lane;
-      const uint4 *op = reinterpret_cast<const uint4 *>(P.tile_off) + (size_t)tile * T;
-      unsigned nfin = 0;
-#pragma unroll
-      for (int v = 0; v < T; ++v) {
-        const uint4 o = __ldg(op + v);
-        float qv = pf.x;
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.x));
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.y));
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.z));
-        qv = __fadd_rn(qv, *reinterpret_cast<const float *>(tau_b + o.w));
-        Qr[v] = qv;
-        nfin += (qv < __int_as_float(0x7f800000)) ? 1u : 0u;
-        acc[v] = __int_as_float(0x7f800000);
-      }
+      const unsigned nfin = load_tile<T>(P, tau_b, pf.x, tile, Qr, acc);
       unsigned c32 = 0;
       if (grp < P.n_groups_u) {
         // warp-uniform remaining budget: uniform-register b operands
