@@ -607,3 +607,20 @@ def test_uniform_register_batch_groups_vs_oracle(P):
         o = oracle.search(I, lam, I.budget)
         _same(r, o.found, o.latency_key, o.index, o.count, lam)
         _check_winner(P, alp, I, lam, I.budget, r)
+
+
+@pytest.mark.parametrize("B", [0, 1, 9, 64, 255, 256, 10_000])
+def test_c4_budgets_vs_dp(P, B):
+    """The headline instance on the uniform-register path across budgets: empty (0), tiny, binding,
+    at and above the total of the per-LLM maxima (the cap), against the DP oracle (O2)."""
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (d["targets"][0], d["targets"][0] * 3.9):
+        r = alp.search(lam, B)
+        assert alp.last_path == "k_search_u"
+        tab = oracle.option_table(I, lam)
+        f, v, idx, cnt = dp.search(tab["tau"], tab["u"], min(B, int(tab["u"].max(axis=1).sum())))
+        _same(r, f, v, idx, cnt, (B, lam))
+        if r.found:
+            _check_winner(P, alp, I, lam, B, r)
