@@ -309,6 +309,9 @@ def run_ours(args):
                                 "cold = first build after alp_plan_cache_clear (adds host planning + plan upload)"},
             "gpu_launches": launches,
             "clocks": cs,
+            "env": {"device": torch.cuda.get_device_name(dev), "sm_count": sm_count,
+                    "cuda": torch.version.cuda, "torch": torch.__version__, "host_cores": os.cpu_count(),
+                    "search_kernel": alp.last_path},
         }
         if world == 1 and not args.no_cpu_baseline:
             v, cores, sample, _dt, full = oracle_rate(d, seconds=args.cpu_seconds)

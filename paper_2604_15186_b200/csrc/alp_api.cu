@@ -22,12 +22,19 @@
 #include <vector>
 
 #include "alp_internal.h"
+#include "nvtx3/nvToolsExt.h"  // header-only NVTX v3: ranges for nsys timelines (no-ops without a tool)
 
 using namespace alp;
 
 namespace {
 
 thread_local std::string g_err = "no error";
+
+// NVTX range for the duration of a scope (alp_build / search / finalize phases in nsys)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 constexpr size_t kPinnedStageMax = 256 * 1024;  // larger arena uploads skip the pinned staging buffer
 constexpr size_t kArenaWork = 64;  // work counters kept in the handle arena (phases of one search)
 // fused-launch work counters: <= kInlineTargets targets x <= 16 b-chunks (b columns are split in
@@ -1189,6 +1196,7 @@ extern "C" {
 const char *alp_last_error(void) { return g_err.c_str(); }
 
 alp_status alp_build(const alp_desc *d, alp_t **out) {
+  NvtxRange nv("alp_build");
   if (!out) return fail(ALP_EINVAL, "out is NULL");
   *out = nullptr;
   if (!d) return fail(ALP_EINVAL, "desc is NULL");
@@ -1403,6 +1411,7 @@ alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, i
 
 alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
                             uint64_t hi, void *stream, int64_t *d_keys, int64_t *d_counts) {
+  NvtxRange nv("alp_search_shard");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
   return search_shard_impl(h, targets, nullptr, n, budget_units, lo, hi, stream ? (cudaStream_t)stream : h->stream,
@@ -1412,6 +1421,7 @@ alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t 
 
 alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budget_units, const int64_t *d_keys,
                         const int64_t *d_counts, void *stream, alp_result *out) {
+  NvtxRange nv("alp_finalize");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
   alp_status s = check_targets(targets, n);
@@ -1423,6 +1433,7 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
 
 alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
                                  const int64_t *d_gathered, int32_t world, void *stream, alp_result *out) {
+  NvtxRange nv("alp_finalize_gathered");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_gathered) return fail(ALP_EINVAL, "d_gathered is NULL");
   if (world < 1) return fail(ALP_EINVAL, "world must be >= 1");
@@ -1434,6 +1445,7 @@ alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int
 
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
                                  int64_t budget_units, alp_result *out) {
+  NvtxRange nv("alp_search");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!out) return fail(ALP_EINVAL, "out is NULL");
   alp_status s = check_targets(targets, n);
