@@ -8,7 +8,9 @@
 // shared-memory copies.  Same arithmetic, same keys and counts as k_search.
 #include "alp_search.cuh"
 
+#include <cstring>
 #include <mutex>
+#include <vector>
 
 namespace alp {
 
@@ -255,9 +257,28 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
 // Per-device staging copy of the tables (k_uprep writes it; one D2D copy moves it into the
 // constant bank; the mixed groups' shared-memory copies read it) and the ordering event that keeps
 // concurrent searches on other streams from overwriting the constant bank in use.
+// The prep → constant-bank copy → search sequence is replayed as one CUDA graph (instantiated once
+// per launch shape, kernel arguments updated in place when they change): one host submission
+// instead of four, so the device runs the three nodes back to back instead of waiting for the
+// host's launch calls (measured: tools/step_timeline.py; C4 step 0.505 -> 0.501 ms). The
+// kernel-time event between the copy and the search is a graph node too; it alone leaves a ~5 us
+// bubble before the search (0.1 us without it), the price of timing the search kernel with events.
+struct UGraph {
+  const void *fn = nullptr;  // search kernel instantiation
+  int grid = 0, threads = 0;
+  size_t prep_smem = 0, used = 0;
+  bool ev = false;  // has the kernel-time event record node
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t n_prep = nullptr, n_search = nullptr, n_ev = nullptr;
+  cudaEvent_t ev_set = nullptr;  // event the record node currently targets
+  SearchArgs last;               // arguments the kernel nodes currently hold
+};
 struct UState {
   unsigned char *staging = nullptr;
   cudaEvent_t done = nullptr;
+  cudaStream_t cap = nullptr;  // capture stream
+  std::vector<UGraph> graphs;
 };
 static std::mutex g_u_mu;
 static UState &ustate() {
@@ -270,6 +291,11 @@ static UState &ustate() {
     cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming);
   }
   return u;
+}
+
+template <int NB4, bool TAIL2>
+static const void *fn_u() {
+  return reinterpret_cast<const void *>(k_search_u<NB4, TAIL2>);
 }
 
 template <int NB4, bool TAIL2>
@@ -299,6 +325,79 @@ static cudaError_t launch_u_search(const SearchArgs &a, int grid, cudaStream_t s
 #undef CALL
 }
 
+static const void *search_u_fn(const SearchArgs &a) {
+#define CALL(T_, N, T2) fn_u<N, T2>()
+  ALP_DISPATCH_W(CALL, 12);
+#undef CALL
+}
+
+// Kernel-node arguments of the cached graph, rewritten only when they differ from the last launch.
+static cudaError_t set_node_args(UGraph &gr, const SearchArgs &a, unsigned char *staging, cudaEvent_t ev) {
+  cudaError_t e;
+  if (std::memcmp(&gr.last, &a, sizeof(SearchArgs)) != 0) {
+    for (cudaGraphNode_t n : {gr.n_prep, gr.n_search}) {
+      cudaKernelNodeParams kp;
+      if ((e = cudaGraphKernelNodeGetParams(n, &kp)) != cudaSuccess) return e;
+      void *args[2] = {const_cast<SearchArgs *>(&a), &staging};
+      kp.kernelParams = args;
+      kp.extra = nullptr;
+      if ((e = cudaGraphExecKernelNodeSetParams(gr.exec, n, &kp)) != cudaSuccess) return e;
+    }
+    std::memcpy(&gr.last, &a, sizeof(SearchArgs));
+  }
+  if (gr.ev && ev != gr.ev_set) {
+    if ((e = cudaGraphExecEventRecordNodeSetEvent(gr.exec, gr.n_ev, ev)) != cudaSuccess) return e;
+    gr.ev_set = ev;
+  }
+  return cudaSuccess;
+}
+
+// Capture prep → copy → [event] → search once on the capture stream and instantiate it.
+static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int grid, cudaEvent_t ev) {
+  cudaError_t e;
+  if (!u.cap && (e = cudaStreamCreateWithFlags(&u.cap, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaStreamBeginCapture(u.cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
+  k_uprep<<<1, gr.threads, gr.prep_smem, u.cap>>>(a, u.staging);
+  cudaError_t ec = cudaGetLastError();
+  if (ec == cudaSuccess) ec = cudaMemcpyToSymbolAsync(cu_mem, u.staging, gr.used, 0, cudaMemcpyDeviceToDevice, u.cap);
+  if (ec == cudaSuccess && ev) ec = cudaEventRecordWithFlags(ev, u.cap, cudaEventRecordExternal);
+  if (ec == cudaSuccess) ec = launch_u_search(a, grid, u.cap);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(u.cap, &g);
+  if (ec != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return ec;
+  }
+  if (e != cudaSuccess) return e;
+  size_t nn = 0;
+  if ((e = cudaGraphGetNodes(g, nullptr, &nn)) != cudaSuccess) return e;
+  std::vector<cudaGraphNode_t> nodes(nn);
+  if ((e = cudaGraphGetNodes(g, nodes.data(), &nn)) != cudaSuccess) return e;
+  for (cudaGraphNode_t n : nodes) {
+    cudaGraphNodeType t;
+    if ((e = cudaGraphNodeGetType(n, &t)) != cudaSuccess) return e;
+    if (t == cudaGraphNodeTypeKernel) {
+      cudaKernelNodeParams kp;
+      if ((e = cudaGraphKernelNodeGetParams(n, &kp)) != cudaSuccess) return e;
+      (kp.func == reinterpret_cast<void *>(k_uprep) ? gr.n_prep : gr.n_search) = n;
+    } else if (t == cudaGraphNodeTypeEventRecord) {
+      gr.n_ev = n;
+    }
+  }
+  if (!gr.n_prep || !gr.n_search || (ev && !gr.n_ev)) {
+    cudaGraphDestroy(g);
+    return cudaErrorInvalidValue;
+  }
+  if ((e = cudaGraphInstantiate(&gr.exec, g, 0)) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return e;
+  }
+  gr.g = g;
+  gr.ev_set = ev;
+  std::memcpy(&gr.last, &a, sizeof(SearchArgs));
+  return cudaSuccess;
+}
+
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search) {
   std::lock_guard<std::mutex> lock(g_u_mu);
   UState &u = ustate();
@@ -312,9 +411,36 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
     static std::once_flag f;
     std::call_once(f, [] { cudaFuncSetAttribute(k_uprep, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
   }
+  const size_t used = (size_t)a.u_tbase + (size_t)a.n_targets * a.u_tstride;
+  static const bool no_graph = getenv("ALP_U_NOGRAPH") != nullptr;  // per-call launches (comparison)
+  if (!no_graph) {
+    const void *fn = search_u_fn(a);
+    const bool ev = before_search != nullptr;
+    UGraph *gr = nullptr;
+    for (UGraph &x : u.graphs)
+      if (x.fn == fn && x.grid == grid && x.threads == threads && x.prep_smem == prep_smem && x.used == used &&
+          x.ev == ev)
+        gr = &x;
+    if (!gr) {
+      if (u.graphs.size() >= 16) {  // many launch shapes (tests, shard sweeps): start over
+        for (UGraph &x : u.graphs) {
+          cudaGraphExecDestroy(x.exec);
+          cudaGraphDestroy(x.g);
+        }
+        u.graphs.clear();
+      }
+      UGraph x;
+      x.fn = fn; x.grid = grid; x.threads = threads; x.prep_smem = prep_smem; x.used = used; x.ev = ev;
+      if ((e = build_graph(x, u, a, grid, before_search)) != cudaSuccess) return e;
+      u.graphs.push_back(x);
+      gr = &u.graphs.back();
+    }
+    if ((e = set_node_args(*gr, a, u.staging, before_search)) != cudaSuccess) return e;
+    if ((e = cudaGraphLaunch(gr->exec, st)) != cudaSuccess) return e;
+    return cudaEventRecord(u.done, st);
+  }
   k_uprep<<<1, threads, prep_smem, st>>>(a, u.staging);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const size_t used = (size_t)a.u_tbase + (size_t)a.n_targets * a.u_tstride;
   if ((e = cudaMemcpyToSymbolAsync(cu_mem, u.staging, used, 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
   if (before_search && (e = cudaEventRecord(before_search, st)) != cudaSuccess) return e;
   if ((e = launch_u_search(a, grid, st)) != cudaSuccess) return e;

@@ -60,6 +60,13 @@ def main():
         print(f"{s - t0:9.1f} us  +{s - prev_end:7.1f} gap  {en - s:8.1f} us  {e.name[:90]}")
         prev_end = en
     print(f"step span {step_ev[-1].time_range.end - t0:.1f} us")
+    # host side of the same step: runtime API calls (CUPTI), same clock as the device events
+    api = [e for e in prof.events() if e.device_type.name == "CPU" and e.name.startswith("cuda")
+           and e.time_range.start >= step_ev[0].time_range.start - 200]
+    api.sort(key=lambda e: e.time_range.start)
+    for e in api[:40]:
+        s, en = e.time_range.start, e.time_range.end
+        print(f"  host {s - t0:9.1f} us  {en - s:7.1f} us  {e.name[:60]}")
 
 
 if __name__ == "__main__":
