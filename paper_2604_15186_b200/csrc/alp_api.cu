@@ -1048,14 +1048,16 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     g.a.grab2 = std::max(1, g.a.grab / 4);
     g.a.grab_t1 = (n_items - n_items / 8) / (uint64_t)g.a.grab;
     static const bool dbg = getenv("ALP_DBG_TS") != nullptr;  // per-block timeline (diagnostics)
-    if (dbg) {
-      CU(h->g_dbg.ensure((size_t)g.grid * 8));
-      CU(cudaMemsetAsync(h->g_dbg.p, 0, (size_t)g.grid * 8 * sizeof(unsigned long long), st));
-      g.a.dbg_ts = h->g_dbg.p;
-    }
     SearchArgs ua;
     int ugrid = 0;
-    if (fused && ur_path(h, g.a, n, hi, ua, ugrid)) {  // option terms + tables, then the UR search
+    const bool ur = fused && ur_path(h, g.a, n, hi, ua, ugrid);
+    const int dgrid = ur ? ugrid : g.grid;
+    if (dbg) {
+      CU(h->g_dbg.ensure((size_t)dgrid * 8));
+      CU(cudaMemsetAsync(h->g_dbg.p, 0, (size_t)dgrid * 8 * sizeof(unsigned long long), st));
+      g.a.dbg_ts = ua.dbg_ts = h->g_dbg.p;
+    }
+    if (ur) {  // option terms + tables, then the UR search
       // the kernel-time events bracket the search kernel itself (ev0 re-recorded after the prep)
       CU(launch_search_u(ua, ugrid, st, first_of_batch ? h->ev0 : nullptr));
       launches += 2;
@@ -1066,18 +1068,18 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
       h->last_ur = false;
     }
     if (dbg) {
-      std::vector<unsigned long long> ts((size_t)g.grid * 8);
+      std::vector<unsigned long long> ts((size_t)dgrid * 8);
       CU(cudaMemcpyAsync(ts.data(), h->g_dbg.p, ts.size() * 8, cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
       unsigned long long t0 = ~0ull;
-      for (int b = 0; b < g.grid; ++b) t0 = std::min(t0, ts[b * 8]);
+      for (int b = 0; b < dgrid; ++b) t0 = std::min(t0, ts[b * 8]);
       std::vector<double> v[5];
-      for (int b = 0; b < g.grid; ++b)
+      for (int b = 0; b < dgrid; ++b)
         for (int i = 0; i < 5; ++i) v[i].push_back(ts[b * 8 + i] ? (ts[b * 8 + i] - t0) * 1e-3 : 0.0);
       for (auto &x : v) std::sort(x.begin(), x.end());
       auto q = [&](int i, double f) { return v[i][(size_t)(f * (v[i].size() - 1))]; };
       fprintf(stderr, "[alp dbg] grid %d us: start med %.1f max %.1f | terms med %.1f max %.1f | tables med %.1f "
-              "max %.1f | loop-end min %.1f med %.1f max %.1f | end max %.1f\n", g.grid, q(0, .5), q(0, 1), q(4, .5),
+              "max %.1f | loop-end min %.1f med %.1f max %.1f | end max %.1f\n", dgrid, q(0, .5), q(0, 1), q(4, .5),
               q(4, 1), q(1, .5), q(1, 1), q(2, 0), q(2, .5), q(2, 1), q(3, 1));
     }
   }

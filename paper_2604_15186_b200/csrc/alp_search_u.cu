@@ -144,10 +144,21 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
   const int lane = threadIdx.x;
   const uint32_t n = (uint32_t)(P.item_hi - P.item_lo);
   const int *gsum = reinterpret_cast<const int *>(cu_mem);
+  auto stamp = [&](int i) {  // ALP_DBG_TS per-block timeline (outside the target loop only)
+    if (P.dbg_ts && lane == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      P.dbg_ts[blockIdx.x * 8 + i] = g;
+    }
+  };
+  stamp(0);
   pdl_wait();
+  // every block reads the same few lines at launch: L1-allocating loads (ld.global.ca) so one miss
+  // per SM goes to L2 — L2-only loads from all 3552 warps cost ~7.5 us per block (ALP_DBG_TS).
+  // (__ldg or cp.async here change the search loop's register allocation: 2 % slower, measured)
   for (int i = lane; i < P.n_targets * tw; i += 32) {
     const int t = i / tw, j = i % tw;
-    s_tau[i] = j < tw - 2 ? __ldcg(P.tau + (size_t)t * P.M * P.K + j) : (j == tw - 2 ? 0.f : __int_as_float(0x7f800000));
+    s_tau[i] = j < tw - 2 ? __ldca(P.tau + (size_t)t * P.M * P.K + j) : (j == tw - 2 ? 0.f : __int_as_float(0x7f800000));
   }
   // single target: shared-memory copies of the lut and masked rows for the mixed groups
   int2 *s_lut = reinterpret_cast<int2 *>(smem + P.off_lut);
@@ -155,10 +166,15 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
   const bool smem_rows = P.n_targets == 1;
   if (smem_rows) {
     const UView gv0{ug + P.u_tbase, P};
-    for (int i = lane; i < P.lut_n; i += 32) s_lut[i] = __ldcg(&gv0.lut(i));
-    for (int i = lane; i < (P.D + 1) * P.row_stride; i += 32) s_btab[i] = __ldcg(gv0.btab() + i);
+    const int *lut_w = reinterpret_cast<const int *>(&gv0.lut(0));
+    int *s_lut_w = reinterpret_cast<int *>(s_lut);
+    for (int i = lane; i < 2 * P.lut_n; i += 32) s_lut_w[i] = __ldca(lut_w + i);
+    for (int i = lane; i < (P.D + 1) * P.row_stride; i += 32) s_btab[i] = __ldca(gv0.btab() + i);
   }
+  cp_async_wait();
   __syncwarp();
+  stamp(4);
+  stamp(1);
   for (int t = 0; t < P.n_targets; ++t) {  // target phases: the warp moves on when the tickets run out
     const UView cv{cu_mem + P.u_tbase + t * P.u_tstride, P};
     const UView gv{ug + P.u_tbase + t * P.u_tstride, P};
@@ -249,8 +265,10 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       if (cnt) atomicAdd(P.fz.acc_counts + t, cnt);
     }
   }
+  stamp(2);
   pdl_trigger();
   fused_epilogue(P, nullptr);
+  stamp(3);
 }
 
 // ------------------------------------------------------------------ launch

@@ -130,6 +130,26 @@ def test_full_size_vs_dp(P, name):
         assert ok and l32 == r.latency_key
 
 
+def test_uniform_register_graph_replay_interleaved(P):
+    """The uniform-register prep/copy/search sequence is replayed as a cached CUDA graph whose
+    kernel arguments are rewritten when they change: two handles of the same shape (one graph)
+    interleaved, target and budget changing on every call, each result against the DP oracle."""
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    A, B = P.Alp.from_instance(d), P.Alp.from_instance(d)
+    lam0 = d["targets"][0]
+    tabs = {}
+    for i, (h, lam, bud) in enumerate([(A, lam0, I.budget), (B, lam0 * 0.5, I.budget), (A, lam0 * 0.5, I.budget - 7),
+                                        (B, lam0, I.budget - 7), (A, lam0, I.budget), (A, lam0 * 1.7, I.budget),
+                                        (B, lam0 * 1.7, I.budget - 7)]):
+        r = h.search(lam, bud)
+        assert h.last_path == "k_search_u" and h.last_kernel_ms > 0
+        if lam not in tabs:
+            tabs[lam] = oracle.option_table(I, lam)
+        f, v, idx, cnt = dp.search(tabs[lam]["tau"], tabs[lam]["u"], bud)
+        _same(r, f, v, idx, cnt, (i, lam, bud))
+
+
 def test_c4_window_bruteforce(P):
     # exhaustive O1 around the optimum: no candidate in a 2e7-wide canonical window beats it
     d = generate.load("C4")
