@@ -324,6 +324,7 @@ struct alp_s {
     d.n = d_n; d.p = d_p; d.S = d_S; d.T = d_T; d.R = d_R; d.prof_off = d_off;
     d.rate = d_rate; d.lat = d_lat; d.tmax = d_tmax;
     d.min_units = min_units.empty() ? nullptr : d_minu;
+    d.n_pts = (int)rate.size();
     return d;
   }
 
@@ -935,6 +936,7 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   ua.u_off_btab = a16(ua.u_off_lut + ua.lut_n * 8);
   ua.u_tstride = a16(ua.u_off_btab + rows * a.row_stride * 4);
   if ((long long)ua.u_tbase + (long long)n * ua.u_tstride > kUBytes) return false;
+  if (uprep_smem_bytes(ua) > kUPrepSmemMax) return false;
   // shared memory: the option terms of LLMs 0..g1-1 (+ {0, +inf}) of every target; for a single
   // target also copies of its lut and masked rows (the mixed groups read them from there)
   int off = a16(n * (h->g1 * h->K + 2) * 4);
@@ -1081,6 +1083,10 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
       fprintf(stderr, "[alp dbg] grid %d us: start med %.1f max %.1f | terms med %.1f max %.1f | tables med %.1f "
               "max %.1f | loop-end min %.1f med %.1f max %.1f | end max %.1f\n", dgrid, q(0, .5), q(0, 1), q(4, .5),
               q(4, 1), q(1, .5), q(1, 1), q(2, 0), q(2, .5), q(2, 1), q(3, 1));
+      if (ur && ts[5])  // k_uprep phases (us from its start; the search's t0 is later)
+        fprintf(stderr, "[alp dbg] k_uprep us: terms %.2f | plan tables landed %.2f | end %.2f | search t0 %+.2f\n",
+                (ts[6] - ts[5]) * 1e-3, (ts[7] - ts[5]) * 1e-3, (ts[13] - ts[5]) * 1e-3,
+                ((double)t0 - (double)ts[5]) * 1e-3);
     }
   }
   CU(cudaEventRecord(h->ev1, st));

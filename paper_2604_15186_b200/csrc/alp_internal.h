@@ -38,6 +38,7 @@ struct DevProfiles {
   const int *prof_off;
   const double *rate, *lat, *tmax;
   const int *min_units;  // nullptr = no floor
+  int n_pts;             // profile points (rate / lat length)
 };
 
 // Option-term kernel (K1) arguments.
@@ -184,6 +185,8 @@ cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 // (before_search, if set, is recorded on st between the prep and the search kernel)
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search);
 int search_u_max_blocks_per_sm(const SearchArgs &a);
+size_t uprep_smem_bytes(const SearchArgs &a);  // k_uprep dynamic shared memory (<= kUPrepSmemMax)
+constexpr size_t kUPrepSmemMax = 200 * 1024;
 constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);

@@ -28,6 +28,11 @@ struct UView {
   __device__ __forceinline__ const float *btab() const { return reinterpret_cast<const float *>(t + P.u_off_btab); }
 };
 
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
 // ------------------------------------------------------------------ prep: one block
 // Option terms of the (single) target into global (finalize inputs) and shared memory, then the
 // constant-bank tables written through the symbol's global address (the constant cache is
@@ -43,7 +48,47 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   int *s_bp = s_fin + (D + 1);                              // [Kb] bperm
   int *s_u = s_bp + Kb;                                     // [g0*K] prefix units
   int *s_ua = s_u + P.g0 * K;                               // [Ka] a units
-  // static plan tables first (cp.async: in flight while the FP64 option terms are computed)
+  auto stamp = [&](int slot) {  // ALP_DBG_TS: slots 5-7 of blocks 0 and 1 (k_search_u uses 0-4)
+    if (P.dbg_ts && tid == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      P.dbg_ts[slot] = g;
+    }
+  };
+  stamp(5);
+  // the profile tables in shared memory (one wave of cp.async; the lookups' dependent loads then hit
+  // shared memory instead of L2/DRAM)
+  const DevProfiles &gp = P.fz.prof;
+  const int MT = gp.M * gp.nT;
+  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_ua + P.Ka) + 7) & ~uintptr_t(7));
+  DevProfiles sp = gp;
+  {
+    double *d = s_pd;
+    auto stage_d = [&](const double *src, int n) {
+      for (int i = tid; i < n; i += nt) cp_async8(d + i, src + i);
+      const double *r = d;
+      d += n;
+      return r;
+    };
+    sp.n = stage_d(gp.n, gp.M);
+    sp.p = stage_d(gp.p, gp.M);
+    sp.tmax = stage_d(gp.tmax, MT);
+    sp.rate = stage_d(gp.rate, gp.n_pts);
+    sp.lat = stage_d(gp.lat, gp.n_pts);
+    int *w = reinterpret_cast<int *>(d);
+    auto stage_i = [&](const int *src, int n) {
+      for (int i = tid; i < n; i += nt) cp_async4(w + i, src + i);
+      const int *r = w;
+      w += n;
+      return r;
+    };
+    sp.S = stage_i(gp.S, gp.nS);
+    sp.T = stage_i(gp.T, gp.nT);
+    sp.R = stage_i(gp.R, gp.nR);
+    sp.prof_off = stage_i(gp.prof_off, MT + 1);
+    if (gp.min_units) sp.min_units = stage_i(gp.min_units, MT);
+  }
+  // static plan tables (cp.async: in flight with the profile tables)
   for (int i = tid; i < D; i += nt) cp_async4(s_dv + i, P.dv + i);
   for (int i = tid; i <= D; i += nt) cp_async4(s_len + i, P.dcnt + i);
   for (int i = tid; i < Kb; i += nt) cp_async4(s_bp + i, P.bperm + i);
@@ -51,20 +96,23 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   if (P.a_llm >= 0)
     for (int i = tid; i < P.Ka; i += nt) cp_async4(s_ua + i, P.u + P.a_llm * K + i);
   for (uint32_t g = tid; g < P.n_groups_u; g += nt) reinterpret_cast<int *>(T)[g] = P.gsum[g];
+  cp_async_wait();
+  __syncthreads();
   for (int i = tid; i < NT * MK; i += nt) {
     const int t = i / MK, j = i % MK;
     float tau;
     double term, b;
     int u;
-    option_terms(P.fz.prof, P.fz.tgt[t], j / K, j % K, &tau, &term, &b, &u);
+    option_terms(sp, P.fz.tgt[t], j / K, j % K, &tau, &term, &b, &u);
     s_t[i] = tau;
     P.fz.o_tau[i] = tau;
     P.fz.o_term[i] = term;
     P.fz.o_b[i] = b;
   }
-  cp_async_wait();
+  stamp(6);
   for (int i = tid; i <= D; i += nt) s_len[i] = min(s_len[i], Kb);
   __syncthreads();
+  stamp(7);
   for (int t = 0; t < NT; ++t) {
     const float *st = s_t + t * MK;
     unsigned char *tb = T + P.u_tbase + t * P.u_tstride;
@@ -114,6 +162,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     }
     __syncthreads();  // s_bs / s_fin reused by the next target
   }
+  stamp(8 + 5);
 }
 
 template <int NB4, bool TAIL2>
@@ -416,6 +465,14 @@ static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int g
   return cudaSuccess;
 }
 
+size_t uprep_smem_bytes(const SearchArgs &a) {
+  const DevProfiles &pr = a.fz.prof;
+  const int MT = pr.M * pr.nT;
+  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(3 * a.D + 2 + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
+         (size_t)(2 * pr.M + MT + 2 * pr.n_pts) * 8 +
+         (size_t)(pr.nS + pr.nT + pr.nR + MT + 1 + (pr.min_units ? MT : 0)) * 4;
+}
+
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search) {
   std::lock_guard<std::mutex> lock(g_u_mu);
   UState &u = ustate();
@@ -424,10 +481,10 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
   const int threads = NTM >= 512 ? 1024 : (NTM >= 256 ? 512 : 256);
   cudaError_t e = cudaStreamWaitEvent(st, u.done, 0);  // the previous search using the constant bank
   if (e != cudaSuccess) return e;
-  const size_t prep_smem = (size_t)(NTM + a.Kb) * 4 + (size_t)(3 * a.D + 2 + a.Kb + a.g0 * a.K + a.Ka) * 4;
+  const size_t prep_smem = uprep_smem_bytes(a);
   if (prep_smem > 48 * 1024) {
     static std::once_flag f;
-    std::call_once(f, [] { cudaFuncSetAttribute(k_uprep, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    std::call_once(f, [] { cudaFuncSetAttribute(k_uprep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUPrepSmemMax); });
   }
   const size_t used = (size_t)a.u_tbase + (size_t)a.n_targets * a.u_tstride;
   static const bool no_graph = getenv("ALP_U_NOGRAPH") != nullptr;  // per-call launches (comparison)
