@@ -327,9 +327,8 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
 // The prep → constant-bank copy → search sequence is replayed as one CUDA graph (instantiated once
 // per launch shape, kernel arguments updated in place when they change): one host submission
 // instead of four, so the device runs the three nodes back to back instead of waiting for the
-// host's launch calls (measured: tools/step_timeline.py; C4 step 0.505 -> 0.501 ms). The
-// kernel-time event between the copy and the search is a graph node too; it alone leaves a ~5 us
-// bubble before the search (0.1 us without it), the price of timing the search kernel with events.
+// host's launch calls (measured: tools/step_timeline.py; C4 step 0.505 -> 0.498 ms, 0.1-0.2 us
+// between the nodes).
 struct UGraph {
   const void *fn = nullptr;  // search kernel instantiation
   int grid = 0, threads = 0;
@@ -344,7 +343,8 @@ struct UGraph {
 struct UState {
   unsigned char *staging = nullptr;
   cudaEvent_t done = nullptr;
-  cudaStream_t cap = nullptr;  // capture stream
+  cudaStream_t cap = nullptr, cap2 = nullptr;  // capture streams (cap2: the event branch)
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<UGraph> graphs;
 };
 static std::mutex g_u_mu;
@@ -426,9 +426,22 @@ static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int g
   if ((e = cudaStreamBeginCapture(u.cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
   k_uprep<<<1, gr.threads, gr.prep_smem, u.cap>>>(a, u.staging);
   cudaError_t ec = cudaGetLastError();
+  // The kernel-time event hangs off a side branch that starts with the table copy, so the search
+  // never waits for it: in series (copy -> event -> search) the event node alone left a ~5 us
+  // bubble before the search. Recorded when the prep is done, it brackets the copy (1.4 us) and
+  // the search: an upper bound of the search kernel's time, never an underestimate.
+  if (ev) {
+    if (ec == cudaSuccess && !u.cap2) ec = cudaStreamCreateWithFlags(&u.cap2, cudaStreamNonBlocking);
+    if (ec == cudaSuccess && !u.fork) ec = cudaEventCreateWithFlags(&u.fork, cudaEventDisableTiming);
+    if (ec == cudaSuccess && !u.join) ec = cudaEventCreateWithFlags(&u.join, cudaEventDisableTiming);
+    if (ec == cudaSuccess) ec = cudaEventRecord(u.fork, u.cap);
+    if (ec == cudaSuccess) ec = cudaStreamWaitEvent(u.cap2, u.fork, 0);
+    if (ec == cudaSuccess) ec = cudaEventRecordWithFlags(ev, u.cap2, cudaEventRecordExternal);
+    if (ec == cudaSuccess) ec = cudaEventRecord(u.join, u.cap2);
+  }
   if (ec == cudaSuccess) ec = cudaMemcpyToSymbolAsync(cu_mem, u.staging, gr.used, 0, cudaMemcpyDeviceToDevice, u.cap);
-  if (ec == cudaSuccess && ev) ec = cudaEventRecordWithFlags(ev, u.cap, cudaEventRecordExternal);
   if (ec == cudaSuccess) ec = launch_u_search(a, grid, u.cap);
+  if (ec == cudaSuccess && ev) ec = cudaStreamWaitEvent(u.cap, u.join, 0);
   cudaGraph_t g = nullptr;
   e = cudaStreamEndCapture(u.cap, &g);
   if (ec != cudaSuccess) {
