@@ -16,7 +16,7 @@ python tools/sass_blocks.py $G/sass_C4.csv --candidates 11019960576 --top 30 > p
 (echo "# fused single-GPU search (alp_search): one kernel, zero-copy result"; cat $G/timeline_C4_search.txt; echo
  echo "# shard path (alp_search_shard + alp_finalize), world 1, no all-reduce; K3 writes the result zero-copy"
  cat $G/timeline_C4_shard.txt) > profiles/${R}_step_timeline_C4.txt
-(echo "# per-block %globaltimer stamps of the search kernel (k_search_u on C4; ALP_DBG_TS=1), rank-0 shard of world 1/2/4/8; us from the first block start. k_search_u: terms = tables = after the block's shared-memory copies, loop-end = its last work item, end = after the epilogue"
+(echo "# per-block %globaltimer stamps of the search kernel (k_search_u on C4; ALP_DBG_TS=1), rank-0 shard of world 1/2/4/8; us from the first block start. k_search_u: terms = tables = after the block's shared-memory copies, loop-end = its last work item, end = after the epilogue; k_uprep lines: its phases, us from its own start (search t0 = first search block start)"
  cat $G/block_timeline_C4.txt) > profiles/${R}_block_timeline_C4.txt
 cp $G/shard_timing.jsonl profiles/${R}_shard_scaling.jsonl
 cp $G/mb_pipes5.txt profiles/${R}_microbench_pipes5.txt

@@ -15,7 +15,8 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 python tools/step_timeline.py --workload C4 --mode search > gpurun_out/timeline_C4_search.txt 2>/dev/null
 python tools/step_timeline.py --workload C4 --mode shard > gpurun_out/timeline_C4_shard.txt 2>/dev/null
 (python tools/shard_timing.py C4; python tools/shard_timing.py C3) > gpurun_out/shard_timing.jsonl 2>&1
-ALP_DBG_TS=1 python tools/shard_timing.py C4 2>&1 | grep "alp dbg" | awk 'NR%20==10' > gpurun_out/block_timeline_C4.txt
+ALP_DBG_TS=1 python tools/shard_timing.py C4 2>&1 | grep "alp dbg" > gpurun_out/dbg_all.txt
+(grep "dbg\] grid" gpurun_out/dbg_all.txt | awk 'NR%20==10'; grep "k_uprep" gpurun_out/dbg_all.txt | awk 'NR%20==10') > gpurun_out/block_timeline_C4.txt
 bash tools/multirank_check.sh > gpurun_out/multirank.txt 2>&1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pipes5 tools/microbench/pipes5.cu && /tmp/pipes5 > gpurun_out/mb_pipes5.txt 2>&1
 if [ "${NCU:-1}" = "1" ]; then
