@@ -423,6 +423,9 @@ static cudaError_t set_node_args(UGraph &gr, const SearchArgs &a, unsigned char 
 static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int grid, cudaEvent_t ev) {
   cudaError_t e;
   if (!u.cap && (e = cudaStreamCreateWithFlags(&u.cap, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if (!u.cap2 && (e = cudaStreamCreateWithFlags(&u.cap2, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if (!u.fork && (e = cudaEventCreateWithFlags(&u.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if (!u.join && (e = cudaEventCreateWithFlags(&u.join, cudaEventDisableTiming)) != cudaSuccess) return e;
   if ((e = cudaStreamBeginCapture(u.cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
   k_uprep<<<1, gr.threads, gr.prep_smem, u.cap>>>(a, u.staging);
   cudaError_t ec = cudaGetLastError();
@@ -431,9 +434,6 @@ static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int g
   // bubble before the search. Recorded when the prep is done, it brackets the copy (1.4 us) and
   // the search: an upper bound of the search kernel's time, never an underestimate.
   if (ev) {
-    if (ec == cudaSuccess && !u.cap2) ec = cudaStreamCreateWithFlags(&u.cap2, cudaStreamNonBlocking);
-    if (ec == cudaSuccess && !u.fork) ec = cudaEventCreateWithFlags(&u.fork, cudaEventDisableTiming);
-    if (ec == cudaSuccess && !u.join) ec = cudaEventCreateWithFlags(&u.join, cudaEventDisableTiming);
     if (ec == cudaSuccess) ec = cudaEventRecord(u.fork, u.cap);
     if (ec == cudaSuccess) ec = cudaStreamWaitEvent(u.cap2, u.fork, 0);
     if (ec == cudaSuccess) ec = cudaEventRecordWithFlags(ev, u.cap2, cudaEventRecordExternal);
