@@ -272,7 +272,9 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
         const int xl = P.lut_base - upfx - __ldg(P.tile_s + tile);
         if (smem_rows) {
           const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
-#pragma unroll 2
+          // not unrolled: the smaller mixed-group code leaves the instruction cache to the uniform
+          // loop (C4 0.4763 vs 0.4784 ms with unroll 2)
+#pragma unroll 1
           for (int a = a0; a < a1; ++a) {
             const float4 av = cv.a(a);
             const int2 lu = s_lut[xl - __float_as_int(av.y)];
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
             eval_row<T, NB4, TAIL2>(bbase + 4u * (uint32_t)lu.x, Qa, acc, 0);
           }
         } else
-#pragma unroll 2
+#pragma unroll 1
         for (int a = a0; a < a1; ++a) {
           const float4 av = cv.a(a);
           const int2 lu = __ldg(&gv.lut(xl - __float_as_int(av.y)));
