@@ -150,6 +150,37 @@ def test_uniform_register_graph_replay_interleaved(P):
         _same(r, f, v, idx, cnt, (i, lam, bud))
 
 
+def test_uniform_register_without_graph_matches(P):
+    """ALP_U_NOGRAPH=1 (read once per process, so in a child process) launches the prep, the
+    constant-bank copy and the search as separate stream calls: same results as the graph replay."""
+    import os
+    import subprocess
+    import sys
+    code = ("import json, paper_2604_15186_b200 as P\n"
+            "from workloads import generate\n"
+            "out = []\n"
+            "for name in ('hand', 'C4'):\n"
+            "    d = generate.load(name); a = P.Alp.from_instance(d)\n"
+            "    for f in (1.0, 0.4):\n"
+            "        r = a.search(d['targets'][0] * f, d['budget_units'])\n"
+            "        out.append([a.last_path, r.index, r.feasible_count, r.latency_key])\n"
+            "print(json.dumps(out))\n")
+    env = dict(os.environ, ALP_U_NOGRAPH="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    child = json.loads(res.stdout.strip().splitlines()[-1])
+    mine = []
+    for name in ("hand", "C4"):
+        d = generate.load(name)
+        a = P.Alp.from_instance(d)
+        for f in (1.0, 0.4):
+            r = a.search(d["targets"][0] * f, d["budget_units"])
+            mine.append([a.last_path, r.index, r.feasible_count, r.latency_key])
+    assert all(x[0] == "k_search_u" for x in mine)
+    assert child == mine
+
+
 def test_c4_window_bruteforce(P):
     # exhaustive O1 around the optimum: no candidate in a 2e7-wide canonical window beats it
     d = generate.load("C4")
