@@ -1,7 +1,8 @@
 """Randomised parity sweep of the CUDA path against the oracle (more cases than the test suite):
 seeded random instances (2-8 LLMs, 1-48 options per LLM, random budgets, memory floors on a third
-of them), three targets each; every result against the DP oracle (O2) and, when the space is small,
-the brute-force oracle (O1).  Run once per launch path:
+of them), three targets each plus one batch and one per-query-budget call of 2-19 targets; every
+result against the DP oracle (O2) and, for the single searches in small spaces, the brute-force
+oracle (O1).  Run once per launch path:
 
     python tests/sweep_parity.py [n_instances] [seed0]            # default path choice
     ALP_NO_UR=1 python tests/sweep_parity.py ...                  # fused k_search
@@ -57,6 +58,22 @@ def main():
             else:
                 bad += 1
                 print("MISMATCH", s, lam, budget, r.index, idx, r.feasible_count, cnt, flush=True)
+        # a batch (uniform-register groups of <= 8 targets) and per-query budgets, vs the DP oracle
+        lams = [float(x) for x in rng.uniform(0.01, 4.0, size=int(rng.integers(2, 20)))]
+        buds = [int(x) for x in rng.integers(0, 8 * M * 4, size=len(lams))]
+        for kind, res in (("batch", alp.search_batch(lams, budget)), ("queries", alp.search_queries(lams, buds))):
+            paths[kind] = paths.get(kind, 0) + len(lams)
+            for j, (lam, r) in enumerate(zip(lams, res)):
+                bj = budget if kind == "batch" else buds[j]
+                tab = oracle.option_table(I, lam)
+                f, v, idx, cnt = dp.search(tab["tau"], tab["u"], bj)
+                good = (r.found == f and r.feasible_count == cnt and
+                        (not f or (r.index == idx and np.float32(r.latency_key) == np.float32(v))))
+                if good:
+                    ok += 1
+                else:
+                    bad += 1
+                    print("MISMATCH", kind, s, lam, bj, r.index, idx, r.feasible_count, cnt, flush=True)
     print({"instances": n, "searches": ok + bad, "match": ok, "mismatch": bad, "also_brute_force": brute,
            "paths": paths, "env": {k: v for k, v in os.environ.items() if k.startswith("ALP_")}})
 
