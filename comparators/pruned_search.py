@@ -31,16 +31,22 @@ def count_unpruned(G: int, F: int, M: int) -> int:
 
 
 def fraction_assignments(total: int, mins: list[int]):
-    """Non-increasing compositions of `total` (LLMs already in descending-ratio order), part i >= mins[i]."""
+    """Non-increasing compositions of `total` (LLMs already in descending-ratio order), part i >= mins[i].
+
+    Ordering relaxation: when LLM i's memory minimum exceeds the previous
+    (higher-ratio) LLM's part, the ordering constraint is waived for that pair (part i is then bounded
+    only by the units left); the next LLM is still ordered against part i."""
     M = len(mins)
 
     def rec(i, left, cap):
+        waived = mins[i] > cap
         if i == M - 1:
-            if mins[i] <= left <= cap:
+            if mins[i] <= left and (left <= cap or waived):
                 yield (left,)
             return
         rest_min = sum(mins[i + 1:])
-        for u in range(min(cap, left - rest_min), mins[i] - 1, -1):
+        us = range((left - rest_min) if waived else min(cap, left - rest_min), mins[i] - 1, -1)
+        for u in us:
             for tail in rec(i + 1, left - u, u):
                 yield (u,) + tail
 

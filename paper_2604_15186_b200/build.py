@@ -15,7 +15,8 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libscepsy_alp.so")
 SOURCES = ["alp_api.cu", "alp_kernels.cu", "alp_search_t8.cu", "alp_search_t12.cu", "alp_search_t16.cu",
            "alp_search_u.cu"]
-HEADERS = ["alp_internal.h", "alp_search.cuh", os.path.join("..", "..", "include", "alp.h")]
+# every file under csrc/ (sources and headers) plus the public header is a dependency
+HEADERS = [os.path.join("..", "..", "include", "alp.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # IEEE semantics: no fast-math, no FTZ; explicit __d*_rn intrinsics in the FP64 option terms.
@@ -27,7 +28,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
+    deps = [os.path.join(CSRC, s) for s in os.listdir(CSRC)] + [os.path.join(CSRC, h) for h in HEADERS]
+    deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
 
 

@@ -150,17 +150,20 @@ struct Arena {
           return e;
         }
       }
-      // the staging buffer may still feed the previous (async) upload: wait for that copy only
-      static cudaEvent_t staged = nullptr;
-      if (staged) {
-        e = cudaEventSynchronize(staged);
-      } else {
-        e = cudaEventCreateWithFlags(&staged, cudaEventDisableTiming);
-      }
+      // the staging buffer may still feed a previous (async) upload on any device: wait for those
+      // copies only.  One event per device (an event can only be recorded on a stream of the
+      // device it was created on).
+      static cudaEvent_t staged[kMaxDevices] = {};
+      int dev = 0;
+      e = cudaGetDevice(&dev);
       if (e != cudaSuccess) return e;
+      if (dev >= kMaxDevices) return cudaErrorInvalidDevice;
+      for (cudaEvent_t ev : staged)
+        if (ev && (e = cudaEventSynchronize(ev)) != cudaSuccess) return e;
+      if (!staged[dev] && (e = cudaEventCreateWithFlags(&staged[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
       memcpy(pinned, host.data(), copied);
       e = cudaMemcpyAsync(*base, pinned, copied, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaEventRecord(staged, st);
+      if (e == cudaSuccess) e = cudaEventRecord(staged[dev], st);
     }
     h2d += copied;
     for (auto &f : fix) *f.second = static_cast<unsigned char *>(*base) + f.first;
@@ -670,8 +673,9 @@ alp_status init_device(alp_s *h) {
   CU(ctx_acquire(h->device, h->ctx));
   h->stream = h->ctx.stream;
   h->ev0 = h->ctx.ev0; h->ev1 = h->ctx.ev1; h->evs0 = h->ctx.evs0; h->evs1 = h->ctx.evs1;
-  static std::once_flag pool_once[64];
-  std::call_once(pool_once[h->device & 63], [&] {
+  if (h->device >= kMaxDevices) return fail(ALP_ECUDA, "device index %d >= %d", h->device, kMaxDevices);
+  static std::once_flag pool_once[kMaxDevices];
+  std::call_once(pool_once[h->device], [&] {
     // keep freed handle memory in the default pool so the next alp_build reuses it cheaply
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
@@ -797,13 +801,16 @@ alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st
   const bool inline_t = !h->from_terms && n <= kInlineTargets;  // targets travel in K1's parameters
   if (inline_t) {
   } else if (pin) {
-    // the pinned buffer may still feed an earlier copy (any stream): wait for that copy only
-    static thread_local cudaEvent_t pin_ev = nullptr;
-    if (!pin_ev) CU(cudaEventCreateWithFlags(&pin_ev, cudaEventDisableTiming));
-    CU(cudaEventSynchronize(pin_ev));
+    // the pinned buffer may still feed an earlier copy (any stream, any device): wait for those
+    // copies only (one event per device: events record only on their own device's streams)
+    static thread_local cudaEvent_t pin_ev[kMaxDevices] = {};
+    if (h->device >= kMaxDevices) return fail(ALP_ECUDA, "device index %d >= %d", h->device, kMaxDevices);
+    for (cudaEvent_t ev : pin_ev)
+      if (ev) CU(cudaEventSynchronize(ev));
+    if (!pin_ev[h->device]) CU(cudaEventCreateWithFlags(&pin_ev[h->device], cudaEventDisableTiming));
     memcpy(pin, targets, n * sizeof(double));
     CU(cudaMemcpyAsync(h->s_targets, pin, n * sizeof(double), cudaMemcpyHostToDevice, st));
-    CU(cudaEventRecord(pin_ev, st));
+    CU(cudaEventRecord(pin_ev[h->device], st));
   } else {
     CU(cudaMemcpyAsync(h->s_targets, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
   }
@@ -879,7 +886,7 @@ void fill_finalize(alp_s *h, SearchArgs &a) {
   FinalizeExtra &f = a.fin;
   f.term = h->s_term;
   f.b = h->s_b;
-  if (h->from_terms && a.fz.on) {
+  if (h->from_terms) {  // injected terms: the FP64 terms are the handle's fixed tables (any path)
     f.term = h->d_term_fixed;
     f.b = h->d_b_fixed;
   }

@@ -9,6 +9,7 @@
 
 namespace alp {
 
+constexpr int kMaxDevices = 64;         // per-device state arrays (events, graphs, attributes)
 constexpr int kWarpTiles = 32;           // lane tiles per warp group
 constexpr int kThreads = 256;            // threads per search block
 constexpr uint32_t kPfxTableMax = 4096;  // prefix chunks tabulated in shared memory (8 B each)
@@ -119,7 +120,7 @@ struct SearchArgs {
   const int *tile_s;     // [n_tiles] units of the lane tile's sort-group options
   const uint32_t *tile_e;// [n_tiles][T] canonical sort-group entry index (kDummy = padding)
   const uint32_t *tile_off;// [n_tiles][T][4] smem byte offsets of the row's sort-group terms
-  int rows_per_lane;     // T (8 or 16)
+  int rows_per_lane;     // T (12 by default; 8 or 16 via ALP_ROWS_PER_LANE)
   int min_blocks;        // launch-bounds variant for T = 8 (3 or 4 blocks/SM)
   int t_begin, t_end, c_begin, c_end;  // phases (target, b-chunk) evaluated by this launch
   const int *bperm;      // [Kb] canonical option of u-sorted column j

@@ -15,10 +15,10 @@
 //  * the b options are sorted by units; for a remaining budget r the feasible b options are a
 //    prefix of that order, so a shared-memory "masked row" (tau_b, or +inf when u_b > r) folds
 //    the budget test into the value.  Sort-group entries are pre-sorted (static, at build) by
-//    their unit sum so the 8 rows of a lane share one remaining budget -> one masked row.
+//    their unit sum so the T rows of a lane (T = 12 by default; 8 / 16 variants) share one remaining budget -> one masked row.
 //  * per candidate the SASS is half an FADD2 (add.rn.f32x2, binary32 RNE, scalar broadcast of
 //    Q_a) and half an FMNMX3 (3-input min): 1 issue slot per candidate, with the b values
-//    streamed by LDS.128 (4 columns x 8 rows = 32 candidates per load).
+//    streamed by LDS.128 (4 columns x T rows = 48 candidates per load at T = 12).
 //  * argmin: per-row min over the item's (a,b) block, folded into the thread's (value, segment)
 //    best with a lowest-segment tie-break; keys = bits(value)<<32 | segment; warp shuffle ->
 //    block -> atomicMin.  K3 re-scans the single winning segment for the lowest index.

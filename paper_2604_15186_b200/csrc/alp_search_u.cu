@@ -351,10 +351,10 @@ struct UState {
 };
 static std::mutex g_u_mu;
 static UState &ustate() {
-  static UState s[64];
+  static UState s[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
-  UState &u = s[dev & 63];
+  UState &u = s[dev & (kMaxDevices - 1)];
   if (!u.staging) {
     cudaMalloc(reinterpret_cast<void **>(&u.staging), kUBytes);
     cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming);
@@ -410,6 +410,7 @@ static cudaError_t set_node_args(UGraph &gr, const SearchArgs &a, unsigned char 
       void *args[2] = {const_cast<SearchArgs *>(&a), &staging};
       kp.kernelParams = args;
       kp.extra = nullptr;
+      if (n == gr.n_search) kp.sharedMemBytes = (unsigned)a.smem_bytes;  // the search's layout may differ
       if ((e = cudaGraphExecKernelNodeSetParams(gr.exec, n, &kp)) != cudaSuccess) return e;
     }
     std::memcpy(&gr.last, &a, sizeof(SearchArgs));
@@ -497,9 +498,12 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
   cudaError_t e = cudaStreamWaitEvent(st, u.done, 0);  // the previous search using the constant bank
   if (e != cudaSuccess) return e;
   const size_t prep_smem = uprep_smem_bytes(a);
-  if (prep_smem > 48 * 1024) {
-    static std::once_flag f;
-    std::call_once(f, [] { cudaFuncSetAttribute(k_uprep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUPrepSmemMax); });
+  if (prep_smem > 48 * 1024) {  // function attributes are per device: one grant per device
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    static std::once_flag f[kMaxDevices];
+    std::call_once(f[dev & (kMaxDevices - 1)],
+                   [] { cudaFuncSetAttribute(k_uprep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUPrepSmemMax); });
   }
   const size_t used = (size_t)a.u_tbase + (size_t)a.n_targets * a.u_tstride;
   static const bool no_graph = getenv("ALP_U_NOGRAPH") != nullptr;  // per-call launches (comparison)

@@ -20,6 +20,19 @@ def test_enumeration_ordering_example():
     assert list(ps.fraction_assignments(7, [1])) == [(7,)]           # single LLM: all units
 
 
+def test_ordering_relaxation_for_memory_minimums():
+    # SPEC.md:349 / :401: a lower-ratio LLM whose memory minimum exceeds the higher-ratio LLM's part
+    # waives the ordering for that pair: mins [1, 3] with 4 units -> (1, 3), which ordering alone forbids
+    assert list(ps.fraction_assignments(4, [1, 3])) == [(1, 3)]
+    # 6 units: (3, 3) is ordered; after parts 2 and 1 the minimum 3 forces the waiver -> (2, 4), (1, 5)
+    assert sorted(ps.fraction_assignments(6, [1, 3])) == [(1, 5), (2, 4), (3, 3)]
+    # mins [1, 1] never waive: the SPEC.md:347 example is unchanged
+    assert sorted(ps.fraction_assignments(4, [1, 1])) == [(2, 2), (3, 1)]
+    # the waiver is pairwise: the third LLM is still ordered against the second
+    got = list(ps.fraction_assignments(6, [1, 3, 1]))
+    assert sorted(got) == [(1, 3, 2), (1, 4, 1), (2, 3, 1)] and all(c[2] <= c[1] for c in got)
+
+
 def test_packing_example():
     # PAPER.md:392 / SPEC.md:356: 1.66 GPUs with F = 10 -> 10 units on GPU 1 and 6 on GPU 2
     (pieces, whole), = ps.pack((16,), 10)
