@@ -27,10 +27,10 @@ def reduce_keys(keys: torch.Tensor, counts: torch.Tensor, group=None) -> None:
 def gather_pairs(pairs: torch.Tensor, gathered: torch.Tensor, group=None) -> int:
     """One all-gather of this rank's int64[2n] (keys, counts) into int64[world][2n]; returns world.
     Without a process group (or world size 1) the pairs are copied through."""
-    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+    if not dist.is_available() or not dist.is_initialized():
         gathered[: pairs.numel()].copy_(pairs)
         return 1
-    world = dist.get_world_size(group)
+    world = dist.get_world_size(group)  # world 1 still runs the collective (one code path)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(gathered, pairs, group=group)
     else:  # gloo (CPU tests, several ranks on one GPU): list form

@@ -98,6 +98,61 @@ def test_hand_case_all_rows(P):
             _check_winner(P, alp, I, lam, B, r)
 
 
+# ----------------------------------------------------------------------------- percentile P
+def test_percentile_hand_case(P):
+    # PAPER.md:356 "the percentile P": each row of the golden percentile table (App. A terms x the
+    # column's factors, exact-rational winners) through the C ABI with that column selected
+    with open("tests/golden/hand_case.json") as f:
+        g = json.load(f)["percentile_searches"]
+    from fractions import Fraction
+    d = generate.load("hand")
+    for pct, lam_s, B, idx, _kg, _kv, Lw, Tw, units, feas in g["rows"]:
+        I = oracle.from_json(d, pct)
+        alp = P.Alp.from_instance(d, pct)
+        lam = float(Fraction(lam_s))
+        r = alp.search(lam, B)
+        assert (r.found, r.index, r.feasible_count, r.units) == (True, idx, feas, units), (pct, B)
+        assert r.latency == pytest.approx(float(Fraction(Lw)), rel=1e-12)
+        assert r.throughput == float(Fraction(Tw))
+        _check_winner(P, alp, I, lam, B, r)
+        alp.close()
+
+
+@pytest.mark.parametrize("pct", ["p50", "p90", "p99"])
+def test_percentile_option_tables_bitexact(P, pct):
+    # the stock C4 columns (mean x {0.8, 1.9, 3.5}) and a per-(LLM, tp) skewed column
+    for d in (generate.load("C4"), generate.skew_percentile(generate.load("C4"), pct, seed=11)):
+        I = oracle.from_json(d, pct)
+        alp = P.Alp.from_instance(d, pct)
+        for lam in (d["targets"][0], d["lambda_star"]):
+            g = alp.option_table(lam, I.K)
+            o = oracle.option_table(I, lam)
+            assert np.array_equal(g["tau"].view(np.uint32), o["tau"].view(np.uint32)), (pct, lam)
+            assert np.array_equal(g["term"][o["ok"]].view(np.uint64), o["term"][o["ok"]].view(np.uint64))
+        alp.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pct", ["p90", "p99"])
+def test_percentile_c4_vs_bruteforce(P, pct):
+    # C4 with a skewed tail column: the optimum moves away from the mean's; GPU (the column selected
+    # in alp_desc.pct) == full O1 brute force on every host core == O2
+    import os
+    d = generate.skew_percentile(generate.load("C4"), pct, seed=5)
+    I = oracle.from_json(d, pct)
+    lam = d["targets"][0]
+    alp = P.Alp.from_instance(d, pct)
+    r = alp.search(lam, I.budget)
+    o = oracle.search(I, lam, I.budget, threads=os.cpu_count() or 8)
+    _same(r, o.found, o.latency_key, o.index, o.count, pct)
+    tab = oracle.option_table(I, lam)
+    f, v, idx, cnt = dp.search(tab["tau"], tab["u"], I.budget)
+    _same(r, f, v, idx, cnt, pct)
+    _check_winner(P, alp, I, lam, I.budget, r)
+    mean = P.Alp.from_instance(d, "mean").search(lam, I.budget)
+    assert mean.index != r.index  # the selected column decides the optimum
+
+
 # ----------------------------------------------------------------------------- configs
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_full_bruteforce_small(P, name):
@@ -128,6 +183,23 @@ def test_full_size_vs_dp(P, name):
         # the winner, recomputed one by one from the profiles
         ok, l32, _ = oracle.candidate(I, lam, r.index, B)
         assert ok and l32 == r.latency_key
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_vs_bruteforce(P, name):
+    # SURVEY.md §8(c) parity contract: full C3 / C4 against O1 (literal brute force over every
+    # canonical index) on all host cores (C3: 6.9e10 candidates, ~17 s on 16 cores)
+    import os
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    lam = d["targets"][0]
+    alp = P.Alp.from_instance(d)
+    r = alp.search(lam, I.budget)
+    o = oracle.search(I, lam, I.budget, threads=os.cpu_count() or 8)
+    _same(r, o.found, o.latency_key, o.index, o.count, name)
+    assert r.candidates == I.N
+    _check_winner(P, alp, I, lam, I.budget, r)
 
 
 def test_uniform_register_graph_replay_interleaved(P):
@@ -201,10 +273,12 @@ def test_c5_target_batch(P):
     res = alp.search_batch(targets, I.budget)
     assert len(res) == 256
     prev_cnt = None
-    for j in list(range(0, 256, 17)) + [255]:
+    for j in range(256):  # every target against O2
         tab = oracle.option_table(I, targets[j])
         f, v, idx, cnt = dp.search(tab["tau"], tab["u"], I.budget)
         _same(res[j], f, v, idx, cnt, j)
+    for j in (0, 128, 255):
+        _check_winner(P, alp, I, targets[j], I.budget, res[j])
     for j in range(256):  # Pareto invariants over the sweep (exact count monotonicity)
         if prev_cnt is not None:
             assert res[j].feasible_count <= prev_cnt
@@ -281,7 +355,9 @@ def test_partition_independence(P):
     alp = P.Alp.from_instance(d)
     lam = [d["targets"][0]]
     ref = alp.search(lam[0], I.budget)
-    for world in (2, 3, 8):
+    tab = oracle.option_table(I, lam[0])
+    o2 = dp.search(tab["tau"], tab["u"], I.budget)
+    for world in (2, 3, 5, 8):
         keys = torch.empty((world, 1), dtype=torch.int64, device="cuda")
         counts = torch.empty((world, 1), dtype=torch.int64, device="cuda")
         for rank in range(world):
@@ -292,6 +368,8 @@ def test_partition_independence(P):
         c = counts.sum(dim=0).contiguous()
         r = alp.finalize(lam, I.budget, k.data_ptr(), c.data_ptr())[0]
         assert (r.index, r.feasible_count, r.latency_key) == (ref.index, ref.feasible_count, ref.latency_key)
+        _same(r, *o2, world)  # the reduced shards against the oracle directly
+        _check_winner(P, alp, I, lam[0], I.budget, r)
 
 
 def test_finalize_gathered_matches_allreduce(P):
@@ -311,9 +389,12 @@ def test_finalize_gathered_matches_allreduce(P):
             alp.search_shard(lam, I.budget, lo, hi, row.data_ptr(), row.data_ptr() + 8 * n)
             torch.cuda.synchronize()
         res = alp.finalize_gathered(lam, I.budget, gathered.data_ptr(), world)
-        for r, e in zip(res, ref):
+        for r, e, l in zip(res, ref, lam):
             assert (r.found, r.index, r.feasible_count, r.latency_key, r.units) == (e.found, e.index, e.feasible_count,
                                                                                    e.latency_key, e.units)
+            tab = oracle.option_table(I, l)
+            _same(r, *dp.search(tab["tau"], tab["u"], I.budget), (world, l))  # against the oracle directly
+            _check_winner(P, alp, I, l, I.budget, r)
 
 
 def test_infeasible_and_zero_budget(P):
@@ -559,6 +640,40 @@ def test_search_distributed_single_process(P):
     for _ in range(3):
         res = search_distributed(alp, lam, d["budget_units"])
         assert [(r.index, r.feasible_count) for r in res] == [(e.index, e.feasible_count) for e in ref]
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_nccl_search_distributed(P, world):
+    """Row A6 end to end over a real NCCL process group (torch.distributed.run, 127.0.0.1): sharded
+    search, ONE NCCL all-gather of the (key, count) pairs, the finalize kernel's MIN/SUM -- checked
+    against O2 on C4.  world 2 puts both ranks on one GPU when only one is visible; NCCL may refuse
+    that (duplicate GPU), which skips the case."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "tests/nccl_worker.py", "C4"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    if p.returncode != 0 and world > 1 and ("uplicate GPU" in p.stderr + p.stdout or "ncclInvalidUsage" in p.stderr + p.stdout):
+        pytest.skip("NCCL refuses two ranks on one GPU")
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
+    out = json.loads(line)
+    assert out["world"] == world and out["backend"] == "nccl"
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    targets = [d["targets"][0], 2.0 * d["targets"][0], 40.0 * d["targets"][0]]
+    for (found, idx, cnt, key, lat), lam in zip(out["results"], targets):
+        tab = oracle.option_table(I, lam)
+        f, v, oi, oc = dp.search(tab["tau"], tab["u"], I.budget)
+        assert (found, cnt) == (f, oc)
+        if f:
+            assert idx == oi and np.float32(key) == np.float32(v)
+            assert lat == pytest.approx(oracle.predict(I, lam, oracle.decode(I, idx))["latency"], rel=1e-6)
 
 
 def test_fused_many_b_chunks_eight_targets(P):

@@ -154,6 +154,92 @@ def test_hand_case_fp_goldens():
         assert oracle.predict(I, lam, oracle.decode(I, r.index), B)["latency"] == float(lat)
 
 
+def _hand_pct_enumeration(pct):
+    """Exact-rational winners of the hand case at a percentile column: App. A terms (golden) times the
+    column's per-tp factor, brute force over the 64 candidates (lowest index on exact ties)."""
+    from workloads.generate import HAND_PCT_FACTOR
+    rows = _gold("hand_case.json")["option_terms_lambda_1"]["rows"]
+    c = [Fraction(x).limit_denominator() for x in HAND_PCT_FACTOR[pct]]
+    fac = [c[0] if r[2] == 1 else c[1] for r in rows]  # tp 1 -> tp index 0, tp 2 -> tp index 1
+    G = [fac[k] * _F(r[5]) for k, r in enumerate(rows)]
+    V = [fac[k] * _F(r[9]) for k, r in enumerate(rows)]
+    out = {}
+    for B in (8, 16, 3):
+        best, cnt = None, 0
+        for kg, kv in itertools.product(range(8), range(8)):
+            if rows[kg][7] + rows[kv][11] <= B:
+                cnt += 1
+                L = G[kg] + V[kv]
+                if best is None or L < best[0]:
+                    best = (L, 8 * kg + kv)
+        out[B] = (best[1], best[0], cnt)
+    return G, V, out
+
+
+@pytest.mark.parametrize("pct", ["mean", "p50", "p90", "p99"])
+def test_hand_case_percentile_columns(pct):
+    # PAPER.md:356: the prediction takes "the percentile P at which latency should be evaluated".
+    # The hand instance's percentile columns are the mean column times per-tp factors; the Eq. 1
+    # term is linear in the latency column, so every option term is factor x the App. A term.
+    I = oracle.from_json(generate.load("hand"), pct)
+    G, V, _ = _hand_pct_enumeration(pct)
+    for k in range(8):
+        for m, want in ((0, G[k]), (1, V[k])):
+            o = oracle.option(I, 1.0, m, k)
+            assert o["ok"] and o["term"] == pytest.approx(float(want), rel=4e-16, abs=0), (pct, m, k)
+
+
+def test_hand_case_percentile_searches():
+    g = _gold("hand_case.json")["percentile_searches"]
+    d = generate.load("hand")
+    for pct, lam_s, B, idx, kg, kv, Lw, Tw, units, feas in g["rows"]:
+        _, _, enum = _hand_pct_enumeration(pct)
+        assert enum[B] == (idx, _F(Lw), feas), (pct, B)   # the fixture is the enumeration
+        I = oracle.from_json(d, pct)
+        lam = float(_F(lam_s))
+        r = oracle.search(I, lam, B)
+        assert r.found and r.index == idx and r.count == feas, (pct, B)
+        p = oracle.predict(I, lam, [kg, kv], B)
+        assert p["units"] == units and p["throughput"] == float(_F(Tw))
+        assert p["latency"] == pytest.approx(float(_F(Lw)), rel=1e-15)
+    # the selected column matters: p90 moves the B = 8 winner from TP (54) to replicas (45)
+    I_mean, I_p90 = oracle.from_json(d, "mean"), oracle.from_json(d, "p90")
+    assert oracle.search(I_mean, 1.0, 8).index == 54 and oracle.search(I_p90, 1.0, 8).index == 45
+
+
+# ----------------------------------------------------------------------------- lambda*
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_lambda_star_is_maximal(name):
+    # SURVEY.md §8(d): lambda* = the largest Eq. 2 value v = b_m[k] at which some candidate is
+    # feasible with target lambda = v (i.e. the largest T_w of an allocation that is feasible at its
+    # own T_w).  Pinned with the counting DP (O2, an independent algorithm): >= 1 feasible candidate
+    # at lambda*, none at the next distinct Eq. 2 value above it, nor at 2 lambda*.  Option
+    # feasibility is monotone non-increasing in lambda (x = ((lambda n)/d)/f is RNE-monotone and
+    # "x <= T", "b >= lambda" both tighten), so no larger Eq. 2 value is feasible either.  (Targets
+    # strictly between lambda* and the next Eq. 2 value can still be feasible: there the bound
+    # x <= T, evaluated in FP64, decides at the option whose b is that next value; such a target is
+    # not an Eq. 2 value of any allocation feasible at it.)
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    ls = d["lambda_star"]
+    assert ls == oracle.lambda_star(I)
+    b = np.unique(oracle.option_table(I, 1.0)["b"])
+    nxt = b[b > ls]
+    tab = oracle.option_table(I, ls)
+    assert dp.count(tab["tau"], tab["u"], I.budget) >= 1
+    above = [2.0 * ls] + ([float(nxt[0])] if nxt.size else [])
+    for lam in above:
+        tab = oracle.option_table(I, lam)
+        assert dp.count(tab["tau"], tab["u"], I.budget) == 0, (name, lam)
+    # monotonicity spot-check on a few more Eq. 2 values above lambda*
+    for lam in nxt[1:4]:
+        tab = oracle.option_table(I, float(lam))
+        assert dp.count(tab["tau"], tab["u"], I.budget) == 0, (name, lam)
+    if I.N <= 100_000:  # brute force agrees (C1, C2)
+        assert oracle.search(I, ls).count >= 1
+        assert all(oracle.search(I, lam).count == 0 for lam in above)
+
+
 # ----------------------------------------------------------------------------- closed forms
 def test_canonical_sum_order():
     # tau = [1, 2^-24, 2^-24]: ((1 + 2^-24) + 2^-24) rounds to 1 twice (ties-to-even), whereas

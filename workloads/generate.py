@@ -128,10 +128,17 @@ def make_c5() -> dict[str, Any]:
     return inst
 
 
+# Hand-case percentile columns: the mean column times a per-tp factor (tp index 0, tp index 1), so
+# every percentile's option terms are exact multiples of App. A's (tests/golden/hand_case.json
+# "percentile_searches"); p90/p99 penalise tensor parallelism, which moves the winner.
+HAND_PCT_FACTOR = {"mean": (1.0, 1.0), "p50": (0.5, 0.5), "p90": (1.0, 3.0), "p99": (2.0, 5.0)}
+
+
 def make_hand() -> dict[str, Any]:
     """F=2, S={1,2}, T={1,2}, R={1,2}; exact-rational profiles."""
-    def prof(rates, lats):
-        return {"rate": rates, "lat": {"mean": lats, "p50": lats, "p90": lats, "p99": lats}, "tmax": rates[-1]}
+    def prof(rates, lats, ti):
+        return {"rate": rates, "lat": {k: [c[ti] * x for x in lats] for k, c in HAND_PCT_FACTOR.items()},
+                "tmax": rates[-1]}
     return {
         "name": "hand", "config_id": 0, "seed": 0,
         "description": "SURVEY.md App. A two-LLM hand case (GEN n=4 p=2, VER n=2 p=1)",
@@ -139,8 +146,8 @@ def make_hand() -> dict[str, Any]:
         "n": [4.0, 2.0], "p": [2.0, 1.0],
         "llm_params": [{"name": "GEN"}, {"name": "VER"}],
         "profiles": [
-            [prof([1.0, 8.0], [0.5, 1.5]), prof([1.0, 14.0], [0.25, 1.0])],
-            [prof([1.0, 4.0], [1.0, 3.0]), prof([1.0, 7.0], [0.5, 2.0])],
+            [prof([1.0, 8.0], [0.5, 1.5], 0), prof([1.0, 14.0], [0.25, 1.0], 1)],
+            [prof([1.0, 4.0], [1.0, 3.0], 0), prof([1.0, 7.0], [0.5, 2.0], 1)],
         ],
         "min_units": None, "budget_units": 8, "percentile": "mean",
     }
@@ -174,6 +181,19 @@ def write_profiles(names=None) -> None:
         with open(path, "w") as f:
             json.dump(inst, f, indent=1)
             f.write("\n")
+
+
+def skew_percentile(d: dict[str, Any], pct: str, seed: int, lo: float = 1.0, hi: float = 4.0) -> dict[str, Any]:
+    """Copy of instance d whose `pct` latency column is the mean column times a seeded per-(LLM, tp)
+    factor in [lo, hi) (tests: a tail percentile whose shape differs from the mean's, so the optimum
+    moves when the percentile is selected)."""
+    rng = np.random.default_rng(seed)
+    out = json.loads(json.dumps(d))
+    for per_t in out["profiles"]:
+        for c in per_t:
+            f = float(rng.uniform(lo, hi))
+            c["lat"][pct] = [f * x for x in c["lat"]["mean"]]
+    return out
 
 
 # ---------------------------------------------------------------- random small instances (tests)
