@@ -19,10 +19,13 @@
  *  - Every entry point returns alp_status; on error alp_last_error() names the offending field.
  *    No C++ exception crosses this boundary.
  *  - alp_build copies every input array; the caller may free them on return.  The handle owns
- *    host copies plus device tables on the device current at build time.  A handle may be used
- *    by one host thread at a time; its calls are ordered on the device even across streams (a
- *    call on another stream waits for the handle's previous work), and alp_destroy releases
- *    device memory stream-ordered after that work (no host synchronisation).
+ *    host copies plus immutable device tables on the device current at build time.  A handle may
+ *    be used by one host thread at a time.  Calls that use the handle's own scratch are ordered on
+ *    the device even across streams (a call on another stream waits for the handle's previous
+ *    work), and alp_destroy releases device memory stream-ordered after that work.  Calls given a
+ *    caller workspace (alp_workspace_bytes; "predictions are pure and may run
+ *    concurrently") are NOT ordered against each other: searches on distinct workspaces and
+ *    streams overlap on the device; alp_destroy then synchronises the device first.
  *  - Budgets are integer GPU units (1 unit = 1/F GPU); targets are workflow requests/second.
  *  - All results are bit-identical for any rank count / grid shape (see alp_search_shard).
  */
@@ -172,19 +175,31 @@ alp_status alp_place(int32_t G, int32_t F, const int32_t *gpu_node, const int32_
 uint64_t alp_num_items(const alp_t *h, int64_t budget_units);
 alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, int32_t world, uint64_t *lo,
                            uint64_t *hi);
-/* d_keys/d_counts: device int64[n] (initialised by this call).  stream: cudaStream_t or NULL. */
+/* Bytes of a caller-owned device workspace for searches of n_targets targets (0 on a NULL handle
+ * or n_targets < 1).  A workspace holds one search's option tables, accumulators, work counters
+ * and finalize scratch.  It must be 256-byte aligned and zero-filled before its first use (e.g.
+ * torch.zeros); every call leaves its leading control section zero again, so it can be reused
+ * without re-clearing.  Give alp_finalize the workspace (and n) the shard search used. */
+size_t alp_workspace_bytes(const alp_t *h, int32_t n_targets);
+/* d_keys/d_counts: device int64[n] (initialised by this call).  d_workspace: NULL (the handle's
+ * own scratch; calls ordered across streams) or alp_workspace_bytes(h, n) caller-owned bytes (no
+ * ordering against other calls: concurrent searches on distinct workspaces / streams).
+ * stream: cudaStream_t or NULL (the handle's stream).  Asynchronous. */
 alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
-                            uint64_t hi, void *stream, int64_t *d_keys, int64_t *d_counts);
+                            uint64_t hi, void *d_workspace, void *stream, int64_t *d_keys, int64_t *d_counts);
 /* Decode reduced keys on the device (lowest index inside the winning segment, FP64 Eq. 1/Eq. 2
- * of the winner) and copy n results to the host (synchronises `stream`). */
+ * of the winner) and copy n results to the host (synchronises `stream`).  d_workspace: the one the
+ * shard search used (NULL: the handle's own). */
 alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
-                        const int64_t *d_keys, const int64_t *d_counts, void *stream, alp_result *out);
+                        const int64_t *d_keys, const int64_t *d_counts, void *d_workspace, void *stream,
+                        alp_result *out);
 /* Same, from the per-rank pairs gathered by ONE all-gather instead of two all-reduces: every rank
  * searches with d_keys = buf, d_counts = buf + n (a contiguous int64[2n] buffer), all-gathers buf
  * into d_gathered = int64[world][2][n], and the finalize kernel takes the MIN of the keys and the
  * SUM of the counts itself (the result equals alp_finalize's on the all-reduced pair). */
 alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
-                                 const int64_t *d_gathered, int32_t world, void *stream, alp_result *out);
+                                 const int64_t *d_gathered, int32_t world, void *d_workspace, void *stream,
+                                 alp_result *out);
 
 /* Device time (ms) of the last search kernel launched through this handle (CUDA events on the
  * launching stream), and the number of kernels the last search/finalize launched.  Searches with

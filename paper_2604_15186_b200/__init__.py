@@ -52,7 +52,7 @@ EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidat
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
            "alp_search_shard", "alp_finalize", "alp_finalize_gathered", "alp_last_kernel_ms", "alp_last_launches",
            "alp_last_step_ms", "alp_last_path", "alp_last_error", "alp_plan_cache_clear", "alp_search_queries",
-           "alp_schedule_egalitarian", "alp_workflow_stats", "alp_place"]
+           "alp_schedule_egalitarian", "alp_workflow_stats", "alp_place", "alp_workspace_bytes"]
 
 _lib = None
 
@@ -73,9 +73,10 @@ def lib():
             "alp_predict": (i32, [vp, vp, i32, d, i64, vp, vp, vp, vp]),
             "alp_search": (i32, [vp, d, i64, vp]), "alp_search_batch": (i32, [vp, vp, i32, i64, vp]),
             "alp_num_items": (u64, [vp, i64]), "alp_shard_range": (i32, [vp, i64, i32, i32, vp, vp]),
-            "alp_search_shard": (i32, [vp, vp, i32, i64, u64, u64, vp, vp, vp]),
-            "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp]),
-            "alp_finalize_gathered": (i32, [vp, vp, i32, i64, vp, i32, vp, vp]),
+            "alp_search_shard": (i32, [vp, vp, i32, i64, u64, u64, vp, vp, vp, vp]),
+            "alp_finalize": (i32, [vp, vp, i32, i64, vp, vp, vp, vp, vp]),
+            "alp_finalize_gathered": (i32, [vp, vp, i32, i64, vp, i32, vp, vp, vp]),
+            "alp_workspace_bytes": (ctypes.c_size_t, [vp, i32]),
             "alp_last_kernel_ms": (ctypes.c_float, [vp]), "alp_last_launches": (i32, [vp]),
             "alp_last_step_ms": (ctypes.c_float, [vp]), "alp_last_path": (i32, [vp]),
             "alp_last_error": (ctypes.c_char_p, []), "alp_plan_cache_clear": (None, []),
@@ -335,30 +336,35 @@ class Alp:
         _check(lib().alp_shard_range(self._h, budget, rank, world, ctypes.byref(lo), ctypes.byref(hi)))
         return lo.value, hi.value
 
+    def workspace_bytes(self, n_targets: int) -> int:
+        """alp_workspace_bytes: size of a caller workspace for n_targets (allocate zero-filled, e.g.
+        torch.zeros(bytes, dtype=torch.uint8, device="cuda"))."""
+        return int(lib().alp_workspace_bytes(self._h, n_targets))
+
     def search_shard(self, targets: Sequence[float], budget: int, lo: int, hi: int, keys_ptr: int, counts_ptr: int,
-                     stream_ptr: int | None = None) -> None:
-        """Async: evaluate items [lo, hi) for every target into device int64 keys/counts."""
+                     stream_ptr: int | None = None, workspace_ptr: int | None = None) -> None:
+        """Async: evaluate items [lo, hi) for every target into device int64 keys/counts (on a caller
+        workspace when workspace_ptr is given: not ordered against other calls)."""
         t = _arr(targets, np.float64)
-        _check(lib().alp_search_shard(self._h, t.ctypes.data, len(t), budget, lo, hi, _stream(stream_ptr), keys_ptr,
-                                      counts_ptr))
+        _check(lib().alp_search_shard(self._h, t.ctypes.data, len(t), budget, lo, hi, workspace_ptr,
+                                      _stream(stream_ptr), keys_ptr, counts_ptr))
 
     def finalize(self, targets: Sequence[float], budget: int, keys_ptr: int, counts_ptr: int,
-                 stream_ptr: int | None = None) -> list[Result]:
+                 stream_ptr: int | None = None, workspace_ptr: int | None = None) -> list[Result]:
         t = _arr(targets, np.float64)
         out = (_Result * len(t))()
-        _check(lib().alp_finalize(self._h, t.ctypes.data, len(t), budget, keys_ptr, counts_ptr, _stream(stream_ptr),
-                                  out),
+        _check(lib().alp_finalize(self._h, t.ctypes.data, len(t), budget, keys_ptr, counts_ptr, workspace_ptr,
+                                  _stream(stream_ptr), out),
                (ALP_OK, ALP_EINFEASIBLE))
         return [Result._from(x) for x in out]
 
     def finalize_gathered(self, targets: Sequence[float], budget: int, gathered_ptr: int, world: int,
-                          stream_ptr: int | None = None) -> list[Result]:
+                          stream_ptr: int | None = None, workspace_ptr: int | None = None) -> list[Result]:
         """alp_finalize_gathered: finalize from all-gathered per-rank int64[world][2][n] pairs."""
         t = _arr(targets, np.float64)
         out = (_Result * len(t))()
         _check(lib().alp_finalize_gathered(self._h, t.ctypes.data, len(t), budget, gathered_ptr, world,
-                                           _stream(stream_ptr),
-                                           out), (ALP_OK, ALP_EINFEASIBLE))
+                                           workspace_ptr, _stream(stream_ptr), out), (ALP_OK, ALP_EINFEASIBLE))
         return [Result._from(x) for x in out]
 
     @property

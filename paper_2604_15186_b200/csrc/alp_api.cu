@@ -119,6 +119,14 @@ struct Arena {
     copied = total;
     fix.push_back({off, reinterpret_cast<void **>(dptr)});
   }
+  // a trailing region of `bytes` whose first `zeros` bytes are uploaded as zeros (must come last)
+  void region(size_t bytes, size_t zeros, unsigned char **dptr) {
+    const size_t off = align(total);
+    host.resize(off + zeros, 0);
+    copied = off + zeros;
+    total = off + bytes;
+    fix.push_back({off, reinterpret_cast<void **>(dptr)});
+  }
   template <class T>
   void scratch(size_t count, T **dptr) {
     const size_t off = align(total);
@@ -234,6 +242,26 @@ void ctx_release(const StreamCtx &c) {
   g_ctx_pool.push_back(c);
 }
 
+// Per-search scratch: the option tables of the searched targets, the (key, count) accumulators, the
+// work counters and the finalize inputs/outputs of one search.  It is either the handle's own (one
+// target: inside the handle's arena; more: a grown buffer) or a caller workspace (alp_search_shard /
+// alp_finalize with d_workspace, sized by alp_workspace_bytes).  Layout (ws_layout): a fixed-size
+// section that the kernels leave zero after every call (fused accumulators: complemented keys,
+// counts, work counters, ticket), then the per-target tables.
+struct Scratch {
+  unsigned long long *fzkeys = nullptr, *fzcounts = nullptr, *fzwork = nullptr;  // zero at rest
+  unsigned *fzticket = nullptr;                                                 // zero at rest
+  unsigned long long *fbest = nullptr;  // [n] finalize combine (zeroed by every search launch)
+  unsigned *fdone = nullptr;            // [n]
+  double *targets = nullptr, *term = nullptr, *b = nullptr;
+  float *tau = nullptr;
+  alp_result *res = nullptr;
+  unsigned long long *keys = nullptr, *counts = nullptr, *work = nullptr;
+  int *qb = nullptr;
+  int cap = 0;        // targets the tables hold
+  bool ws = false;    // a caller workspace (no cross-stream ordering through the handle)
+};
+
 // Device copy of a static search plan (sort-list tiles, u-sorted b columns, units).  The plan depends
 // only on the grids (units table), rows per lane and the device, so handles with the same key share it.
 struct PlanDev {
@@ -280,32 +308,15 @@ struct alp_s {
   uint32_t *d_tile_e = nullptr, *d_tile_off = nullptr;
   float *d_tau_fixed = nullptr;
   double *d_term_fixed = nullptr, *d_b_fixed = nullptr;
-  // per-search scratch: arena (1 target) or grown buffers (n > 1)
-  double *a_targets = nullptr, *a_term = nullptr, *a_b = nullptr;
-  float *a_tau = nullptr;
-  alp_result *a_res = nullptr;
-  unsigned long long *a_keys = nullptr, *a_counts = nullptr;
-  DBuf<double> g_targets, g_term, g_b;
-  DBuf<float> g_tau;
-  DBuf<alp_result> g_res;
-  DBuf<unsigned long long> g_keys, g_counts, g_work, g_dbg;
-  int *a_qb = nullptr;
-  unsigned long long *a_fbest = nullptr;  // finalize scratch (1 target), ~0 / 0 between calls
-  unsigned *a_fdone = nullptr;
-  DBuf<unsigned long long> g_fbest;
-  DBuf<unsigned> g_fdone;
-  unsigned long long *a_work = nullptr;  // kArenaWork work counters
-  // fused-launch scratch (rest state ~0 / 0, restored by the last block of every fused launch)
-  unsigned long long *a_fzkeys = nullptr, *a_fzcounts = nullptr, *a_fzwork = nullptr;
-  unsigned *a_fzticket = nullptr;
+  // per-search scratch (Scratch / ws_layout): own1 = one target, inside the arena; g_ws = the
+  // handle's own for more targets (capacity g_ws_cap); sc = the scratch of the current call
+  Scratch own1, sc;
+  DBuf<unsigned char> g_ws;
+  int g_ws_cap = 0;
+  DBuf<unsigned long long> g_dbg;
   cudaEvent_t evs0 = nullptr, evs1 = nullptr;  // step events: search start .. result D2H enqueued
   float last_step_ms = 0.f;
-  DBuf<int> g_qb;
-  int *s_qb = nullptr;  // per-query budgets (device) when the last search used them, else nullptr
-  double *s_targets = nullptr, *s_term = nullptr, *s_b = nullptr;
-  float *s_tau = nullptr;
-  alp_result *s_res = nullptr;
-  unsigned long long *s_keys = nullptr, *s_counts = nullptr;
+  int *s_qb = nullptr;  // per-query budgets (device) when the current search uses them, else nullptr
   DBuf<int> d_opts, d_pfeas;
   DBuf<double> d_plat, d_pthr;
   DBuf<long long> d_punits;
@@ -316,7 +327,8 @@ struct alp_s {
   bool ev_pending = false;
   float last_ms = 0.f;
   int last_launches = 0;
-  bool last_ur = false;  // the last search ran the uniform-register pair (k_uprep + k_search_u)
+  bool last_ur = false;
+  bool ws_used = false;  // a call ran on a caller workspace (its stream is not tracked: destroy syncs)  // the last search ran the uniform-register pair (k_uprep + k_search_u)
   uint64_t h2d = 0;
   SearchArgs last_args{};
   std::map<long long, int> occ_cache;  // (smem bytes, b width, T, MB) -> resident blocks per SM
@@ -335,19 +347,14 @@ struct alp_s {
     int cur = -1;
     cudaGetDevice(&cur);
     if (ctx.stream && cur != device) cudaSetDevice(device);
-    for (auto *b : {&g_targets, &g_term, &g_b, &d_plat, &d_pthr}) b->release();
-    for (auto *b : {&d_opts, &d_pfeas, &g_qb}) b->release();
-    g_tau.release();
-    g_res.release();
-    g_keys.release();
-    g_counts.release();
-    g_work.release();
+    for (auto *b : {&d_plat, &d_pthr}) b->release();
+    for (auto *b : {&d_opts, &d_pfeas}) b->release();
+    g_ws.release();
     g_dbg.release();
-    g_fbest.release();
-    g_fdone.release();
     d_punits.release();
     // stream-ordered release: after the last work on the handle's stream and on the last caller
     // stream (alp_search_shard may run on a caller's stream), without a host synchronisation
+    if (ws_used) cudaDeviceSynchronize();  // workspace calls may still run on untracked streams
     if (stream && last_stream && last_stream != stream) {
       cudaEventRecord(ctx.last, last_stream);
       cudaStreamWaitEvent(stream, ctx.last, 0);
@@ -594,6 +601,39 @@ alp_status get_plan(alp_s *h) {
   return ALP_OK;
 }
 
+// Byte layout of a Scratch for n targets at `base` (nullptr: sizes only).  Returns the total bytes;
+// *rest = the bytes of the leading section that must be zero before the first use (fixed size,
+// independent of n, so one buffer serves calls with any n up to its capacity).
+size_t ws_layout(const alp_s *h, int n, unsigned char *base, Scratch *sc, size_t *rest = nullptr) {
+  const size_t MK = (size_t)h->M * h->K, nn = (size_t)std::max(n, 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> unsigned char * {
+    const size_t o = (off + 255) & ~size_t(255);
+    off = o + bytes;
+    return base ? base + o : nullptr;
+  };
+  Scratch x;
+  x.fzkeys = reinterpret_cast<unsigned long long *>(take(8 * kInlineTargets));
+  x.fzcounts = reinterpret_cast<unsigned long long *>(take(8 * kInlineTargets));
+  x.fzwork = reinterpret_cast<unsigned long long *>(take(8 * kFusedWork));
+  x.fzticket = reinterpret_cast<unsigned *>(take(4));
+  if (rest) *rest = off;
+  x.fbest = reinterpret_cast<unsigned long long *>(take(8 * nn));
+  x.fdone = reinterpret_cast<unsigned *>(take(4 * nn));
+  x.targets = reinterpret_cast<double *>(take(8 * nn));
+  x.tau = reinterpret_cast<float *>(take(4 * nn * MK));
+  x.term = reinterpret_cast<double *>(take(8 * nn * MK));
+  x.b = reinterpret_cast<double *>(take(8 * nn * MK));
+  x.res = reinterpret_cast<alp_result *>(take(sizeof(alp_result) * nn));
+  x.keys = reinterpret_cast<unsigned long long *>(take(8 * nn));
+  x.counts = reinterpret_cast<unsigned long long *>(take(8 * nn));
+  x.qb = reinterpret_cast<int *>(take(4 * nn));
+  x.work = reinterpret_cast<unsigned long long *>(take(8 * std::max<size_t>(kArenaWork, 16 * nn)));
+  x.cap = (int)nn;
+  if (sc) *sc = x;
+  return (off + 255) & ~size_t(255);
+}
+
 // Stage the handle's own tables (profiles or injected terms) + single-target scratch in one allocation.
 alp_status upload_all(alp_s *h) {
   alp_status s = get_plan(h);
@@ -616,40 +656,22 @@ alp_status upload_all(alp_s *h) {
   }
   A.add(h->T, &h->d_T);
   A.add(h->R, &h->d_R);
-  // self-resetting scratch, initialised through the copied section (rest state), packed in one
-  // section: [fbest | fz keys x8 | fz counts x8 | fz work x128 | fdone, fz ticket (u32 pair)]
-  static const std::vector<unsigned long long> rest = [] {
-    std::vector<unsigned long long> v(1 + 2 * kInlineTargets + kFusedWork + 1, 0ull);
-    v[0] = ~0ull;
-    for (int i = 0; i < kInlineTargets; ++i) v[1 + i] = ~0ull;
-    return v;
-  }();
-  unsigned long long *d_rest = nullptr;
-  A.add(rest, &d_rest);
-  A.scratch(1, &h->a_targets);
-  A.scratch(MK, &h->a_tau);
-  A.scratch(MK, &h->a_term);
-  A.scratch(MK, &h->a_b);
-  A.scratch(1, &h->a_res);
-  A.scratch(1, &h->a_keys);
-  A.scratch(1, &h->a_counts);
-  A.scratch(1, &h->a_qb);
-  A.scratch(kArenaWork, &h->a_work);
+  // the single-target scratch: its zero-at-rest section rides in the copied part (no memset)
+  size_t rest = 0;
+  const size_t own = ws_layout(h, 1, nullptr, nullptr, &rest);
+  unsigned char *d_own = nullptr;
+  A.region(own, rest, &d_own);
   CU(A.commit(&h->d_arena, h->h2d, h->stream));
-  h->a_fbest = d_rest;
-  h->a_fzkeys = d_rest + 1;
-  h->a_fzcounts = d_rest + 1 + kInlineTargets;
-  h->a_fzwork = d_rest + 1 + 2 * kInlineTargets;
-  h->a_fdone = reinterpret_cast<unsigned *>(d_rest + 1 + 2 * kInlineTargets + kFusedWork);
-  h->a_fzticket = h->a_fdone + 1;
+  ws_layout(h, 1, d_own, &h->own1);
   CU(cudaEventRecord(h->ctx.ready, h->stream));  // searches on other streams wait for the upload
   return ALP_OK;
 }
 
 // Order a caller's stream after the handle's upload and after the handle's previous work on
 // another stream (the per-handle scratch is reused by every call); remember it for alp_destroy.
-alp_status use_stream(alp_s *h, cudaStream_t st) {
+alp_status use_stream(alp_s *h, cudaStream_t st, bool own_scratch = true) {
   if (st != h->stream) CU(cudaStreamWaitEvent(st, h->ctx.ready, 0));
+  if (!own_scratch) return ALP_OK;  // caller workspace: calls on other streams may overlap
   if (h->last_stream && h->last_stream != st) {
     CU(cudaEventRecord(h->ctx.last, h->last_stream));
     CU(cudaStreamWaitEvent(st, h->ctx.last, 0));
@@ -774,23 +796,36 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   return ALP_OK;
 }
 
-alp_status ensure_scratch(alp_s *h, int n) {
-  const size_t MK = (size_t)h->M * h->K;
+// Select the handle's own scratch for n targets (grown on demand; a new buffer's zero-at-rest
+// section is cleared on `st`).
+alp_status ensure_scratch(alp_s *h, int n, cudaStream_t st) {
   if (n <= 1) {
-    h->s_targets = h->a_targets; h->s_tau = h->a_tau; h->s_term = h->a_term; h->s_b = h->a_b;
-    h->s_res = h->a_res; h->s_keys = h->a_keys; h->s_counts = h->a_counts;
+    h->sc = h->own1;
     return ALP_OK;
   }
-  CU(h->g_targets.ensure(n));
-  CU(h->g_tau.ensure(n * MK));
-  CU(h->g_term.ensure(n * MK));
-  CU(h->g_b.ensure(n * MK));
-  CU(h->g_res.ensure(n));
-  CU(h->g_keys.ensure(n));
-  CU(h->g_counts.ensure(n));
-  h->s_targets = h->g_targets.p; h->s_tau = h->g_tau.p; h->s_term = h->g_term.p; h->s_b = h->g_b.p;
-  h->s_res = h->g_res.p; h->s_keys = h->g_keys.p; h->s_counts = h->g_counts.p;
+  if (h->g_ws_cap < n) {
+    const int cap = std::max(n, 2 * h->g_ws_cap);
+    size_t rest = 0;
+    CU(h->g_ws.ensure(ws_layout(h, cap, nullptr, nullptr, &rest)));
+    CU(cudaMemsetAsync(h->g_ws.p, 0, rest, st));
+    h->g_ws_cap = cap;
+  }
+  ws_layout(h, h->g_ws_cap, h->g_ws.p, &h->sc);  // laid out for the capacity: any n <= cap
   return ALP_OK;
+}
+
+// Select a caller workspace (alp_workspace_bytes(h, n) bytes, zero-filled before its first use).
+alp_status bind_workspace(alp_s *h, void *ws, int n) {
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(ALP_EINVAL, "d_workspace must be 256-byte aligned");
+  ws_layout(h, n, static_cast<unsigned char *>(ws), &h->sc);
+  h->sc.ws = true;
+  h->ws_used = true;
+  return ALP_OK;
+}
+
+// Scratch of a call: the caller's workspace when given, else the handle's own.
+alp_status select_scratch(alp_s *h, void *ws, int n, cudaStream_t st) {
+  return ws ? bind_workspace(h, ws, n) : ensure_scratch(h, n, st);
 }
 
 // K1 for n targets into the scratch tables (profiles mode) or replicate the fixed terms.
@@ -809,33 +844,35 @@ alp_status option_tables(alp_s *h, const double *targets, int n, cudaStream_t st
       if (ev) CU(cudaEventSynchronize(ev));
     if (!pin_ev[h->device]) CU(cudaEventCreateWithFlags(&pin_ev[h->device], cudaEventDisableTiming));
     memcpy(pin, targets, n * sizeof(double));
-    CU(cudaMemcpyAsync(h->s_targets, pin, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(h->sc.targets, pin, n * sizeof(double), cudaMemcpyHostToDevice, st));
     CU(cudaEventRecord(pin_ev[h->device], st));
   } else {
-    CU(cudaMemcpyAsync(h->s_targets, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(h->sc.targets, targets, n * sizeof(double), cudaMemcpyHostToDevice, st));
   }
   if (h->from_terms) {
     for (int t = 0; t < n; ++t) {
-      CU(cudaMemcpyAsync(h->s_tau + t * MK, h->d_tau_fixed, MK * sizeof(float), cudaMemcpyDeviceToDevice, st));
-      CU(cudaMemcpyAsync(h->s_term + t * MK, h->d_term_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      CU(cudaMemcpyAsync(h->s_b + t * MK, h->d_b_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->sc.tau + t * MK, h->d_tau_fixed, MK * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->sc.term + t * MK, h->d_term_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(h->sc.b + t * MK, h->d_b_fixed, MK * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
-    if (keys) CU(launch_init_keys(keys, counts, n, work, n_work, st));
+    if (keys) CU(launch_init_keys(keys, counts, n, work, n_work, h->sc.fbest, h->sc.fdone, st));
     return ALP_OK;
   }
   OptionArgs o;
   o.prof = h->dprof();
-  o.targets = inline_t ? nullptr : h->s_targets;
+  o.targets = inline_t ? nullptr : h->sc.targets;
   for (int i = 0; i < kInlineTargets; ++i) o.tgt[i] = (inline_t && i < n) ? targets[i] : 0.0;
   o.n_targets = n;
-  o.tau = h->s_tau;
-  o.term = h->s_term;
-  o.b = h->s_b;
+  o.tau = h->sc.tau;
+  o.term = h->sc.term;
+  o.b = h->sc.b;
   o.u = h->d_u;
   o.keys = keys;
   o.counts = counts;
   o.work = work;
   o.n_work = n_work;
+  o.fbest = h->sc.fbest;  // finalize combine scratch, zeroed for the K3 after this search
+  o.fdone = h->sc.fdone;
   CU(launch_option_table(o, st));
   return ALP_OK;
 }
@@ -859,12 +896,7 @@ alp_status prepare_budgets(alp_s *h, const int64_t *budgets, int n, cudaStream_t
     qb[i] = (int)std::min<int64_t>(budgets[i], h->umax_total);
     mx = std::max<int64_t>(mx, budgets[i]);
   }
-  if (n <= 1) {
-    h->s_qb = h->a_qb;
-  } else {
-    CU(h->g_qb.ensure(n));
-    h->s_qb = h->g_qb.p;
-  }
+  h->s_qb = h->sc.qb;
   CU(cudaMemcpyAsync(h->s_qb, qb.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
   CU(cudaStreamSynchronize(st));  // qb is a host temporary
   *rmax = mx;
@@ -884,8 +916,8 @@ bool use_fused(const alp_s *h, int n, const int64_t *budgets) {
 // Finalize inputs of the handle's scratch (K3 and the fused last block).
 void fill_finalize(alp_s *h, SearchArgs &a) {
   FinalizeExtra &f = a.fin;
-  f.term = h->s_term;
-  f.b = h->s_b;
+  f.term = h->sc.term;
+  f.b = h->sc.b;
   if (h->from_terms) {  // injected terms: the FP64 terms are the handle's fixed tables (any path)
     f.term = h->d_term_fixed;
     f.b = h->d_b_fixed;
@@ -895,24 +927,9 @@ void fill_finalize(alp_s *h, SearchArgs &a) {
   f.R = h->d_R;
   f.nS = h->nS; f.nT = h->nT; f.nR = h->nR;
   f.N = h->N;
-  f.out = h->s_res;
-  const int n = a.n_targets;
-  f.best = h->a_fbest;
-  f.done = h->a_fdone;
-  if (n > 1) {
-    f.best = h->g_fbest.p;
-    f.done = h->g_fdone.p;
-  }
-}
-
-alp_status ensure_finalize_scratch(alp_s *h, int n, cudaStream_t st) {
-  if (n > 1 && h->g_fbest.n < (size_t)n) {
-    CU(h->g_fbest.ensure(n));
-    CU(h->g_fdone.ensure(n));
-    CU(cudaMemsetAsync(h->g_fbest.p, 0xff, n * sizeof(unsigned long long), st));
-    CU(cudaMemsetAsync(h->g_fdone.p, 0, n * sizeof(unsigned), st));
-  }
-  return ALP_OK;
+  f.out = h->sc.res;
+  f.best = h->sc.fbest;
+  f.done = h->sc.fdone;
 }
 
 // Uniform-register path (alp_search_u.cu) for single-target searches with short b rows: the
@@ -986,14 +1003,14 @@ int ur_batch_group(alp_s *h, int64_t budget) {
 alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
                              uint64_t lo, uint64_t hi, cudaStream_t st, unsigned long long *keys,
                              unsigned long long *counts, bool fuse_finalize = false,
-                             alp_result *fused_out = nullptr, bool first_of_batch = true) {
+                             alp_result *fused_out = nullptr, bool first_of_batch = true, void *ws = nullptr) {
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
-  s = use_stream(h, st);
+  s = use_stream(h, st, ws == nullptr);
   if (s != ALP_OK) return s;
   if (first_of_batch) CU(cudaEventRecord(h->evs0, st));  // step start (a batch of launches: the first)
-  s = ensure_scratch(h, n);
+  s = select_scratch(h, ws, n, st);
   if (s != ALP_OK) return s;
   s = prepare_budgets(h, budgets, n, st, &budget);
   if (s != ALP_OK) return s;
@@ -1006,7 +1023,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
                                          (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)items);
   const size_t nctr = (size_t)n * g.a.n_bchunks;
   int launches = 0;
-  unsigned long long *work = h->a_work;
+  unsigned long long *work = h->sc.work;
   if (fused) {
     if (nctr > kFusedWork) return fail(ALP_EINTERNAL, "fused search: %zu work counters", nctr);
     FusedArgs &z = g.a.fz;
@@ -1015,24 +1032,16 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     if (!h->from_terms) z.prof = h->dprof();
     for (int i = 0; i < kInlineTargets; ++i) z.tgt[i] = i < n ? targets[i] : 0.0;
     z.tau_fixed = h->from_terms ? h->d_tau_fixed : nullptr;
-    z.o_tau = h->s_tau;
-    z.o_term = h->s_term;
-    z.o_b = h->s_b;
-    z.acc_keys = h->a_fzkeys;
-    z.acc_counts = h->a_fzcounts;
-    z.work = h->a_fzwork;
-    z.ticket = h->a_fzticket;
-    work = h->a_fzwork;
-    if (fuse_finalize) {
-      s = ensure_finalize_scratch(h, n, st);
-      if (s != ALP_OK) return s;
-    }
+    z.o_tau = h->sc.tau;
+    z.o_term = h->sc.term;
+    z.o_b = h->sc.b;
+    z.acc_keys = h->sc.fzkeys;
+    z.acc_counts = h->sc.fzcounts;
+    z.work = h->sc.fzwork;
+    z.ticket = h->sc.fzticket;
+    work = h->sc.fzwork;
   } else {
-    // work counters (one per phase, zeroed by K1)
-    if (nctr > kArenaWork) {
-      CU(h->g_work.ensure(nctr));
-      work = h->g_work.p;
-    }
+    // work counters (one per phase, zeroed by K1; the scratch holds >= 16 per target)
     s = option_tables(h, targets, n, st, keys, counts, work, (int)nctr);
     if (s != ALP_OK) return s;
     launches = 1;  // K1
@@ -1040,7 +1049,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   g.a.q_budget = h->s_qb;
   g.a.item_lo = lo;
   g.a.item_hi = hi;
-  g.a.tau = h->s_tau;
+  g.a.tau = h->sc.tau;
   g.a.keys = keys;
   g.a.counts = counts;
   fill_finalize(h, g.a);
@@ -1059,7 +1068,10 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     static const bool dbg = getenv("ALP_DBG_TS") != nullptr;  // per-block timeline (diagnostics)
     SearchArgs ua;
     int ugrid = 0;
-    const bool ur = fused && ur_path(h, g.a, n, hi, ua, ugrid);
+    // the uniform-register path shares one constant bank per device: a search on a caller
+    // workspace whose bank is still in use by another stream's search takes k_search instead
+    // (same keys and counts), so searches on distinct workspaces and streams overlap
+    const bool ur = fused && ur_path(h, g.a, n, hi, ua, ugrid) && !(h->sc.ws && search_u_busy());
     const int dgrid = ur ? ugrid : g.grid;
     if (dbg) {
       CU(h->g_dbg.ensure((size_t)dgrid * 8));
@@ -1149,12 +1161,12 @@ alp_status collect_results(alp_s *h, int n, cudaStream_t st, alp_result *out, co
     memcpy(out, host_zc, n * sizeof(alp_result));
   } else if (pin) {
     pin = static_cast<unsigned char *>(pin) + kPinHalf;
-    CU(cudaMemcpyAsync(pin, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(pin, h->sc.res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(h->evs1, st));
     CU(cudaStreamSynchronize(st));
     memcpy(out, pin, n * sizeof(alp_result));
   } else {
-    CU(cudaMemcpyAsync(out, h->s_res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(out, h->sc.res, n * sizeof(alp_result), cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(h->evs1, st));
     CU(cudaStreamSynchronize(st));
   }
@@ -1170,12 +1182,12 @@ alp_status collect_results(alp_s *h, int n, cudaStream_t st, alp_result *out, co
 
 alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
                          const unsigned long long *keys, const unsigned long long *counts, cudaStream_t st,
-                         alp_result *out, int world = 0) {
+                         alp_result *out, int world = 0, void *ws = nullptr) {
   if (!out) return fail(ALP_EINVAL, "out is NULL");
   CU(cudaSetDevice(h->device));
-  alp_status s = use_stream(h, st);
+  alp_status s = use_stream(h, st, ws == nullptr);
   if (s != ALP_OK) return s;
-  s = ensure_scratch(h, n);
+  s = select_scratch(h, ws, n, st);  // the scratch the shard search wrote (same n)
   if (s != ALP_OK) return s;
   if (budgets) {
     s = prepare_budgets(h, budgets, n, st, &budget);
@@ -1189,9 +1201,7 @@ alp_status finalize_impl(alp_s *h, const double *targets, const int64_t *budgets
   // option tables must describe these targets (the shard call computed them on this handle)
   (void)targets;
   g.a.q_budget = h->s_qb;
-  g.a.tau = h->s_tau;
-  s = ensure_finalize_scratch(h, n, st);
-  if (s != ALP_OK) return s;
+  g.a.tau = h->sc.tau;
   fill_finalize(h, g.a);
   g.a.fin.keys = keys;
   g.a.fin.counts = counts;
@@ -1355,14 +1365,14 @@ alp_status alp_option_table(alp_t *h, double lambda, float *tau, double *term, d
   CU(cudaSetDevice(h->device));
   s = use_stream(h, h->stream);
   if (s != ALP_OK) return s;
-  s = ensure_scratch(h, 1);
+  s = ensure_scratch(h, 1, h->stream);
   if (s != ALP_OK) return s;
   s = option_tables(h, &lambda, 1, h->stream, nullptr, nullptr);
   if (s != ALP_OK) return s;
   const size_t MK = (size_t)h->M * h->K;
-  if (tau) CU(cudaMemcpyAsync(tau, h->s_tau, MK * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
-  if (term) CU(cudaMemcpyAsync(term, h->s_term, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  if (b) CU(cudaMemcpyAsync(b, h->s_b, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (tau) CU(cudaMemcpyAsync(tau, h->sc.tau, MK * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  if (term) CU(cudaMemcpyAsync(term, h->sc.term, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (b) CU(cudaMemcpyAsync(b, h->sc.b, MK * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   if (u) memcpy(u, h->u.data(), MK * sizeof(int32_t));
   return ALP_OK;
@@ -1424,18 +1434,23 @@ alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, i
   return ALP_OK;
 }
 
+size_t alp_workspace_bytes(const alp_t *h, int32_t n_targets) {
+  if (!h || n_targets < 1) return 0;
+  return ws_layout(h, n_targets, nullptr, nullptr);
+}
+
 alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
-                            uint64_t hi, void *stream, int64_t *d_keys, int64_t *d_counts) {
+                            uint64_t hi, void *d_workspace, void *stream, int64_t *d_keys, int64_t *d_counts) {
   NvtxRange nv("alp_search_shard");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
   return search_shard_impl(h, targets, nullptr, n, budget_units, lo, hi, stream ? (cudaStream_t)stream : h->stream,
                            reinterpret_cast<unsigned long long *>(d_keys),
-                           reinterpret_cast<unsigned long long *>(d_counts));
+                           reinterpret_cast<unsigned long long *>(d_counts), false, nullptr, true, d_workspace);
 }
 
 alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budget_units, const int64_t *d_keys,
-                        const int64_t *d_counts, void *stream, alp_result *out) {
+                        const int64_t *d_counts, void *d_workspace, void *stream, alp_result *out) {
   NvtxRange nv("alp_finalize");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
@@ -1443,11 +1458,12 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
   if (s != ALP_OK) return s;
   return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
                        reinterpret_cast<const unsigned long long *>(d_counts),
-                       stream ? (cudaStream_t)stream : h->stream, out);
+                       stream ? (cudaStream_t)stream : h->stream, out, 0, d_workspace);
 }
 
 alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
-                                 const int64_t *d_gathered, int32_t world, void *stream, alp_result *out) {
+                                 const int64_t *d_gathered, int32_t world, void *d_workspace, void *stream,
+                                 alp_result *out) {
   NvtxRange nv("alp_finalize_gathered");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!d_gathered) return fail(ALP_EINVAL, "d_gathered is NULL");
@@ -1455,7 +1471,7 @@ alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_gathered),
-                       nullptr, stream ? (cudaStream_t)stream : h->stream, out, world);
+                       nullptr, stream ? (cudaStream_t)stream : h->stream, out, world, d_workspace);
 }
 
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
@@ -1466,7 +1482,7 @@ static alp_status search_queries(alp_t *h, const double *targets, const int64_t 
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
-  s = ensure_scratch(h, n);
+  s = ensure_scratch(h, n, h->stream);
   if (s != ALP_OK) return s;
   const uint64_t items = alp_num_items(h, budget_units);
   const int ug = budgets ? 0 : ur_batch_group(h, budget_units);
@@ -1478,7 +1494,7 @@ static alp_status search_queries(alp_t *h, const double *targets, const int64_t 
     int launches = 0;
     for (int i = 0; i < n; i += ug) {
       const int g = std::min(ug, n - i);
-      s = search_shard_impl(h, targets + i, nullptr, g, budget_units, 0, items, h->stream, h->s_keys, h->s_counts,
+      s = search_shard_impl(h, targets + i, nullptr, g, budget_units, 0, items, h->stream, h->sc.keys, h->sc.counts,
                             true, zc + i, i == 0);
       if (s != ALP_OK) return s;
       launches += h->last_launches;
@@ -1488,14 +1504,14 @@ static alp_status search_queries(alp_t *h, const double *targets, const int64_t 
   }
   if (use_fused(h, n, budgets)) {  // one launch: terms + search + finalize
     alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);  // the last block stores the results
-    s = search_shard_impl(h, targets, nullptr, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts, true,
+    s = search_shard_impl(h, targets, nullptr, n, budget_units, 0, items, h->stream, h->sc.keys, h->sc.counts, true,
                           zc);
     if (s != ALP_OK) return s;
     return collect_results(h, n, h->stream, out, hzc);
   }
-  s = search_shard_impl(h, targets, budgets, n, budget_units, 0, items, h->stream, h->s_keys, h->s_counts);
+  s = search_shard_impl(h, targets, budgets, n, budget_units, 0, items, h->stream, h->sc.keys, h->sc.counts);
   if (s != ALP_OK) return s;
-  return finalize_impl(h, targets, budgets, n, budget_units, h->s_keys, h->s_counts, h->stream, out);
+  return finalize_impl(h, targets, budgets, n, budget_units, h->sc.keys, h->sc.counts, h->stream, out);
 }
 
 alp_status alp_search_batch(alp_t *h, const double *targets, int32_t n, int64_t budget_units, alp_result *out) {

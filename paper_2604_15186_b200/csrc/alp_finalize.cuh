@@ -99,7 +99,7 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
     // combine the blocks of this target: global min, then only the last block continues
     __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
-      if (found) atomicMin(F.best + t, s_best);
+      if (found) atomicMax(F.best + t, ~s_best);  // complemented minimum: zero at rest
       __threadfence();
       s_last = (atomicAdd(F.done + t, 1u) == (unsigned)nparts - 1) ? 1u : 0u;
     }
@@ -107,8 +107,8 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
     if (!s_last) return;
     if (threadIdx.x == 0) {
       __threadfence();
-      s_best = atomicAdd(F.best + t, 0ull);  // coherent read of the combined minimum
-      F.best[t] = ~0ull;                    // reset for the next finalize on this scratch
+      s_best = ~atomicAdd(F.best + t, 0ull);  // coherent read of the combined minimum
+      F.best[t] = 0ull;                      // rest state (zero) for the next finalize on this scratch
       F.done[t] = 0u;
     }
     __syncthreads();

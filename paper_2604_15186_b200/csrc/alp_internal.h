@@ -56,6 +56,8 @@ struct OptionArgs {
   unsigned long long *counts;  // [n_t] initialised to 0 (may be null)
   unsigned long long *work;    // [n_work] search work counters, zeroed (may be null)
   int n_work;
+  unsigned long long *fbest;   // [n_targets] finalize combine scratch, zeroed (may be null)
+  unsigned *fdone;             // [n_targets] zeroed (may be null)
 };
 
 
@@ -70,7 +72,7 @@ struct FinalizeExtra {
   const unsigned long long *counts;  // [n_t] reduced counts (K3 input; unused when world > 0)
   int world;                         // > 0: K3 reduces the gathered per-rank (keys, counts) itself
   alp_result *out;       // [n_t] device
-  unsigned long long *best;  // [n_t] scratch: ~0 between calls (self-resetting)
+  unsigned long long *best;  // [n_t] scratch: complemented minimum, 0 between calls (self-resetting)
   unsigned *done;            // [n_t] scratch: 0 between calls (self-resetting)
 };
 
@@ -85,7 +87,7 @@ struct FusedArgs {
   const float *tau_fixed;     // injected terms (alp_build_from_terms) instead of prof, or nullptr
   float *o_tau;               // [n_t][M][K] written by block 0 (K3 / finalize inputs)
   double *o_term, *o_b;       // [n_t][M][K] written by block 0 (nullptr with injected terms)
-  unsigned long long *acc_keys;    // [n_t] ~0 at rest
+  unsigned long long *acc_keys;    // [n_t] complemented keys (~key, atomicMax), 0 at rest
   unsigned long long *acc_counts;  // [n_t] 0 at rest
   unsigned long long *work;        // [n_t * n_bchunks] 0 at rest
   unsigned *ticket;                // 0 at rest
@@ -180,12 +182,13 @@ inline cudaError_t launch_pdl(void (*fn)(Args), dim3 grid, dim3 block, size_t sm
 // Launchers (alp_kernels.cu). Return cudaError_t of the launch.
 cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st);
 cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
-                             int n_work, cudaStream_t st);
+                             int n_work, unsigned long long *fbest, unsigned *fdone, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 // uniform-register path: prep (option terms + constant-bank tables, one block) and search
 // (before_search, if set, is recorded on st between the prep and the search kernel)
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search);
 int search_u_max_blocks_per_sm(const SearchArgs &a);
+bool search_u_busy();  // a uniform-register search launched on this device has not completed yet
 size_t uprep_smem_bytes(const SearchArgs &a);  // k_uprep dynamic shared memory (<= kUPrepSmemMax)
 constexpr size_t kUPrepSmemMax = 200 * 1024;
 constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path

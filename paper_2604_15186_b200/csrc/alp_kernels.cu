@@ -45,6 +45,8 @@ __global__ void k_option_table(const __grid_constant__ OptionArgs A) {
   if (i < A.n_targets) {
     if (A.keys) A.keys[i] = kKeyNone;
     if (A.counts) A.counts[i] = 0ull;
+    if (A.fbest) A.fbest[i] = 0ull;  // the finalize after this search combines into zeroed scratch
+    if (A.fdone) A.fdone[i] = 0u;
   }
   if (i < A.n_work) A.work[i] = 0ull;
   if (i >= A.n_targets * MK) return;
@@ -60,11 +62,13 @@ __global__ void k_option_table(const __grid_constant__ OptionArgs A) {
 }
 
 __global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
-                            int n_work) {
+                            int n_work, unsigned long long *fbest, unsigned *fdone) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     keys[i] = kKeyNone;
     counts[i] = 0ull;
+    if (fbest) fbest[i] = 0ull;
+    if (fdone) fdone[i] = 0u;
   }
   if (i < n_work) work[i] = 0ull;
 }
@@ -219,10 +223,10 @@ cudaError_t launch_option_table(const OptionArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
-                             int n_work, cudaStream_t st) {
+                             int n_work, unsigned long long *fbest, unsigned *fdone, cudaStream_t st) {
   const int m = n > n_work ? n : n_work;
   max_carveout(reinterpret_cast<const void *>(k_init_keys));
-  k_init_keys<<<(m + 255) / 256, 256, 0, st>>>(keys, counts, n, work, n_work);
+  k_init_keys<<<(m + 255) / 256, 256, 0, st>>>(keys, counts, n, work, n_work, fbest, fdone);
   return cudaGetLastError();
 }
 

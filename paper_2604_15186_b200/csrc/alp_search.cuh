@@ -428,7 +428,7 @@ __device__ inline void fused_epilogue(const SearchArgs &P, const float *tau_last
   if (!s_last) return;
   __threadfence();
   for (int t = threadIdx.x; t < P.n_targets; t += blockDim.x) {
-    unsigned long long k = atomicExch(P.fz.acc_keys + t, ~0ull);
+    unsigned long long k = ~atomicExch(P.fz.acc_keys + t, 0ull);  // complemented keys, zero at rest
     const unsigned long long n = atomicExch(P.fz.acc_counts + t, 0ull);
     if (k == ~0ull) k = kKeyNone;
     P.keys[t] = k;
@@ -438,6 +438,12 @@ __device__ inline void fused_epilogue(const SearchArgs &P, const float *tau_last
   }
   for (int i = threadIdx.x; i < P.n_targets * P.n_bchunks; i += blockDim.x) P.fz.work[i] = 0ull;
   if (threadIdx.x == 0) atomicExch(P.fz.ticket, 0u);
+  // a K3 finalize after this (shard) search combines its blocks in zeroed scratch
+  if (!P.fz.finalize && P.fin.best)
+    for (int t = threadIdx.x; t < P.n_targets; t += blockDim.x) {
+      P.fin.best[t] = 0ull;
+      P.fin.done[t] = 0u;
+    }
   __syncthreads();
   if (P.fz.finalize)  // the last target's option terms are still in shared memory (tau_last)
     for (int t = 0; t < P.n_targets; ++t)
@@ -503,9 +509,13 @@ __global__ void __launch_bounds__(kThreads, MB)
         k = red_key[w] < k ? red_key[w] : k;
         n += red_cnt[w];
       }
-      unsigned long long *kd = P.fz.on ? P.fz.acc_keys : P.keys;
       unsigned long long *cd = P.fz.on ? P.fz.acc_counts : P.counts;
-      if (k != kKeyNone) atomicMin(kd + t, k);
+      if (k != kKeyNone) {
+        if (P.fz.on)
+          atomicMax(P.fz.acc_keys + t, ~k);  // fused scratch holds complemented keys (zero at rest)
+        else
+          atomicMin(P.keys + t, k);
+      }
       if (n) atomicAdd(cd + t, n);
     }
   }

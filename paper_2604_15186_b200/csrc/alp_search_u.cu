@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       cnt += oc;
     }
     if (lane == 0) {
-      if (key != kKeyNone) atomicMin(P.fz.acc_keys + t, key);
+      if (key != kKeyNone) atomicMax(P.fz.acc_keys + t, ~key);  // complemented: zero at rest
       if (cnt) atomicAdd(P.fz.acc_counts + t, cnt);
     }
   }
@@ -539,6 +539,17 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
   if (before_search && (e = cudaEventRecord(before_search, st)) != cudaSuccess) return e;
   if ((e = launch_u_search(a, grid, st)) != cudaSuccess) return e;
   return cudaEventRecord(u.done, st);
+}
+
+bool search_u_busy() {
+  std::lock_guard<std::mutex> lock(g_u_mu);
+  UState &u = ustate();
+  const cudaError_t e = cudaEventQuery(u.done);
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();  // not an error: clear it
+    return true;
+  }
+  return false;
 }
 
 int search_u_max_blocks_per_sm(const SearchArgs &a) {

@@ -49,7 +49,20 @@ def search_distributed(alp: Alp, targets: Sequence[float], budget: int, group=No
     n = len(targets)
     pairs = torch.empty(2 * n, dtype=torch.int64, device="cuda")
     gathered = torch.empty(world * 2 * n, dtype=torch.int64, device="cuda")
+    ws = workspace(alp, n)
     with torch.cuda.stream(st):
-        alp.search_shard(targets, budget, lo, hi, pairs.data_ptr(), pairs.data_ptr() + 8 * n, st.cuda_stream)
+        alp.search_shard(targets, budget, lo, hi, pairs.data_ptr(), pairs.data_ptr() + 8 * n, st.cuda_stream,
+                         ws.data_ptr())
         w = gather_pairs(pairs, gathered, group)
-        return alp.finalize_gathered(targets, budget, gathered.data_ptr(), w, st.cuda_stream)
+        return alp.finalize_gathered(targets, budget, gathered.data_ptr(), w, st.cuda_stream, ws.data_ptr())
+
+
+def workspace(alp: Alp, n: int) -> torch.Tensor:
+    """A torch-owned, zero-filled caller workspace for n targets (alp_workspace_bytes), cached on the
+    handle: every call leaves its control section zero, so it is reused without clearing."""
+    cache = alp.__dict__.setdefault("_workspaces", {})
+    ws = cache.get(n)
+    if ws is None:
+        ws = torch.zeros(alp.workspace_bytes(n), dtype=torch.uint8, device="cuda")
+        cache[n] = ws
+    return ws

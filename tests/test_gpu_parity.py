@@ -760,6 +760,75 @@ def test_uniform_register_path_concurrent_streams(P):
         assert (rB.index, rB.feasible_count, rB.latency_key) == (refB.index, refB.feasible_count, refB.latency_key)
 
 
+def _wait_event(ev, timeout_s):
+    """Poll a CUDA event from the host; True if it completed within timeout_s."""
+    import time
+    t0 = time.monotonic()
+    while not ev.query():
+        if time.monotonic() - t0 > timeout_s:
+            return False
+        time.sleep(0.0005)
+    return True
+
+
+def test_workspace_searches_overlap_across_streams(P):
+    """SURVEY.md §8(b) / SPEC.md:303 ("predictions are pure and may run concurrently"): two searches
+    on ONE handle with distinct caller workspaces on two streams are not ordered against each other.
+    Stream A is held by a ~1 s spin kernel before its search; search B on stream B completes while A
+    is still held (it would wait the whole second if the library serialised it behind A), then both
+    results match the oracle (O2).  Control: with the handle's own scratch, B does wait for A."""
+    import torch
+    d = generate.load("C4")
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    B_ = I.budget
+    la, lb = [d["targets"][0]], [2.0 * d["targets"][0]]
+    nbytes = alp.workspace_bytes(1)
+    assert nbytes > 0
+    wA = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    wB = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    sA, sB = torch.cuda.Stream(), torch.cuda.Stream()
+    kA = torch.empty(2, dtype=torch.int64, device="cuda")
+    kB = torch.empty(2, dtype=torch.int64, device="cuda")
+    lo, hi = alp.shard_range(B_, 0, 1)
+    rate = torch.cuda.get_device_properties(0).clock_rate * 1000  # kHz -> Hz
+    for use_ws in (True, False):
+        torch.cuda.synchronize()
+        endA, endB = torch.cuda.Event(), torch.cuda.Event()
+        with torch.cuda.stream(sA):
+            torch.cuda._sleep(int(1.0 * rate))  # hold stream A for ~1 s
+        alp.search_shard(la, B_, lo, hi, kA.data_ptr(), kA.data_ptr() + 8, sA.cuda_stream,
+                         wA.data_ptr() if use_ws else None)
+        endA.record(sA)
+        alp.search_shard(lb, B_, lo, hi, kB.data_ptr(), kB.data_ptr() + 8, sB.cuda_stream,
+                         wB.data_ptr() if use_ws else None)
+        endB.record(sB)
+        b_first = _wait_event(endB, 0.5)
+        a_pending = not endA.query()
+        torch.cuda.synchronize()
+        if use_ws:
+            assert b_first and a_pending, "search B was serialised behind search A"
+            for lam, k, w in ((la, kA, wA), (lb, kB, wB)):
+                r = alp.finalize(lam, B_, k.data_ptr(), k.data_ptr() + 8, None, w.data_ptr())[0]
+                tab = oracle.option_table(I, lam[0])
+                _same(r, *dp.search(tab["tau"], tab["u"], B_), lam)
+                _check_winner(P, alp, I, lam[0], B_, r)
+        else:
+            assert not b_first, "control: the handle's own scratch orders B after A"
+    # a workspace is reusable without clearing (its control section is zero after every call), for
+    # any target count up to its size
+    w8 = torch.zeros(alp.workspace_bytes(8), dtype=torch.uint8, device="cuda")
+    k8 = torch.empty(16, dtype=torch.int64, device="cuda")
+    for n in (1, 3, 8, 2):
+        lams = [d["targets"][0] * (1 + 0.5 * j) for j in range(n)]
+        alp.search_shard(lams, B_, lo, hi, k8.data_ptr(), k8.data_ptr() + 8 * n, None, w8.data_ptr())
+        res = alp.finalize(lams, B_, k8.data_ptr(), k8.data_ptr() + 8 * n, None, w8.data_ptr())
+        for r, lam in zip(res, lams):
+            tab = oracle.option_table(I, lam)
+            _same(r, *dp.search(tab["tau"], tab["u"], B_), (n, lam))
+    assert bool((w8[:64] == 0).all())
+
+
 def test_uniform_register_batch_groups_vs_oracle(P):
     """A 12-target batch runs as uniform-register groups of 8 + 4 (results zero-copy, one sync);
     every target against the brute-force oracle, including infeasible ones."""
