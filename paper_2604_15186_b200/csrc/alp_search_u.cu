@@ -15,6 +15,8 @@
 namespace alp {
 
 __constant__ __align__(16) unsigned char cu_mem[kUBytes];  // tables (layout: SearchArgs u_*)
+// the same bank as b pairs (masked rows start at even float offsets inside 16-byte aligned blocks)
+#define cu_pairs (reinterpret_cast<const float2 *>(cu_mem))
 
 // typed views of a target's block of the tables (constant bank or its global staging copy)
 struct UView {
@@ -165,18 +167,21 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   stamp(8 + 5);
 }
 
+// "candidate = Q_a,i + tau_b; acc_i = min(acc_i, candidate)" over a uniform masked row: per b PAIR
+// one LDCU.64 into a uniform register pair, then per row one FADD2 Q_a,i.F32 + {b_j, b_j+1} (the
+// scalar vector operand broadcast by .F32; the b pair read from the uniform register file) and one
+// FMNMX3 acc_i = min(acc_i, x, y): 1 issue slot per candidate and half the LDCU of the row-pair form
+// (tools/microbench/pipes7: 96 vs 93 candidates/clk/SM at 18 b per row, 103 vs 98 at 64).
 template <int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row_u(const float *rb, const float (&Qa)[12], float (&acc)[12]) {
+__device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[12], float (&acc)[12]) {
 #pragma unroll
-  for (int j = 0; j < 4 * NB4 + (TAIL2 ? 2 : 0); j += 2) {
-    const float b0 = rb[j], b1 = rb[j + 1];
+  for (int j = 0; j < 2 * NB4 + (TAIL2 ? 1 : 0); ++j) {
+    const float2 b = rb[j];
 #pragma unroll
-    for (int i = 0; i < 12; i += 2) {
-      float x0, y0, x1, y1;
-      add2b(x0, y0, Qa[i], Qa[i + 1], b0);
-      add2b(x1, y1, Qa[i], Qa[i + 1], b1);
-      acc[i] = min3(acc[i], x0, x1);
-      acc[i + 1] = min3(acc[i + 1], y0, y1);
+    for (int i = 0; i < 12; ++i) {
+      float x, y;
+      add2(x, y, Qa[i], b.x, b.y);
+      acc[i] = min3(acc[i], x, y);
     }
   }
 }
@@ -263,7 +268,11 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
           float Qa[T];
 #pragma unroll
           for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-          eval_row_u<NB4, TAIL2>(cv.btab() + lu.x, Qa, acc);
+          // float2 indexing from the 16-byte aligned bank base: the address is provably 8-byte
+          // aligned, so ptxas loads each b pair with ONE LDCU.64 (a float* + offset form is split
+          // into two scalar LDCU)
+          eval_row_u<NB4, TAIL2>(cu_pairs + ((P.u_tbase + t * P.u_tstride + P.u_off_btab) >> 3) + (lu.x >> 1), Qa,
+                                 acc);
         }
       } else {
         // mixed group: the lanes' own remaining budgets, rows from the global staging copy of the
