@@ -290,7 +290,9 @@ struct alp_s {
   uint32_t L = 1, n_chunks = 1, n_groups = 1, nQ = 1, A = 1;
   uint32_t pw[ALP_MAX_M] = {0};
   std::vector<int> tile_s, bperm, bu, dv, dcnt;
-  std::vector<int> gsum;     // unit sum of each uniform warp group (groups [0, n_groups_u))
+  // per warp group: the unit sum shared by its 32 lane tiles (uniform groups [0, n_groups_u)), or
+  // the smallest tile sum of a mixed group (all its lanes are over budget when that one is)
+  std::vector<int> gsum;
   uint32_t n_groups_u = 0;
   std::vector<uint32_t> tile_e, tile_off;
   int rows_per_lane = 8;
@@ -464,6 +466,8 @@ alp_status make_plan(alp_s *h) {
       ts.push_back(ts.back());
       for (int r = 0; r < T; ++r) te.push_back(kDummy);
     }
+    for (size_t g = h->n_groups_u * (size_t)kWarpTiles; g < ts.size(); g += kWarpTiles)
+      h->gsum.push_back(*std::min_element(ts.begin() + g, ts.begin() + g + kWarpTiles));
     h->tile_s.swap(ts);
     h->tile_e.swap(te);
   }
@@ -530,7 +534,7 @@ struct PlanSnap {
   uint32_t L, n_chunks, n_groups, nQ, A;
   uint32_t pw[ALP_MAX_M];
   long long umax_total;
-  std::vector<int> dv, gsum;
+  std::vector<int> dv, dcnt, gsum;
   uint32_t n_groups_u;
   int *d_u, *d_tile_s, *d_bperm, *d_dv, *d_dcnt, *d_gsum;
   uint32_t *d_tile_e, *d_tile_off;
@@ -582,10 +586,11 @@ alp_status get_plan(alp_s *h) {
     memcpy(P->pw, h->pw, sizeof(P->pw));
     P->umax_total = h->umax_total;
     P->dv = h->dv;
+    P->dcnt = h->dcnt;
     P->gsum = h->gsum;
     P->n_groups_u = h->n_groups_u;
     g_plans[key] = P;
-    h->tile_s.clear(); h->tile_e.clear(); h->tile_off.clear(); h->bperm.clear(); h->bu.clear(); h->dcnt.clear();
+    h->tile_s.clear(); h->tile_e.clear(); h->tile_off.clear(); h->bperm.clear(); h->bu.clear();
   }
   h->N = P->N; h->a_llm = P->a_llm; h->b_llm = P->b_llm; h->Ka = P->Ka; h->Kb = P->Kb; h->g0 = P->g0;
   h->g1 = P->g1; h->ng = P->ng; h->umax_a = P->umax_a; h->umax_b = P->umax_b;
@@ -593,6 +598,7 @@ alp_status get_plan(alp_s *h) {
   memcpy(h->pw, P->pw, sizeof(h->pw));
   h->umax_total = P->umax_total;
   h->dv = P->dv;
+  h->dcnt = P->dcnt;
   h->gsum = P->gsum;
   h->n_groups_u = P->n_groups_u;
   h->d_u = P->d_u; h->d_tile_s = P->d_tile_s; h->d_tile_e = P->d_tile_e; h->d_tile_off = P->d_tile_off;
@@ -936,40 +942,77 @@ void fill_finalize(alp_s *h, SearchArgs &a) {
 // arguments with its shared-memory layout, lut geometry and grid; false when not applicable.
 bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, int &grid) {
   if (getenv("ALP_NO_UR") || n < 1 || n > kInlineTargets || a.q_budget || h->from_terms ||
-      h->rows_per_lane != 12 || a.n_bchunks != 1 || a.bchunk_wpad > 34 || hi >= (1ull << 31) ||
-      n * h->M * h->K > 8192)
+      h->rows_per_lane != 12 || hi >= (1ull << 31) || n * h->M * h->K > 8192)
     return false;
+  const int R = a.budget, Kb = h->Kb;
   auto umax = [&](int m) {
     int x = 0;
     for (int k = 0; k < h->K; ++k) x = std::max(x, h->u[(size_t)m * h->K + k]);
     return x;
   };
-  int lb = 0;
-  for (int m = 0; m < h->g1; ++m) lb += umax(m);  // prefix + sort-group LLMs
-  if (h->a_llm >= 0) lb += umax(h->a_llm);
+  // lut span: the prefix, sort-group and a unit sums enter clamped at R + 1 (a clamped sum keeps
+  // the remaining budget negative, i.e. the all-+inf row, exactly like the true sum)
+  int up = 0, ug = 0;
+  for (int m = 0; m < h->g0; ++m) up += umax(m);
+  for (int m = h->g0; m < h->g1; ++m) ug += umax(m);
+  const int lb = std::min(up, R + 1) + std::min(ug, R + 1) + (h->a_llm >= 0 ? std::min(umax(h->a_llm), R + 1) : 0);
   ua = a;
   ua.lut_base = lb;
   ua.lut_n = lb + 1;
-  const int rows = a.D + 1;
+  // b chunks: a short b row (<= 34 options) is one chunk with the k_search row layout; longer rows
+  // are cut into chunks of kUChunkW u-sorted columns, each with its own lut and de-duplicated masked
+  // rows (a chunk has a new row only where the budget threshold falls inside it)
+  int W, wpad, cstride;
+  if (Kb <= 34) {
+    if (a.n_bchunks != 1) return false;
+    W = Kb;
+    wpad = a.bchunk_wpad;
+    cstride = a.row_stride;
+  } else {
+    W = wpad = cstride = kUChunkW;
+  }
+  const int nch = (Kb + W - 1) / W;
+  if (nch > kUMaxChunks) return false;
+  ua.bchunk_w = W;
+  ua.bchunk_wpad = wpad;
+  ua.n_bchunks = nch;
+  ua.u_nch = nch;
+  ua.u_cstride = cstride;
+  ua.row_stride = cstride;
+  ua.u_smem_rows = (n == 1 && nch == 1) ? 1 : 0;
   auto a16 = [](int x) { return (x + 15) & ~15; };
-  // constant-bank layout: gsum, then one block per target (a-options, prefix chunks, lut, rows)
-  ua.u_tbase = a16((int)h->n_groups_u * 4);
+  // constant-bank layout: gsum (every group), then one block per target: a-options, prefix chunks,
+  // then per chunk its lut and rows
+  ua.u_tbase = a16((int)h->n_groups * 4);
   ua.u_off_a = 0;
   ua.u_off_pfx = a16(h->Ka * 16);
-  ua.u_off_lut = a16(ua.u_off_pfx + (int)h->n_chunks * 8);
-  ua.u_off_btab = a16(ua.u_off_lut + ua.lut_n * 8);
-  ua.u_tstride = a16(ua.u_off_btab + rows * a.row_stride * 4);
+  int off = a16(ua.u_off_pfx + (int)h->n_chunks * 8), rows0 = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int c0 = c * W, wc = std::min(W, Kb - c0);
+    int rows = 1, prev = 0;  // row 0: all +inf
+    for (int i = 1; i <= a.D; ++i) {
+      const int len = std::min(std::max(std::min(h->dcnt[i], Kb) - c0, 0), wc);
+      if (len > prev) ++rows;
+      prev = len;
+    }
+    if (c == 0) rows0 = rows;
+    ua.u_off_lut_c[c] = off;
+    off = a16(off + ua.lut_n * 8);
+    ua.u_off_btab_c[c] = off;
+    off = a16(off + rows * cstride * 4);
+  }
+  ua.u_tstride = off;
   if ((long long)ua.u_tbase + (long long)n * ua.u_tstride > kUBytes) return false;
   if (uprep_smem_bytes(ua) > kUPrepSmemMax) return false;
-  // shared memory: the option terms of LLMs 0..g1-1 (+ {0, +inf}) of every target; for a single
-  // target also copies of its lut and masked rows (the mixed groups read them from there)
-  int off = a16(n * (h->g1 * h->K + 2) * 4);
+  // shared memory: the option terms of LLMs 0..g1-1 (+ {0, +inf}) of every target; with u_smem_rows
+  // also copies of the chunk's lut and masked rows (the mixed groups read them from there)
+  off = a16(n * (h->g1 * h->K + 2) * 4);
   ua.off_lut = off;
   ua.off_btab = off;
-  if (n == 1) {
+  if (ua.u_smem_rows) {
     off = a16(off + ua.lut_n * 8);
     ua.off_btab = off;
-    off = a16(off + rows * a.row_stride * 4);
+    off = a16(off + rows0 * cstride * 4);
   }
   ua.smem_bytes = off;
   const long long okey = (1ll << 60) | ((long long)ua.smem_bytes << 8) | ua.bchunk_wpad;
@@ -1021,14 +1064,22 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
   if (lo > hi || hi > items) return fail(ALP_EINVAL, "item range [%llu, %llu) outside [0, %llu)",
                                          (unsigned long long)lo, (unsigned long long)hi, (unsigned long long)items);
-  const size_t nctr = (size_t)n * g.a.n_bchunks;
+  // The uniform-register pair (k_uprep + k_search_u) computes the option terms itself and
+  // accumulates like the fused launch.  It shares one constant bank per device: a search on a
+  // caller workspace whose bank is still in use by another stream's search takes k_search instead
+  // (same keys and counts), so searches on distinct workspaces and streams overlap.
+  SearchArgs ua;
+  int ugrid = 0;
+  const bool ur = !budgets && ur_path(h, g.a, n, hi, ua, ugrid) && !(h->sc.ws && search_u_busy());
+  const bool accum = fused || ur;  // self-resetting accumulators + last-block epilogue (no K1)
+  const size_t nctr = (size_t)n * (ur ? ua.u_nch : g.a.n_bchunks);
   int launches = 0;
   unsigned long long *work = h->sc.work;
-  if (fused) {
+  if (accum) {
     if (nctr > kFusedWork) return fail(ALP_EINTERNAL, "fused search: %zu work counters", nctr);
     FusedArgs &z = g.a.fz;
     z.on = 1;
-    z.finalize = fuse_finalize ? 1 : 0;
+    z.finalize = (fuse_finalize && fused) ? 1 : 0;
     if (!h->from_terms) z.prof = h->dprof();
     for (int i = 0; i < kInlineTargets; ++i) z.tgt[i] = i < n ? targets[i] : 0.0;
     z.tau_fixed = h->from_terms ? h->d_tau_fixed : nullptr;
@@ -1055,7 +1106,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   fill_finalize(h, g.a);
   if (fused_out) g.a.fin.out = fused_out;
   if (first_of_batch) CU(cudaEventRecord(h->ev0, st));
-  if (hi > lo || fused) {  // the fused launch also computes the terms and writes keys/counts
+  if (hi > lo || accum) {  // the fused / UR launch also computes the terms and writes keys/counts
     g.a.t_begin = 0; g.a.t_end = n; g.a.c_begin = 0; g.a.c_end = g.a.n_bchunks;
     g.a.work = work;
     // ~16 grabs per warp; the last ~1/8 of the items go in grabs a quarter that size (tail balance;
@@ -1066,12 +1117,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     g.a.grab2 = std::max(1, g.a.grab / 4);
     g.a.grab_t1 = (n_items - n_items / 8) / (uint64_t)g.a.grab;
     static const bool dbg = getenv("ALP_DBG_TS") != nullptr;  // per-block timeline (diagnostics)
-    SearchArgs ua;
-    int ugrid = 0;
-    // the uniform-register path shares one constant bank per device: a search on a caller
-    // workspace whose bank is still in use by another stream's search takes k_search instead
-    // (same keys and counts), so searches on distinct workspaces and streams overlap
-    const bool ur = fused && ur_path(h, g.a, n, hi, ua, ugrid) && !(h->sc.ws && search_u_busy());
+    if (ur && !ur_path(h, g.a, n, hi, ua, ugrid)) return fail(ALP_EINTERNAL, "uniform-register geometry changed");
     const int dgrid = ur ? ugrid : g.grid;
     if (dbg) {
       CU(h->g_dbg.ensure((size_t)dgrid * 8));

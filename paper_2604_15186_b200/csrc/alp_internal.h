@@ -15,6 +15,8 @@ constexpr int kThreads = 256;            // threads per search block
 constexpr uint32_t kPfxTableMax = 4096;  // prefix chunks tabulated in shared memory (8 B each)
 constexpr uint32_t kDummy = 0xFFFFFFFFu; // padded row marker in the tile list
 constexpr unsigned long long kKeyNone = 0x7FFFFFFFFFFFFFFFull;  // INT64_MAX: nothing feasible
+constexpr int kUMaxChunks = 16;          // b chunks of the uniform-register path (K <= 1024, 64 columns each)
+constexpr int kUChunkW = 64;             // b chunk width of the uniform-register path for long b rows
 constexpr int kInlineTargets = 8;        // targets passed in kernel parameters (no H2D copy)
 constexpr int kFusedMaxTerms = 1024;     // max option terms (M*K) recomputed per block by the fused launch
 constexpr uint64_t kFusedMaxRescan = 65536;  // max finalize re-scan (Ka*Kb) done by one block
@@ -137,12 +139,17 @@ struct SearchArgs {
   unsigned long long *dbg_ts;  // [grid][8] %globaltimer stamps per block (ALP_DBG_TS) or nullptr
   // uniform-register path (k_uprep + k_search_u): tables in the constant bank
   uint32_t n_groups_u;   // warp groups [0, n_groups_u) have one unit sum (uniform remaining budget)
-  const int *gsum;       // [n_groups_u] their unit sums (device, plan)
-  int lut_base;          // lut index of remaining budget r = r + lut_base - R (>= 0 for every r reached)
+  const int *gsum;       // [n_groups] their unit sums; mixed groups: their smallest tile sum (plan)
+  int lut_base;          // lut index of remaining budget r = r + lut_base - R (>= 0 for every r reached;
+                         // unit sums enter clamped at R + 1, which keeps an over-budget r negative)
   int lut_n;             // lut entries (lut_base + 1)
   // byte layout of the constant-bank tables: gsum at 0; target t's block at u_tbase + t*u_tstride
-  // with the a-options, prefix chunks, lut and masked rows at these offsets inside it
-  int u_tbase, u_tstride, u_off_a, u_off_pfx, u_off_lut, u_off_btab;
+  // with the a-options and prefix chunks at these offsets inside it, then per b chunk c its lut and
+  // its masked rows (u_off_lut_c[c], u_off_btab_c[c]; rows of u_cstride floats)
+  int u_tbase, u_tstride, u_off_a, u_off_pfx;
+  int u_off_lut_c[kUMaxChunks], u_off_btab_c[kUMaxChunks];
+  int u_nch, u_cstride;  // b chunks (each bchunk_w u-sorted columns, padded to bchunk_wpad) and row stride
+  int u_smem_rows;       // 1: the mixed groups read the (single) chunk's lut and rows from shared memory
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
   int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it

@@ -26,8 +26,11 @@ struct UView {
   __device__ __forceinline__ const float2 &pfx(uint32_t c) const {
     return reinterpret_cast<const float2 *>(t + P.u_off_pfx)[c];
   }
-  __device__ __forceinline__ const int2 &lut(int x) const { return reinterpret_cast<const int2 *>(t + P.u_off_lut)[x]; }
-  __device__ __forceinline__ const float *btab() const { return reinterpret_cast<const float *>(t + P.u_off_btab); }
+  // b chunk c: its lut (remaining budget -> {row offset in floats, #finite entries}) and masked rows
+  __device__ __forceinline__ const int2 &lut(int c, int x) const {
+    return reinterpret_cast<const int2 *>(t + P.u_off_lut_c[c])[x];
+  }
+  __device__ __forceinline__ const float *btab(int c) const { return reinterpret_cast<const float *>(t + P.u_off_btab_c[c]); }
 };
 
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
@@ -50,6 +53,10 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   int *s_bp = s_fin + (D + 1);                              // [Kb] bperm
   int *s_u = s_bp + Kb;                                     // [g0*K] prefix units
   int *s_ua = s_u + P.g0 * K;                               // [Ka] a units
+  int *s_crow = s_fin;                                      // [D+1] chunk row of each budget row (reuses s_fin)
+  int *s_clen = s_ua + P.Ka;                                // [D+1] length of each chunk row
+  int *s_cfin = s_clen + (D + 1);                           // [D+1] finite entries of each chunk row
+  __shared__ int s_rows;                                    // chunk rows
   auto stamp = [&](int slot) {  // ALP_DBG_TS: slots 5-7 of blocks 0 and 1 (k_search_u uses 0-4)
     if (P.dbg_ts && tid == 0) {
       unsigned long long g;
@@ -62,7 +69,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   // shared memory instead of L2/DRAM)
   const DevProfiles &gp = P.fz.prof;
   const int MT = gp.M * gp.nT;
-  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_ua + P.Ka) + 7) & ~uintptr_t(7));
+  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_cfin + (D + 1)) + 7) & ~uintptr_t(7));
   DevProfiles sp = gp;
   {
     double *d = s_pd;
@@ -97,7 +104,8 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   for (int i = tid; i < P.g0 * K; i += nt) cp_async4(s_u + i, P.u + i);
   if (P.a_llm >= 0)
     for (int i = tid; i < P.Ka; i += nt) cp_async4(s_ua + i, P.u + P.a_llm * K + i);
-  for (uint32_t g = tid; g < P.n_groups_u; g += nt) reinterpret_cast<int *>(T)[g] = P.gsum[g];
+  // group unit sums, clamped at R + 1 (an over-budget sum only has to keep r negative)
+  for (uint32_t g = tid; g < P.n_groups; g += nt) reinterpret_cast<int *>(T)[g] = min(P.gsum[g], R + 1);
   cp_async_wait();
   __syncthreads();
   for (int i = tid; i < NT * MK; i += nt) {
@@ -120,9 +128,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     unsigned char *tb = T + P.u_tbase + t * P.u_tstride;
     float2 *pfx = reinterpret_cast<float2 *>(tb + P.u_off_pfx);
     float4 *ta4 = reinterpret_cast<float4 *>(tb + P.u_off_a);
-    int2 *lut = reinterpret_cast<int2 *>(tb + P.u_off_lut);
-    float *btab = reinterpret_cast<float *>(tb + P.u_off_btab);
-    // prefix chunks: canonical sum over LLMs 0..g0-1
+    // prefix chunks: canonical sum over LLMs 0..g0-1 (units clamped at R + 1)
     for (uint32_t c = tid; c < P.n_chunks; c += nt) {
       float pa = 0.f;
       int U = 0;
@@ -131,38 +137,62 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
         pa = __fadd_rn(pa, st[m * K + d]);
         U += s_u[m * K + d];
       }
-      pfx[c] = make_float2(pa, __int_as_float(U));
+      pfx[c] = make_float2(pa, __int_as_float(min(U, R + 1)));
     }
     for (int a = tid; a < P.Ka; a += nt) {
       const float ta = P.a_llm >= 0 ? st[P.a_llm * K + a] : 0.f;
-      const int ua = P.a_llm >= 0 ? s_ua[a] : 0;
+      const int ua = P.a_llm >= 0 ? min(s_ua[a], R + 1) : 0;
       const int feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
       ta4[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), 0.f);
     }
-    // masked rows: row i holds the u-sorted b columns with u <= dv[i-1] (row 0 none), +inf elsewhere
+    // u-sorted b terms
     for (int j = tid; j < Kb; j += nt) s_bs[j] = st[P.b_llm * K + s_bp[j]];
     __syncthreads();
-    for (int row = tid; row <= D; row += nt) {
-      int f = 0;
-      for (int j = 0; j < s_len[row]; ++j) f += (s_bs[j] < __int_as_float(0x7f800000)) ? 1 : 0;
-      s_fin[row] = f;
-    }
-    for (int i = tid; i < (D + 1) * P.bchunk_wpad; i += nt) {
-      const int row = i / P.bchunk_wpad, j = i % P.bchunk_wpad;
-      btab[row * P.row_stride + j] = (j < s_len[row]) ? s_bs[j] : __int_as_float(0x7f800000);
-    }
-    __syncthreads();
-    // lut: index x <-> remaining budget r = R - lut_base + x; row = #{distinct b unit values <= r}
-    for (int x = tid; x < P.lut_n; x += nt) {
-      const int r = R - P.lut_base + x;
-      int lo = 0, hi = D;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
+    // per b chunk: budget row i (the u-sorted columns with u <= dv[i-1]; row 0 none) restricted to
+    // the chunk's columns; equal restrictions share one chunk row (the length is non-decreasing in i)
+    for (int c = 0; c < P.u_nch; ++c) {
+      const int c0 = c * P.bchunk_w, wc = min(P.bchunk_w, Kb - c0);
+      if (tid == 0) {
+        int rows = 0, prev = -1;
+        for (int i = 0; i <= D; ++i) {
+          const int len = min(max(s_len[i] - c0, 0), wc);
+          if (len > prev) {
+            s_clen[rows] = len;
+            ++rows;
+          }
+          s_crow[i] = rows - 1;
+          prev = len;
+        }
+        s_rows = rows;
       }
-      lut[x] = make_int2(lo * P.row_stride, s_fin[lo]);
+      __syncthreads();
+      const int rows = s_rows;
+      for (int row = tid; row < rows; row += nt) {
+        int f = 0;
+        for (int j = 0; j < s_clen[row]; ++j) f += (s_bs[c0 + j] < __int_as_float(0x7f800000)) ? 1 : 0;
+        s_cfin[row] = f;
+      }
+      float *btab = reinterpret_cast<float *>(tb + P.u_off_btab_c[c]);
+      for (int i = tid; i < rows * P.u_cstride; i += nt) {
+        const int row = i / P.u_cstride, j = i % P.u_cstride;
+        btab[i] = (j < s_clen[row]) ? s_bs[c0 + j] : __int_as_float(0x7f800000);
+      }
+      __syncthreads();
+      // lut: index x <-> remaining budget r = R - lut_base + x; budget row = #{distinct b unit
+      // values <= r}, mapped to its chunk row
+      int2 *lut = reinterpret_cast<int2 *>(tb + P.u_off_lut_c[c]);
+      for (int x = tid; x < P.lut_n; x += nt) {
+        const int r = R - P.lut_base + x;
+        int lo = 0, hi = D;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
+        }
+        const int row = s_crow[lo];
+        lut[x] = make_int2(row * P.u_cstride, s_cfin[row]);
+      }
+      __syncthreads();  // s_clen / s_crow / s_cfin / s_rows reused by the next chunk and target
     }
-    __syncthreads();  // s_bs / s_fin reused by the next target
   }
   stamp(8 + 5);
 }
@@ -217,14 +247,15 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
   // single target: shared-memory copies of the lut and masked rows for the mixed groups
   int2 *s_lut = reinterpret_cast<int2 *>(smem + P.off_lut);
   float *s_btab = reinterpret_cast<float *>(smem + P.off_btab);
-  const bool smem_rows = P.n_targets == 1;
+  const bool smem_rows = P.u_smem_rows;  // single target, single b chunk (its rows: D + 1)
   if (smem_rows) {
     const UView gv0{ug + P.u_tbase, P};
-    const int *lut_w = reinterpret_cast<const int *>(&gv0.lut(0));
+    const int *lut_w = reinterpret_cast<const int *>(&gv0.lut(0, 0));
     int *s_lut_w = reinterpret_cast<int *>(s_lut);
     for (int i = lane; i < 2 * P.lut_n; i += 32) s_lut_w[i] = __ldca(lut_w + i);
-    for (int i = lane; i < (P.D + 1) * P.row_stride; i += 32) s_btab[i] = __ldca(gv0.btab() + i);
+    for (int i = lane; i < (P.D + 1) * P.u_cstride; i += 32) s_btab[i] = __ldca(gv0.btab(0) + i);
   }
+  const int R1 = P.budget + 1;  // unit sums enter the lut index clamped at R + 1
   cp_async_wait();
   __syncwarp();
   stamp(4);
@@ -237,9 +268,14 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
     uint32_t best_seg = 0xffffffffu;
     unsigned long long cnt = 0ull;
     float Qr[T], acc[T];
+    for (int c = 0; c < P.u_nch; ++c) {  // b-chunk phases of the target (C4: one)
     // dynamic item tickets: lane 0 takes the next ticket while the current item is evaluated;
     // redux.sync broadcasts it into a uniform register (ptxas keeps the derived indices uniform)
-    unsigned long long *ctr = P.work + t;
+    unsigned long long *ctr = P.work + t * P.u_nch + c;
+    // the chunk's masked rows as b pairs: float2 indexing from the 16-byte aligned bank base makes
+    // every address provably 8-byte aligned, so ptxas loads each pair with ONE LDCU.64 (a float* +
+    // offset form is split into two scalar LDCU)
+    const float2 *rows_u = cu_pairs + ((P.u_tbase + t * P.u_tstride + P.u_off_btab_c[c]) >> 3);
     unsigned tnext = 0xffffffffu;
     if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
     for (;;) {
@@ -253,32 +289,33 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       const uint32_t grp = tq - chunk * P.n_groups;
       const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
       const float2 pf = cv.pfx(chunk);
-      const int upfx = __float_as_int(pf.y);
+      const int upfx = __float_as_int(pf.y);       // clamped at R + 1
       const uint32_t tile = grp * kWarpTiles + lane;
       const unsigned nfin = load_tile<T>(P, tau_b, pf.x, tile, Qr, acc);
       unsigned c32 = 0;
-      if (grp < P.n_groups_u) {
-        // warp-uniform remaining budget: uniform-register b operands
-        const int xg = P.lut_base - upfx - gsum[grp];
-#pragma unroll 2
+      const int gs = gsum[grp];                     // clamped at R + 1
+      if (grp < P.n_groups_u || gs + upfx >= R1) {
+        // warp-uniform remaining budget (one unit sum, or a mixed group whose every lane is over
+        // budget, where every row is the all-+inf row 0): uniform-register b operands
+        const int xg = P.lut_base - upfx - gs;
+        // a-loop unrolled by 2 for short rows; long rows (64-column chunks: an ~800-instruction body)
+        // stay rolled so the uniform and mixed loops together fit the 32 KB instruction cache
+        constexpr int kUA = NB4 > 8 ? 1 : 2;
+#pragma unroll(kUA)
         for (int a = a0; a < a1; ++a) {
           const float4 av = cv.a(a);
-          const int2 lu = cv.lut(xg - __float_as_int(av.y));
+          const int2 lu = cv.lut(c, xg - __float_as_int(av.y));
           c32 += (unsigned)(lu.y * __float_as_int(av.z));
           float Qa[T];
 #pragma unroll
           for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-          // float2 indexing from the 16-byte aligned bank base: the address is provably 8-byte
-          // aligned, so ptxas loads each b pair with ONE LDCU.64 (a float* + offset form is split
-          // into two scalar LDCU)
-          eval_row_u<NB4, TAIL2>(cu_pairs + ((P.u_tbase + t * P.u_tstride + P.u_off_btab) >> 3) + (lu.x >> 1), Qa,
-                                 acc);
+          eval_row_u<NB4, TAIL2>(rows_u + (lu.x >> 1), Qa, acc);
         }
       } else {
         // mixed group: the lanes' own remaining budgets, rows from the global staging copy of the
         // tables (L1-resident; a different memory space keeps the compiler from merging this loop
         // with the uniform one into a single vector loop)
-        const int xl = P.lut_base - upfx - __ldg(P.tile_s + tile);
+        const int xl = P.lut_base - upfx - min(__ldg(P.tile_s + tile), R1);
         if (smem_rows) {
           const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
           // not unrolled: the smaller mixed-group code leaves the instruction cache to the uniform
@@ -297,12 +334,12 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
 #pragma unroll 1
         for (int a = a0; a < a1; ++a) {
           const float4 av = cv.a(a);
-          const int2 lu = __ldg(&gv.lut(xl - __float_as_int(av.y)));
+          const int2 lu = __ldg(&gv.lut(c, xl - __float_as_int(av.y)));
           c32 += (unsigned)(lu.y * __float_as_int(av.z));
           float Qa[T];
 #pragma unroll
           for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-          const float *rb = gv.btab() + lu.x;
+          const float *rb = gv.btab(c) + lu.x;
 #pragma unroll
           for (int g = 0; g < NB4; ++g) eval4<T>(__ldg(reinterpret_cast<const float4 *>(rb) + g), Qa, acc);
           if constexpr (TAIL2) eval2<T>(__ldg(reinterpret_cast<const float2 *>(rb + 4 * NB4)), Qa, acc);
@@ -310,6 +347,7 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       }
       cnt += (unsigned long long)c32 * nfin;
       fold_rows<T>(P, acc, tile, chunk, q, best, best_seg);  // segment: from a-range q to the row's end
+    }
     }
     unsigned long long key = (best < __int_as_float(0x7f800000))
                                  ? ((unsigned long long)__float_as_uint(best) << 32) | best_seg : kKeyNone;
@@ -397,15 +435,23 @@ static int occ_u(const SearchArgs &a) {
 }
 
 
+// b-chunk widths of the uniform-register path: the short-row specialisations (<= 34) and kUChunkW
+#define ALP_DISPATCH_U(CALL)                                 \
+  do {                                                       \
+    static_assert(kUChunkW == 64, "chunk width dispatch");   \
+    if (a.bchunk_wpad == 64) return CALL(12, 16, false);     \
+    ALP_DISPATCH_W(CALL, 12);                                \
+  } while (0)
+
 static cudaError_t launch_u_search(const SearchArgs &a, int grid, cudaStream_t st) {
 #define CALL(T_, N, T2) launch_u<N, T2>(a, grid, st)
-  ALP_DISPATCH_W(CALL, 12);
+  ALP_DISPATCH_U(CALL);
 #undef CALL
 }
 
 static const void *search_u_fn(const SearchArgs &a) {
 #define CALL(T_, N, T2) fn_u<N, T2>()
-  ALP_DISPATCH_W(CALL, 12);
+  ALP_DISPATCH_U(CALL);
 #undef CALL
 }
 
@@ -493,7 +539,7 @@ static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int g
 size_t uprep_smem_bytes(const SearchArgs &a) {
   const DevProfiles &pr = a.fz.prof;
   const int MT = pr.M * pr.nT;
-  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(3 * a.D + 2 + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
+  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(5 * a.D + 4 + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
          (size_t)(2 * pr.M + MT + 2 * pr.n_pts) * 8 +
          (size_t)(pr.nS + pr.nT + pr.nR + MT + 1 + (pr.min_units ? MT : 0)) * 4;
 }
@@ -563,7 +609,7 @@ bool search_u_busy() {
 
 int search_u_max_blocks_per_sm(const SearchArgs &a) {
 #define CALL(T_, N, T2) occ_u<N, T2>(a)
-  ALP_DISPATCH_W(CALL, 12);
+  ALP_DISPATCH_U(CALL);
 #undef CALL
 }
 
