@@ -49,14 +49,14 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   float *s_bs = s_t + NT * MK;                              // [Kb] u-sorted b terms (per target, reused)
   int *s_dv = reinterpret_cast<int *>(s_bs + Kb);           // [D]
   int *s_len = s_dv + D;                                    // [D+1] masked-row lengths (dcnt)
-  int *s_fin = s_len + (D + 1);                             // [D+1] finite entries per row
-  int *s_bp = s_fin + (D + 1);                              // [Kb] bperm
+  int *s_bp = s_len + (D + 1);                              // [Kb] bperm
   int *s_u = s_bp + Kb;                                     // [g0*K] prefix units
   int *s_ua = s_u + P.g0 * K;                               // [Ka] a units
-  int *s_crow = s_fin;                                      // [D+1] chunk row of each budget row (reuses s_fin)
-  int *s_clen = s_ua + P.Ka;                                // [D+1] length of each chunk row
-  int *s_cfin = s_clen + (D + 1);                           // [D+1] finite entries of each chunk row
-  __shared__ int s_rows;                                    // chunk rows
+  const int NC = P.u_nch, D1 = D + 1;
+  int *s_crow = s_ua + P.Ka;                                // [NC][D+1] chunk row of each budget row
+  int *s_clen = s_crow + NC * D1;                           // [NC][D+1] length of each chunk row
+  int *s_cfin = s_clen + NC * D1;                           // [NC][D+1] finite entries of each chunk row
+  __shared__ int s_rows[kUMaxChunks];                       // rows per chunk
   auto stamp = [&](int slot) {  // ALP_DBG_TS: slots 5-7 of blocks 0 and 1 (k_search_u uses 0-4)
     if (P.dbg_ts && tid == 0) {
       unsigned long long g;
@@ -69,7 +69,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   // shared memory instead of L2/DRAM)
   const DevProfiles &gp = P.fz.prof;
   const int MT = gp.M * gp.nT;
-  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_cfin + (D + 1)) + 7) & ~uintptr_t(7));
+  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_cfin + NC * D1) + 7) & ~uintptr_t(7));
   DevProfiles sp = gp;
   {
     double *d = s_pd;
@@ -149,50 +149,54 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     for (int j = tid; j < Kb; j += nt) s_bs[j] = st[P.b_llm * K + s_bp[j]];
     __syncthreads();
     // per b chunk: budget row i (the u-sorted columns with u <= dv[i-1]; row 0 none) restricted to
-    // the chunk's columns; equal restrictions share one chunk row (the length is non-decreasing in i)
-    for (int c = 0; c < P.u_nch; ++c) {
+    // the chunk's columns; equal restrictions share one chunk row (the length is non-decreasing in
+    // i).  All chunks at once: one thread per chunk de-duplicates, then every (chunk, row) pair,
+    // row element and lut entry in parallel (three barriers in all, not three per chunk).
+    for (int c = tid; c < NC; c += nt) {
       const int c0 = c * P.bchunk_w, wc = min(P.bchunk_w, Kb - c0);
-      if (tid == 0) {
-        int rows = 0, prev = -1;
-        for (int i = 0; i <= D; ++i) {
-          const int len = min(max(s_len[i] - c0, 0), wc);
-          if (len > prev) {
-            s_clen[rows] = len;
-            ++rows;
-          }
-          s_crow[i] = rows - 1;
-          prev = len;
+      int rows = 0, prev = -1;
+      for (int i = 0; i <= D; ++i) {
+        const int len = min(max(s_len[i] - c0, 0), wc);
+        if (len > prev) {
+          s_clen[c * D1 + rows] = len;
+          ++rows;
         }
-        s_rows = rows;
+        s_crow[c * D1 + i] = rows - 1;
+        prev = len;
       }
-      __syncthreads();
-      const int rows = s_rows;
-      for (int row = tid; row < rows; row += nt) {
-        int f = 0;
-        for (int j = 0; j < s_clen[row]; ++j) f += (s_bs[c0 + j] < __int_as_float(0x7f800000)) ? 1 : 0;
-        s_cfin[row] = f;
-      }
+      s_rows[c] = rows;
+    }
+    __syncthreads();
+    for (int i = tid; i < NC * D1; i += nt) {
+      const int c = i / D1, row = i % D1, c0 = c * P.bchunk_w;
+      if (row >= s_rows[c]) continue;
+      int f = 0;
+      for (int j = 0; j < s_clen[i]; ++j) f += (s_bs[c0 + j] < __int_as_float(0x7f800000)) ? 1 : 0;
+      s_cfin[i] = f;
+    }
+    __syncthreads();
+    for (int c = 0; c < NC; ++c) {
+      const int c0 = c * P.bchunk_w, rows = s_rows[c];
       float *btab = reinterpret_cast<float *>(tb + P.u_off_btab_c[c]);
       for (int i = tid; i < rows * P.u_cstride; i += nt) {
         const int row = i / P.u_cstride, j = i % P.u_cstride;
-        btab[i] = (j < s_clen[row]) ? s_bs[c0 + j] : __int_as_float(0x7f800000);
+        btab[i] = (j < s_clen[c * D1 + row]) ? s_bs[c0 + j] : __int_as_float(0x7f800000);
       }
-      __syncthreads();
-      // lut: index x <-> remaining budget r = R - lut_base + x; budget row = #{distinct b unit
-      // values <= r}, mapped to its chunk row
-      int2 *lut = reinterpret_cast<int2 *>(tb + P.u_off_lut_c[c]);
-      for (int x = tid; x < P.lut_n; x += nt) {
-        const int r = R - P.lut_base + x;
-        int lo = 0, hi = D;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
-        }
-        const int row = s_crow[lo];
-        lut[x] = make_int2(row * P.u_cstride, s_cfin[row]);
-      }
-      __syncthreads();  // s_clen / s_crow / s_cfin / s_rows reused by the next chunk and target
     }
+    // lut: index x <-> remaining budget r = R - lut_base + x; budget row = #{distinct b unit values
+    // <= r}, mapped to the chunk row
+    for (int i = tid; i < NC * P.lut_n; i += nt) {
+      const int c = i / P.lut_n, x = i % P.lut_n;
+      const int r = R - P.lut_base + x;
+      int lo = 0, hi = D;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
+      }
+      const int row = s_crow[c * D1 + lo];
+      reinterpret_cast<int2 *>(tb + P.u_off_lut_c[c])[x] = make_int2(row * P.u_cstride, s_cfin[c * D1 + row]);
+    }
+    __syncthreads();  // s_bs and the chunk tables are reused by the next target
   }
   stamp(8 + 5);
 }
@@ -539,7 +543,7 @@ static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int g
 size_t uprep_smem_bytes(const SearchArgs &a) {
   const DevProfiles &pr = a.fz.prof;
   const int MT = pr.M * pr.nT;
-  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(5 * a.D + 4 + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
+  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(2 * a.D + 1 + 3 * a.u_nch * (a.D + 1) + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
          (size_t)(2 * pr.M + MT + 2 * pr.n_pts) * 8 +
          (size_t)(pr.nS + pr.nT + pr.nR + MT + 1 + (pr.min_units ? MT : 0)) * 4;
 }

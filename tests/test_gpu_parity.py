@@ -737,6 +737,40 @@ def test_uniform_register_path_random_vs_bruteforce(P, seed):
         _check_winner(P, alp, I, lam, budget, r)
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_uniform_register_long_rows_vs_bruteforce(P, seed, monkeypatch):
+    """Long b rows (K > 34 options per LLM) on the uniform-register path: 64-column b chunks with
+    per-chunk luts and de-duplicated masked rows, a ragged last chunk, unit sums clamped at R + 1,
+    budgets from 0 to above the total -- against brute force (O1) and the k_search path."""
+    rng = np.random.default_rng(9100 + seed)
+    M = int(rng.integers(1, 4))
+    S = sorted(set(int(x) for x in rng.integers(1, 9, size=int(rng.integers(2, 6)))))
+    T = [1, 2, 4, 8][: int(rng.integers(1, 5))]
+    R = list(range(1, int(rng.integers(4, 17))))
+    K = len(S) * len(T) * len(R)
+    while K <= 34:
+        R.append(R[-1] + 1)
+        K = len(S) * len(T) * len(R)
+    while K ** M > 4_000_000:
+        M -= 1
+    budgets = [0, int(rng.integers(1, 20)), int(rng.integers(20, 200)), 10_000]
+    d = generate.random_instance(9100 + seed, M=M, F=8, S=S, T=T, R=R, budget=budgets[1],
+                                 min_units=bool(seed % 3 == 2))
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (0.05, 0.6):
+        for B in budgets:
+            r = alp.search(lam, B)
+            assert alp.last_path == "k_search_u", (K, M)
+            o = oracle.search(I, lam, B, threads=8)
+            _same(r, o.found, o.latency_key, o.index, o.count, (seed, K, M, lam, B))
+            _check_winner(P, alp, I, lam, B, r)
+            monkeypatch.setenv("ALP_NO_UR", "1")
+            f = alp.search(lam, B)
+            monkeypatch.delenv("ALP_NO_UR")
+            assert (f.index, f.feasible_count, f.latency_key) == (r.index, r.feasible_count, r.latency_key)
+
+
 def test_uniform_register_path_concurrent_streams(P):
     """Two handles with different problems search on two streams at once through the shared
     constant-bank tables: the ordering event keeps them from overwriting each other's tables."""
