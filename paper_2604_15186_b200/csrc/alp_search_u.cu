@@ -324,15 +324,26 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
           const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
           // not unrolled: the smaller mixed-group code leaves the instruction cache to the uniform
           // loop (C4 0.4763 vs 0.4784 ms with unroll 2)
+          // the lanes' lut indices span [xlo, xhi] (uniform, by redux); the lut is monotone in its
+          // index, so where lut(xlo - u_a) and lut(xhi - u_a) name the same masked row every lane
+          // uses that row: evaluated with uniform-register b operands like a uniform group
+          const int xlo = __reduce_min_sync(0xffffffffu, xl), xhi = __reduce_max_sync(0xffffffffu, xl);
 #pragma unroll 1
           for (int a = a0; a < a1; ++a) {
             const float4 av = cv.a(a);
-            const int2 lu = s_lut[xl - __float_as_int(av.y)];
-            c32 += (unsigned)(lu.y * __float_as_int(av.z));
+            const int2 l0 = cv.lut(c, xlo - __float_as_int(av.y));
+            const int2 l1 = cv.lut(c, xhi - __float_as_int(av.y));
             float Qa[T];
 #pragma unroll
             for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], av.x);
-            eval_row<T, NB4, TAIL2>(bbase + 4u * (uint32_t)lu.x, Qa, acc, 0);
+            if (l0.x == l1.x) {
+              c32 += (unsigned)(l0.y * __float_as_int(av.z));
+              eval_row_u<NB4, TAIL2>(rows_u + (l0.x >> 1), Qa, acc);
+            } else {
+              const int2 lu = s_lut[xl - __float_as_int(av.y)];
+              c32 += (unsigned)(lu.y * __float_as_int(av.z));
+              eval_row<T, NB4, TAIL2>(bbase + 4u * (uint32_t)lu.x, Qa, acc, 0);
+            }
           }
         } else
 #pragma unroll 1

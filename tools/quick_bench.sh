@@ -1,7 +1,7 @@
 #!/bin/bash
 # Quick A/B measurement (one GPU): GPU parity tests + C4/C3 bench lines without the CPU leg.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 900 python -m pytest tests -m gpu -q -x ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
 tail -2 gpurun_out/pytest_gpu.txt
 for w in ${WORKLOADS:-C4 C3}; do
   timeout 600 python bench.py --workload $w --steps ${STEPS:-100} --warmup 5 --e2e-steps 2 --no-cpu-baseline > gpurun_out/qb_$w.json 2> gpurun_out/qb_$w.err
