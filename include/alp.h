@@ -75,6 +75,16 @@ typedef struct {
   const double *tmax;           /* [M*nT] saturation throughput or NULL */
   const int32_t *min_units;     /* [M*nT] memory floor in units per shard, or NULL */
   int32_t pct;                  /* alp_percentile used by this handle */
+  /* Optional profiles MEASURED at a share (reading R2, "measured profiles always win"):
+   * curve c = (m*nT + t)*nS + s (LLM m, tp index t, share index s) has points meas_off[c] ..
+   * meas_off[c+1]-1; an empty curve means "not measured" (the base curve is capacity-scaled).  A
+   * measured curve is used verbatim: lookup at the per-replica rate, capacity d*T_f, no 1/f factor.
+   * Same rules as the base curves (rates strictly increasing, latencies > 0 non-decreasing,
+   * meas_tmax[c] >= the last rate or NULL = the last rate).  meas_off == NULL: none measured. */
+  const int32_t *meas_off;      /* [M*nT*nS+1] */
+  const double *meas_rate;      /* [meas_off[M*nT*nS]] requests/s */
+  const double *meas_lat[4];    /* per alp_percentile column; the selected one must be present */
+  const double *meas_tmax;      /* [M*nT*nS] or NULL */
 } alp_desc;
 
 /* One search result (all fields host-side after the call returns). */

@@ -42,7 +42,8 @@ class _Inst(ctypes.Structure):
                 ("nR", ctypes.c_int), ("n", ctypes.c_void_p), ("p", ctypes.c_void_p), ("S", ctypes.c_void_p),
                 ("T", ctypes.c_void_p), ("R", ctypes.c_void_p), ("prof_off", ctypes.c_void_p),
                 ("rate", ctypes.c_void_p), ("lat", ctypes.c_void_p), ("tmax", ctypes.c_void_p),
-                ("min_units", ctypes.c_void_p)]
+                ("min_units", ctypes.c_void_p), ("meas_off", ctypes.c_void_p), ("mrate", ctypes.c_void_p),
+                ("mlat", ctypes.c_void_p), ("mtmax", ctypes.c_void_p)]
 
 
 _lib = None
@@ -89,6 +90,10 @@ class Instance:
     min_units: np.ndarray | None
     budget: int
     raw: dict
+    meas_off: np.ndarray | None = None   # measured per-share curves (R2), CSR over (m, t_i, s_i)
+    mrate: np.ndarray | None = None
+    mlat: np.ndarray | None = None
+    mtmax: np.ndarray | None = None
 
     @property
     def K(self) -> int:
@@ -102,7 +107,9 @@ class Instance:
         return _Inst(self.M, self.F, len(self.S), len(self.T), len(self.R), self.n.ctypes.data, self.p.ctypes.data,
                      self.S.ctypes.data, self.T.ctypes.data, self.R.ctypes.data, self.prof_off.ctypes.data,
                      self.rate.ctypes.data, self.lat.ctypes.data, self.tmax.ctypes.data,
-                     self.min_units.ctypes.data if self.min_units is not None else None)
+                     self.min_units.ctypes.data if self.min_units is not None else None,
+                     *((self.meas_off.ctypes.data, self.mrate.ctypes.data, self.mlat.ctypes.data,
+                        self.mtmax.ctypes.data) if self.meas_off is not None else (None, None, None, None)))
 
 
 def from_json(d: dict[str, Any], percentile: str | None = None) -> Instance:
@@ -117,13 +124,32 @@ def from_json(d: dict[str, Any], percentile: str | None = None) -> Instance:
             tmax.append(c["tmax"] if c.get("tmax") is not None else c["rate"][-1])
             off.append(len(rate))
     mu = d.get("min_units")
-    return Instance(M=M, F=d["F"], S=np.asarray(d["share_units"], np.int32), T=np.asarray(T, np.int32),
-                    R=np.asarray(d["replicas"], np.int32), n=np.asarray(d["n"], np.float64),
-                    p=np.asarray(d["p"], np.float64), prof_off=np.asarray(off, np.int32),
-                    rate=np.asarray(rate, np.float64), lat=np.asarray(lat, np.float64),
-                    tmax=np.asarray(tmax, np.float64),
-                    min_units=None if mu is None else np.asarray(mu, np.int32).reshape(-1),
-                    budget=int(d["budget_units"]), raw=d)
+    I = Instance(M=M, F=d["F"], S=np.asarray(d["share_units"], np.int32), T=np.asarray(T, np.int32),
+                 R=np.asarray(d["replicas"], np.int32), n=np.asarray(d["n"], np.float64),
+                 p=np.asarray(d["p"], np.float64), prof_off=np.asarray(off, np.int32),
+                 rate=np.asarray(rate, np.float64), lat=np.asarray(lat, np.float64),
+                 tmax=np.asarray(tmax, np.float64),
+                 min_units=None if mu is None else np.asarray(mu, np.int32).reshape(-1),
+                 budget=int(d["budget_units"]), raw=d)
+    meas = d.get("measured") or []
+    if meas:  # R2: curves measured at (LLM, tp index, share index) -- SPEC.md:204
+        nT, nS = len(T), len(d["share_units"])
+        by = {(c["llm"], c["tp_index"], c["share_index"]): c for c in meas}
+        moff, mrate, mlat, mtmax = [0], [], [], []
+        for m in range(M):
+            for ti in range(nT):
+                for si in range(nS):
+                    c = by.get((m, ti, si))
+                    if c is not None:
+                        mrate += c["rate"]
+                        mlat += c["lat"][pct]
+                    mtmax.append((c["tmax"] if c.get("tmax") is not None else c["rate"][-1]) if c else 0.0)
+                    moff.append(len(mrate))
+        I.meas_off = np.asarray(moff, np.int32)
+        I.mrate = np.asarray(mrate, np.float64)
+        I.mlat = np.asarray(mlat, np.float64)
+        I.mtmax = np.asarray(mtmax, np.float64)
+    return I
 
 
 def lookup(rates, lats, x: float) -> float:

@@ -20,6 +20,14 @@
  *     term  = (L / f) * (n_m / p_m)             Eq. 1 contribution L_m(lambda n_m) n_m/p_m
  *     tau   = ok ? (float)term : +INF           RNE to binary32 (R7)
  *     u     = s_units * t * d                   GPU units
+ *   A profile MEASURED at (m, t, share s) replaces the scaled one (R2: "exact pass-through
+ *   when a directly measured profile at target_fraction exists in the store (measured profiles
+ *   always win)"): the effective profile is that curve verbatim, so with its points and
+ *   saturation throughput T_f:
+ *     x     = rate                              lookup axis (no 1/f scaling)
+ *     b     = ((double)d * T_f) / n_m           capacity d*T_f
+ *     ok    = x <= T_f && b >= lambda && s_units >= minu_mt
+ *     term  = L * (n_m / p_m)                   L = lookup of the measured curve at x
  *   Candidate (k_0..k_{M-1}), idx = sum_m k_m * stride_m, LLM 0 most significant,
  *   k = (s_i * nT + t_i) * nR + r_i:
  *     lat32    = tau_0; lat32 = lat32 + tau_m for m = 1..M-1   (binary32, left to right; R7)
@@ -42,6 +50,11 @@ typedef struct {
   const double *rate, *lat;  /* [P_total] rate and latency at the chosen percentile */
   const double *tmax;        /* [M*nT] saturation throughput T_{m,t} */
   const int *min_units;      /* [M*nT] or NULL (= no floor) */
+  /* measured per-share curves (R2), or meas_off == NULL: curve (m, t_i, s_i) = index
+   * (m*nT + t_i)*nS + s_i has points meas_off[c] .. meas_off[c+1]-1 (none: scale the base curve) */
+  const int *meas_off;       /* [M*nT*nS+1] */
+  const double *mrate, *mlat;/* measured rates / latencies at the chosen percentile */
+  const double *mtmax;       /* [M*nT*nS] saturation throughput of each measured curve */
 } orc_inst;
 
 /* R3: piecewise-linear, clamp below the first point, hold L_last on (r_last, T].
@@ -75,14 +88,31 @@ int orc_option(const orc_inst *I, double lambda, int m, int k, float *tau, doubl
   double lam_m = lambda * I->n[m];
   double rate = lam_m / (double)d;
   double f = (double)s_units / (double)I->F;
-  double x = rate / f;
-  double cap = f * T;
-  double bb = ((double)d * cap) / I->n[m];
-  int ok = (x <= T) && (bb >= lambda);
+  int mc = (m * I->nT + t_i) * I->nS + s_i; /* measured curve of this (LLM, tp, share), if any */
+  int measured = I->meas_off && I->meas_off[mc + 1] > I->meas_off[mc];
+  double x, bb;
+  int ok;
+  if (measured) { /* R2: the measured curve verbatim */
+    double Tf = I->mtmax[mc];
+    x = rate;
+    bb = ((double)d * Tf) / I->n[m];
+    ok = (x <= Tf) && (bb >= lambda);
+  } else {        /* capacity scaling L'(l) = L(l/f)/f, T' = f*T */
+    x = rate / f;
+    double cap = f * T;
+    bb = ((double)d * cap) / I->n[m];
+    ok = (x <= T) && (bb >= lambda);
+  }
   if (I->min_units && s_units < I->min_units[c]) ok = 0;
   *b = bb;
   *u = s_units * t * d;
-  if (ok) {
+  if (ok && measured) {
+    int o = I->meas_off[mc];
+    double L = orc_lookup(I->mrate + o, I->mlat + o, I->meas_off[mc + 1] - o, x);
+    double tt = L * (I->n[m] / I->p[m]);
+    *term = tt;
+    *tau = (float)tt;
+  } else if (ok) {
     double L = orc_lookup(rr, ll, P, x);
     double tt = (L / f) * (I->n[m] / I->p[m]);
     *term = tt;

@@ -37,7 +37,9 @@ class _Desc(ctypes.Structure):
                 ("nS", ctypes.c_int32), ("nT", ctypes.c_int32), ("nR", ctypes.c_int32),
                 ("share_units", ctypes.c_void_p), ("tp", ctypes.c_void_p), ("replicas", ctypes.c_void_p),
                 ("prof_off", ctypes.c_void_p), ("rate", ctypes.c_void_p), ("lat", ctypes.c_void_p * 4),
-                ("tmax", ctypes.c_void_p), ("min_units", ctypes.c_void_p), ("pct", ctypes.c_int32)]
+                ("tmax", ctypes.c_void_p), ("min_units", ctypes.c_void_p), ("pct", ctypes.c_int32),
+                ("meas_off", ctypes.c_void_p), ("meas_rate", ctypes.c_void_p), ("meas_lat", ctypes.c_void_p * 4),
+                ("meas_tmax", ctypes.c_void_p)]
 
 
 class _Result(ctypes.Structure):
@@ -202,6 +204,23 @@ class Desc:
         mu = d.get("min_units")
         if mu is not None:
             keep["minu"] = _arr(mu, np.int32).reshape(-1)
+        meas = d.get("measured") or []
+        if meas:  # profiles measured at (LLM, tp index, share index): CSR over (m, t, s) curves
+            nS = len(d["share_units"])
+            by = {(c["llm"], c["tp_index"], c["share_index"]): c for c in meas}
+            moff, mrate, mlat, mtmax = [0], [], {k: [] for k in PCT}, []
+            for m in range(M):
+                for ti in range(len(T)):
+                    for si in range(nS):
+                        c = by.get((m, ti, si))
+                        if c is not None:
+                            mrate += c["rate"]
+                            for k in PCT:
+                                mlat[k] += c["lat"][k] if k in c["lat"] else [float("nan")] * len(c["rate"])
+                        mtmax.append((c["tmax"] if c.get("tmax") is not None else c["rate"][-1]) if c else 0.0)
+                        moff.append(len(mrate))
+            keep.update(moff=_arr(moff, np.int32), mrate=_arr(mrate, np.float64), mtmax=_arr(mtmax, np.float64),
+                        **{f"mlat_{k}": _arr(v, np.float64) for k, v in mlat.items()})
         c = _Desc()
         c.M, c.F = M, d["F"]
         c.n, c.p = keep["n"].ctypes.data, keep["p"].ctypes.data
@@ -212,14 +231,19 @@ class Desc:
             c.lat[i] = keep[f"lat_{k}"].ctypes.data
         c.tmax = keep["tmax"].ctypes.data
         c.min_units = keep["minu"].ctypes.data if "minu" in keep else None
+        if "moff" in keep:
+            c.meas_off, c.meas_rate, c.meas_tmax = (keep["moff"].ctypes.data, keep["mrate"].ctypes.data,
+                                                    keep["mtmax"].ctypes.data)
+            for k, i in PCT.items():
+                c.meas_lat[i] = keep[f"mlat_{k}"].ctypes.data
         c.pct = PCT[percentile or d.get("percentile", "mean")]
         self.c, self.M, self._keep = c, M, keep
 
     @property
     def nbytes(self) -> int:
         """Bytes of the arrays alp_build reads (the selected latency column only)."""
-        sel = {"lat_" + k for k, i in PCT.items() if i == self.c.pct}
-        return int(sum(v.nbytes for k, v in self._keep.items() if not k.startswith("lat_") or k in sel))
+        sel = {p + k for k, i in PCT.items() if i == self.c.pct for p in ("lat_", "mlat_")}
+        return int(sum(v.nbytes for k, v in self._keep.items() if not k.startswith(("lat_", "mlat_")) or k in sel))
 
 
 class Alp:

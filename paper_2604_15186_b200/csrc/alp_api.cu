@@ -281,6 +281,8 @@ struct alp_s {
   bool from_terms = false;
   std::vector<double> n, p, rate, lat, tmax;
   std::vector<int> S, T, R, prof_off, min_units;
+  std::vector<int> meas_off;               // measured per-share curves (R2), empty = none
+  std::vector<double> mrate, mlat, mtmax;
   std::vector<int> u;  // [M*K] units s*t*d (integer grid product)
   std::vector<float> tau_fixed;
   std::vector<double> term_fixed, b_fixed;
@@ -306,6 +308,8 @@ struct alp_s {
   void *d_arena = nullptr;  // every static table + single-target scratch (one allocation)
   double *d_n = nullptr, *d_p = nullptr, *d_rate = nullptr, *d_lat = nullptr, *d_tmax = nullptr;
   int *d_S = nullptr, *d_T = nullptr, *d_R = nullptr, *d_off = nullptr, *d_minu = nullptr, *d_u = nullptr;
+  int *d_moff = nullptr;
+  double *d_mrate = nullptr, *d_mlat = nullptr, *d_mtmax = nullptr;
   int *d_tile_s = nullptr, *d_bperm = nullptr, *d_dv = nullptr, *d_dcnt = nullptr, *d_gsum = nullptr;
   uint32_t *d_tile_e = nullptr, *d_tile_off = nullptr;
   float *d_tau_fixed = nullptr;
@@ -341,6 +345,9 @@ struct alp_s {
     d.n = d_n; d.p = d_p; d.S = d_S; d.T = d_T; d.R = d_R; d.prof_off = d_off;
     d.rate = d_rate; d.lat = d_lat; d.tmax = d_tmax;
     d.min_units = min_units.empty() ? nullptr : d_minu;
+    d.meas_off = meas_off.empty() ? nullptr : d_moff;
+    d.mrate = d_mrate; d.mlat = d_mlat; d.mtmax = d_mtmax;
+    d.n_mpts = (int)mrate.size();
     d.n_pts = (int)rate.size();
     return d;
   }
@@ -659,6 +666,12 @@ alp_status upload_all(alp_s *h) {
     A.add(h->lat, &h->d_lat);
     A.add(h->tmax, &h->d_tmax);
     if (!h->min_units.empty()) A.add(h->min_units, &h->d_minu);
+    if (!h->meas_off.empty()) {
+      A.add(h->meas_off, &h->d_moff);
+      A.add(h->mrate, &h->d_mrate);
+      A.add(h->mlat, &h->d_mlat);
+      A.add(h->mtmax, &h->d_mtmax);
+    }
   }
   A.add(h->T, &h->d_T);
   A.add(h->R, &h->d_R);
@@ -1313,6 +1326,34 @@ alp_status alp_build(const alp_desc *d, alp_t **out) {
     for (int t = 0; t < d->nT; ++t) lmax = std::max(lmax, lat[d->prof_off[m * d->nT + t + 1] - 1]);
     term_bound += lmax * ((double)d->F / d->share_units[0]) * (d->n[m] / d->p[m]) * 1.0000001;
   }
+  // measured per-share curves (R2): same validation as the base curves
+  const int CM = C * d->nS;
+  const double *mlat = nullptr;
+  if (d->meas_off) {
+    mlat = d->meas_lat[d->pct];
+    if (d->meas_off[0] != 0) return fail(ALP_EINVAL, "meas_off[0] must be 0");
+    if (d->meas_off[CM] > 0 && (!d->meas_rate || !mlat))
+      return fail(ALP_EINVAL, "meas_rate / meas_lat[%d] (selected percentile column) is NULL", d->pct);
+    for (int c = 0; c < CM; ++c) {
+      const int a = d->meas_off[c], b = d->meas_off[c + 1];
+      if (b < a) return fail(ALP_EINVAL, "meas_off not non-decreasing at %d", c);
+      const int m = c / (d->nT * d->nS), ti = (c / d->nS) % d->nT, si = c % d->nS;
+      for (int i = a; i < b; ++i) {
+        if (!std::isfinite(d->meas_rate[i]) || d->meas_rate[i] < 0)
+          return fail(ALP_EINVAL, "meas_rate[%d] must be finite and >= 0", i);
+        if (i > a && !(d->meas_rate[i] > d->meas_rate[i - 1]))
+          return fail(ALP_EINVAL, "measured rates of LLM %d tp index %d share index %d not strictly increasing", m, ti, si);
+        if (!(mlat[i] > 0) || !std::isfinite(mlat[i])) return fail(ALP_EINVAL, "meas_lat[%d] must be finite and > 0", i);
+        if (i > a && mlat[i] < mlat[i - 1])
+          return fail(ALP_EINVAL, "measured latencies of LLM %d tp index %d share index %d decrease", m, ti, si);
+      }
+      if (b > a) {
+        if (d->meas_tmax && (!std::isfinite(d->meas_tmax[c]) || d->meas_tmax[c] < d->meas_rate[b - 1]))
+          return fail(ALP_EINVAL, "meas_tmax[%d] must be finite and >= the last measured rate", c);
+        term_bound += mlat[b - 1] * (d->n[m] / d->p[m]) * 1.0000001;
+      }
+    }
+  }
   if (!(term_bound < 1e37)) return fail(ALP_EINVAL, "latency terms could overflow binary32 (sum bound %g)", term_bound);
 
   alp_s *h = new alp_s();
@@ -1329,6 +1370,16 @@ alp_status alp_build(const alp_desc *d, alp_t **out) {
   h->tmax.resize(C);
   for (int c = 0; c < C; ++c) h->tmax[c] = d->tmax ? d->tmax[c] : d->rate[d->prof_off[c + 1] - 1];
   if (d->min_units) h->min_units.assign(d->min_units, d->min_units + C);
+  if (d->meas_off && d->meas_off[CM] > 0) {
+    h->meas_off.assign(d->meas_off, d->meas_off + CM + 1);
+    const int PM = d->meas_off[CM];
+    h->mrate.assign(d->meas_rate, d->meas_rate + PM);
+    h->mlat.assign(mlat, mlat + PM);
+    h->mtmax.assign(CM, 0.0);
+    for (int c = 0; c < CM; ++c)
+      if (d->meas_off[c + 1] > d->meas_off[c])
+        h->mtmax[c] = d->meas_tmax ? d->meas_tmax[c] : d->meas_rate[d->meas_off[c + 1] - 1];
+  }
   compute_units(h);
   Trace tr;
   tr.mark("validate");

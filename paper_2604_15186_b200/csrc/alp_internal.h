@@ -42,6 +42,11 @@ struct DevProfiles {
   const double *rate, *lat, *tmax;
   const int *min_units;  // nullptr = no floor
   int n_pts;             // profile points (rate / lat length)
+  // measured per-share curves (R2): curve (m*nT + t)*nS + s, points meas_off[c] .. meas_off[c+1]-1
+  // (empty: capacity-scale the base curve); nullptr = none measured
+  const int *meas_off;
+  const double *mrate, *mlat, *mtmax;
+  int n_mpts;            // measured points
 };
 
 // Option-term kernel (K1) arguments.

@@ -84,6 +84,12 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     sp.tmax = stage_d(gp.tmax, MT);
     sp.rate = stage_d(gp.rate, gp.n_pts);
     sp.lat = stage_d(gp.lat, gp.n_pts);
+    const int MTS = MT * gp.nS;
+    if (gp.meas_off) {  // measured per-share curves (R2)
+      sp.mrate = stage_d(gp.mrate, gp.n_mpts);
+      sp.mlat = stage_d(gp.mlat, gp.n_mpts);
+      sp.mtmax = stage_d(gp.mtmax, MTS);
+    }
     int *w = reinterpret_cast<int *>(d);
     auto stage_i = [&](const int *src, int n) {
       for (int i = tid; i < n; i += nt) cp_async4(w + i, src + i);
@@ -96,6 +102,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     sp.R = stage_i(gp.R, gp.nR);
     sp.prof_off = stage_i(gp.prof_off, MT + 1);
     if (gp.min_units) sp.min_units = stage_i(gp.min_units, MT);
+    if (gp.meas_off) sp.meas_off = stage_i(gp.meas_off, MTS + 1);
   }
   // static plan tables (cp.async: in flight with the profile tables)
   for (int i = tid; i < D; i += nt) cp_async4(s_dv + i, P.dv + i);
@@ -556,7 +563,8 @@ size_t uprep_smem_bytes(const SearchArgs &a) {
   const int MT = pr.M * pr.nT;
   return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(2 * a.D + 1 + 3 * a.u_nch * (a.D + 1) + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
          (size_t)(2 * pr.M + MT + 2 * pr.n_pts) * 8 +
-         (size_t)(pr.nS + pr.nT + pr.nR + MT + 1 + (pr.min_units ? MT : 0)) * 4;
+         (size_t)(pr.nS + pr.nT + pr.nR + MT + 1 + (pr.min_units ? MT : 0)) * 4 +
+         (pr.meas_off ? (size_t)(2 * pr.n_mpts + MT * pr.nS) * 8 + (size_t)(MT * pr.nS + 1) * 4 : 0);
 }
 
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search) {

@@ -36,14 +36,31 @@ __device__ __forceinline__ int option_terms(const DevProfiles &P, double lambda,
   const double lam_m = __dmul_rn(lambda, P.n[m]);              // lambda_m = lambda_W n_m
   const double rate = __ddiv_rn(lam_m, (double)d);            // per replica
   const double f = __ddiv_rn((double)s_units, (double)P.F);   // per-shard share
-  const double x = __ddiv_rn(rate, f);                        // L'(l) = L(l/f)/f
-  const double cap = __dmul_rn(f, T);
-  const double bb = __ddiv_rn(__dmul_rn((double)d, cap), P.n[m]);  // Eq. 2 term
-  int ok = (x <= T) && (bb >= lambda);                        // R4
+  const int mc = (m * P.nT + t_i) * P.nS + s_i;               // measured curve of (LLM, tp, share)
+  const bool measured = P.meas_off && P.meas_off[mc + 1] > P.meas_off[mc];
+  double x, bb;
+  int ok;
+  if (measured) {  // R2: the measured curve verbatim ("measured profiles always win")
+    const double Tf = P.mtmax[mc];
+    x = rate;
+    bb = __ddiv_rn(__dmul_rn((double)d, Tf), P.n[m]);         // Eq. 2 term, capacity d*T_f
+    ok = (x <= Tf) && (bb >= lambda);
+  } else {         // capacity scaling L'(l) = L(l/f)/f, T' = f*T
+    x = __ddiv_rn(rate, f);
+    const double cap = __dmul_rn(f, T);
+    bb = __ddiv_rn(__dmul_rn((double)d, cap), P.n[m]);        // Eq. 2 term
+    ok = (x <= T) && (bb >= lambda);                          // R4
+  }
   if (P.min_units && s_units < P.min_units[c]) ok = 0;        // memory floor
   *b = bb;
   *u = s_units * t * d;
-  if (ok) {
+  if (ok && measured) {
+    const int o = P.meas_off[mc];
+    const double L = lookup_latency(P.mrate + o, P.mlat + o, P.meas_off[mc + 1] - o, x);
+    const double tt = __dmul_rn(L, __ddiv_rn(P.n[m], P.p[m]));  // Eq. 1 term of the measured profile
+    *term = tt;
+    *tau = __double2float_rn(tt);
+  } else if (ok) {
     const int o = P.prof_off[c];
     const double L = lookup_latency(P.rate + o, P.lat + o, P.prof_off[c + 1] - o, x);
     const double tt = __dmul_rn(__ddiv_rn(L, f), __ddiv_rn(P.n[m], P.p[m]));  // Eq. 1 term

@@ -153,6 +153,66 @@ def test_percentile_c4_vs_bruteforce(P, pct):
     assert mean.index != r.index  # the selected column decides the optimum
 
 
+# ----------------------------------------------------------------------------- measured profiles (R2)
+def test_measured_profiles_hand_case_gpu(P):
+    # SPEC.md:204 "measured profiles always win": the golden hand rows with two measured curves
+    with open("tests/golden/hand_case.json") as f:
+        g = json.load(f)["measured_profiles"]
+    from fractions import Fraction
+    d = generate.with_measured(generate.load("hand"), g["curves"])
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    tab = alp.option_table(1.0, I.K)
+    for m, k, term, b, u in g["terms_lambda_1"]["rows"]:
+        assert tab["term"][m, k] == pytest.approx(float(Fraction(term)), rel=4e-16) and tab["u"][m, k] == u
+        assert tab["b"][m, k] == float(Fraction(b))
+    for lam_s, B, idx, _kg, _kv, Lw, Tw, units, feas in g["searches"]["rows"]:
+        r = alp.search(float(Fraction(lam_s)), B)
+        assert (r.found, r.index, r.feasible_count, r.units) == (True, idx, feas, units), B
+        assert r.latency == pytest.approx(float(Fraction(Lw)), rel=1e-12) and r.throughput == float(Fraction(Tw))
+        _check_winner(P, alp, I, 1.0, B, r)
+
+
+@pytest.mark.parametrize("name,seed", [("C2", 1), ("C3", 2), ("C4", 3)])
+def test_measured_profiles_option_tables_and_search(P, name, seed):
+    # a seeded subset of (LLM, tp, share) measured (perturbed scaled curves): option tables bit-exact
+    # against the oracle on every launch path's kernel, and the search against O2
+    d = generate.random_measured(generate.load(name), seed)
+    assert d["measured"]
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    for lam in (d["targets"][0], d["targets"][0] * 2.5):
+        g = alp.option_table(lam, I.K)
+        o = oracle.option_table(I, lam)
+        assert np.array_equal(g["tau"].view(np.uint32), o["tau"].view(np.uint32)), lam
+        assert np.array_equal(g["b"].view(np.uint64), o["b"].view(np.uint64)), lam
+        assert np.array_equal(g["term"][o["ok"]].view(np.uint64), o["term"][o["ok"]].view(np.uint64))
+        r = alp.search(lam, I.budget)
+        f, v, idx, cnt = dp.search(o["tau"], o["u"], I.budget)
+        _same(r, f, v, idx, cnt, (name, lam))
+        _check_winner(P, alp, I, lam, I.budget, r)
+    # a measured curve equal to the scaled one changes nothing (powers-of-two shares)
+    F = d["F"]
+    which = [(m, ti, si) for m in range(d["M"]) for ti in range(len(d["tp"]))
+             for si, s in enumerate(d["share_units"]) if (F // s) * s == F and (F // s) & (F // s - 1) == 0]
+    base = generate.load(name)
+    a0 = P.Alp.from_instance(base).search(base["targets"][0], I.budget)
+    a1 = P.Alp.from_instance(generate.scaled_measured(base, which)).search(base["targets"][0], I.budget)
+    assert (a0.index, a0.feasible_count, a0.latency_key, a0.latency) == (a1.index, a1.feasible_count, a1.latency_key,
+                                                                        a1.latency)
+
+
+@pytest.mark.slow
+def test_measured_profiles_c4_vs_bruteforce(P):
+    import os
+    d = generate.random_measured(generate.load("C4"), 7)
+    I = oracle.from_json(d)
+    lam = d["targets"][0]
+    r = P.Alp.from_instance(d).search(lam, I.budget)
+    o = oracle.search(I, lam, I.budget, threads=os.cpu_count() or 8)
+    _same(r, o.found, o.latency_key, o.index, o.count)
+
+
 # ----------------------------------------------------------------------------- configs
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_full_bruteforce_small(P, name):

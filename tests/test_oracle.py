@@ -207,6 +207,77 @@ def test_hand_case_percentile_searches():
     assert oracle.search(I_mean, 1.0, 8).index == 54 and oracle.search(I_p90, 1.0, 8).index == 45
 
 
+# ----------------------------------------------------------------------------- measured profiles (R2)
+def test_measured_profiles_hand_case():
+    # a profile measured at the share is used verbatim (no capacity scaling); the
+    # hand-derived terms and the exact-rational winners (tests/golden/hand_case.json)
+    g = _gold("hand_case.json")["measured_profiles"]
+    d = generate.with_measured(generate.load("hand"), g["curves"])
+    I = oracle.from_json(d)
+    base = oracle.from_json(generate.load("hand"))
+    changed = {(m, k) for m, k, *_ in g["terms_lambda_1"]["rows"]}
+    for m, k, term, b, u in g["terms_lambda_1"]["rows"]:
+        o = oracle.option(I, 1.0, m, k)
+        assert o["ok"] and o["u"] == u and o["b"] == float(_F(b))
+        assert o["term"] == pytest.approx(float(_F(term)), rel=4e-16, abs=0)
+    for m in range(2):  # every other option keeps its scaled (App. A) term
+        for k in range(8):
+            if (m, k) not in changed:
+                assert oracle.option(I, 1.0, m, k) == oracle.option(base, 1.0, m, k)
+    rows = _gold("hand_case.json")["option_terms_lambda_1"]["rows"]
+    G = [_F(r[5]) for r in rows]
+    V = [_F(r[9]) for r in rows]
+    for m, k, term, *_ in g["terms_lambda_1"]["rows"]:
+        (G if m == 0 else V)[k] = _F(term)
+    for lam_s, B, idx, kg, kv, Lw, Tw, units, feas in g["searches"]["rows"]:
+        cands = sorted((G[a] + V[b], 8 * a + b) for a, b in itertools.product(range(8), range(8))
+                       if rows[a][7] + rows[b][11] <= B)
+        assert (cands[0][1], cands[0][0], len(cands)) == (idx, _F(Lw), feas)   # fixture = enumeration
+        r = oracle.search(I, float(_F(lam_s)), B)
+        assert r.found and r.index == idx and r.count == feas, B
+        p = oracle.predict(I, 1.0, [kg, kv], B)
+        assert p["units"] == units and p["throughput"] == float(_F(Tw))
+        assert p["latency"] == pytest.approx(float(_F(Lw)), rel=1e-15)
+
+
+@pytest.mark.parametrize("name", ["hand", "C1", "C2"])
+def test_measured_equal_to_scaled_profile_is_exact(name):
+    # Invariant of R2: a measured curve equal to the capacity-scaled base curve (rates x f,
+    # latencies / f, T x f) reproduces the scaled option terms bit for bit when f is a power of two
+    # (every step of the lookup scales exactly).  All (LLM, tp, share) measured this way.
+    d = generate.load(name)
+    F = d["F"]
+    shares = [si for si, s in enumerate(d["share_units"]) if (F // s) * s == F and (F // s) & (F // s - 1) == 0]
+    which = [(m, ti, si) for m in range(d["M"]) for ti in range(len(d["tp"])) for si in shares]
+    dm = generate.scaled_measured(d, which)
+    I, Im = oracle.from_json(d), oracle.from_json(dm)
+    assert Im.meas_off is not None and int(Im.meas_off[-1]) > 0
+    for lam in (d["targets"][0], d["targets"][0] * 3.0, d.get("lambda_star", d["targets"][0] * 4.0)):
+        a, b = oracle.option_table(I, lam), oracle.option_table(Im, lam)
+        for k in ("tau", "b", "u", "ok"):
+            assert np.array_equal(a[k], b[k]), (name, lam, k)
+        fin = a["ok"]
+        assert np.array_equal(a["term"][fin], b["term"][fin])
+
+
+def test_measured_profile_capacity_and_boundary():
+    # measured T_f bounds the per-replica rate directly (x = T_f feasible, above it infeasible) and
+    # gives the Eq. 2 term d*T_f/n (SPEC.md:190 boundary rule on the measured curve)
+    llm = {"n": 2.0, "p": 1.0, "curves": [_curve([1.0, 4.0], [1.0, 3.0])]}
+    d = {"M": 1, "F": 2, "share_units": [1, 2], "tp": [1], "replicas": [1, 2], "n": [2.0], "p": [1.0],
+         "profiles": [llm["curves"]], "min_units": None, "budget_units": 10, "percentile": "mean"}
+    d = generate.with_measured(d, [{"llm": 0, "tp_index": 0, "share_index": 0, "rate": [1.0, 3.0],
+                                     "lat": [2.0, 6.0], "tmax": 3.0}])
+    I = oracle.from_json(d)
+    o = oracle.option(I, 1.5, 0, 0)       # s=1 (f=1/2), d=1: x = 1.5*2/1 = 3 = T_f -> feasible
+    assert o["ok"] and o["term"] == 6.0 * 2.0 and o["b"] == 1.0 * 3.0 / 2.0
+    assert not oracle.option(I, 1.5000001, 0, 0)["ok"]
+    o = oracle.option(I, 1.0, 0, 1)       # d=2: x = 1 -> L = 2, term 4, b = 2*3/2 = 3
+    assert o["ok"] and o["term"] == 4.0 and o["b"] == 3.0
+    o = oracle.option(I, 1.0, 0, 2)       # s=2 (f=1) not measured: base curve, x = 2 -> L = 5/3
+    assert o["ok"] and o["term"] == pytest.approx((1.0 + 2.0 * (1.0 / 3.0)) * 2.0, rel=1e-15)
+
+
 # ----------------------------------------------------------------------------- lambda*
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_lambda_star_is_maximal(name):

@@ -196,6 +196,54 @@ def skew_percentile(d: dict[str, Any], pct: str, seed: int, lo: float = 1.0, hi:
     return out
 
 
+def with_measured(d: dict[str, Any], curves: list[dict[str, Any]]) -> dict[str, Any]:
+    """Copy of instance d with profiles measured at given (llm, tp_index, share_index); each curve's
+    latency list is used for every percentile column unless it is already a per-percentile dict."""
+    out = json.loads(json.dumps(d))
+    meas = []
+    for c in curves:
+        c = dict(c)
+        if not isinstance(c["lat"], dict):
+            c["lat"] = {k: list(c["lat"]) for k in PCT_SCALE}
+        meas.append(c)
+    out["measured"] = meas
+    return out
+
+
+def scaled_measured(d: dict[str, Any], which) -> dict[str, Any]:
+    """Copy of d where every (llm, tp_index, share_index) in `which` gets a measured curve equal to the
+    capacity-scaled base curve (rates x f, latencies / f, tmax x f with f = share/F): the reading R2
+    makes such a curve reproduce the scaled profile exactly when f is a power of two."""
+    curves = []
+    for m, ti, si in which:
+        base = d["profiles"][m][ti]
+        f = d["share_units"][si] / d["F"]
+        curves.append({"llm": m, "tp_index": ti, "share_index": si, "rate": [r * f for r in base["rate"]],
+                       "lat": {k: [x / f for x in v] for k, v in base["lat"].items()},
+                       "tmax": (base["tmax"] if base.get("tmax") is not None else base["rate"][-1]) * f})
+    return with_measured(d, curves)
+
+
+def random_measured(d: dict[str, Any], seed: int, frac: float = 0.3) -> dict[str, Any]:
+    """Copy of d with seeded measured curves on a random subset of (llm, tp, share): the scaled base
+    curve perturbed (latencies x U[0.7, 1.3], capacity x U[0.8, 1.2]), monotone by construction."""
+    rng = np.random.default_rng(seed)
+    curves = []
+    for m in range(d["M"]):
+        for ti in range(len(d["tp"])):
+            for si in range(len(d["share_units"])):
+                if rng.random() >= frac:
+                    continue
+                base = d["profiles"][m][ti]
+                f = d["share_units"][si] / d["F"]
+                lf, cf = float(rng.uniform(0.7, 1.3)), float(rng.uniform(0.8, 1.2))
+                curves.append({"llm": m, "tp_index": ti, "share_index": si,
+                               "rate": [r * f * cf for r in base["rate"]],
+                               "lat": {k: [x / f * lf for x in v] for k, v in base["lat"].items()},
+                               "tmax": (base["tmax"] if base.get("tmax") is not None else base["rate"][-1]) * f * cf})
+    return with_measured(d, curves)
+
+
 # ---------------------------------------------------------------- random small instances (tests)
 def random_instance(seed: int, M: int, F: int, S: list[int], T: list[int], R: list[int], budget: int,
                     points: int = 4, min_units: bool = False) -> dict[str, Any]:
