@@ -167,7 +167,7 @@ alp_status alp_workflow_stats(int32_t n_req, int32_t M, int64_t n_inv, const int
                               const double *start, const double *end, double *n_out, double *p_out);
 
 /* Topology-aware placement of an allocation ("hierarchical placement",
- * most-constrained-first; SPEC.md:440-445 tie-breaks).  Cluster: G GPUs of F units; gpu_node[g],
+ * most-constrained-first, inter-node stage then intra-node stage; SPEC.md:440-445 tie-breaks).  Cluster: G GPUs of F units; gpu_node[g],
  * gpu_domain[g] = node and NVLink domain of GPU g (a domain never spans nodes).  Allocation: per LLM
  * share_units (per shard, 1..F), tp, replicas; every replica is a tensor group of tp shards.
  * Output shard_gpu[sum_m tp_m*replicas_m], ordered (LLM, replica, shard): the GPU of each shard.

@@ -1742,16 +1742,77 @@ alp_status alp_workflow_stats(int32_t n_req, int32_t M, int64_t n_inv, const int
 // "Hierarchical placement algorithm"; tie-breaks and the imbalance definition from).
 //
 // Host code (alp_place): the placement is a short sequential heuristic over a handful of shards (the paper
-// calls the optimum NP-hard and uses this greedy; it runs once per chosen allocation).
-//  * every replica of LLM m is a tensor group of tp_m shards demanding share_units_m units each;
-//  * groups are placed most-constrained-first: tensor-parallel groups before single shards, larger
-//    total demand first, then (LLM, replica) order;
-//  * a tensor group goes to one NVLink domain: among domains with tp free GPUs of enough capacity
-//    keep those with the smallest imbalance (max - min free units over the domain's GPUs), then
-//    the least total free capacity, then the lowest (node, domain); inside it the tp GPUs with the
-//    least sufficient free units (lowest index on ties);
-//  * single shards are packed onto already occupied GPUs first, best fit by free units, then onto
-//    empty GPUs; ties by (node, GPU index).
+// calls the optimum NP-hard and uses this greedy; it runs once per chosen allocation).  Every replica of
+// LLM m is a tensor group of tp_m shards demanding share_units_m units each.  Two stages (PAPER.md:413
+// "first places LLMs into nodes while prioritizing larger instances (inter-node stage), and then assigns
+// GPU fractions within a node (intra-node stage)"):
+//  * inter-node: groups most-constrained-first (tensor-parallel groups before single shards, larger total
+//    demand first, then (LLM, replica)).  A tensor group goes to one NVLink domain: among domains with tp
+//    free GPUs of enough capacity keep those with the smallest imbalance (max - min free units over the
+//    domain's GPUs), then the least total free capacity, then the lowest (node, domain) -- its node is
+//    the domain's.  A single shard goes to the node with the least free units among the nodes that still
+//    have a GPU it fits on (occupied nodes first), lowest node on ties;
+//  * intra-node: each node re-places its own groups from scratch -- its tensor groups in the same order
+//    and scoring restricted to its domains (the tp GPUs with the least sufficient free units), then its
+//    single shards largest first onto already occupied GPUs first, best fit by free units, lowest GPU on
+//    ties.  Should a node's re-placement fail, the node keeps its inter-node stage GPUs (always valid).
+namespace {
+struct PlaceGroup {
+  int m, r, tp, units, first;  // first = index of the group's first shard in shard_gpu
+};
+
+// Domain choice + GPUs for a tensor group over the given domains (free_units updated); false if none fits.
+bool place_tensor(const PlaceGroup &grp, const std::map<std::pair<int, int>, std::vector<int>> &domains, int node_only,
+                  int F, std::vector<int> &free_units, std::vector<int> &gpus) {
+  const std::vector<int> *best = nullptr;
+  long long best_imb = 0, best_cap = 0;
+  for (const auto &kv : domains) {
+    if (node_only >= 0 && kv.first.first != node_only) continue;
+    const std::vector<int> &gs = kv.second;
+    int fit = 0, mx = 0, mn = F;
+    long long cap = 0;
+    for (int g : gs) {
+      fit += free_units[g] >= grp.units;
+      mx = std::max(mx, free_units[g]);
+      mn = std::min(mn, free_units[g]);
+      cap += free_units[g];
+    }
+    if (fit < grp.tp) continue;
+    const long long imb = mx - mn;
+    if (!best || imb < best_imb || (imb == best_imb && cap < best_cap)) {
+      best = &gs;
+      best_imb = imb;
+      best_cap = cap;
+    }
+  }
+  if (!best) return false;
+  std::vector<int> cand;
+  for (int g : *best)
+    if (free_units[g] >= grp.units) cand.push_back(g);
+  // the tp GPUs with the MOST free units (lowest index on ties): keeps the domain balanced, which is
+  // what its score rewards; taking the least sufficient ones stacks groups on the same GPUs and
+  // strands the rest (3 tp-2 groups on a 3-GPU domain of 2 units each: (0,1),(0,1) then nothing fits)
+  std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return free_units[a] > free_units[b]; });
+  gpus.assign(cand.begin(), cand.begin() + grp.tp);
+  std::sort(gpus.begin(), gpus.end());
+  for (int g : gpus) free_units[g] -= grp.units;
+  return true;
+}
+
+// Single shard onto one of `gs` (index order): occupied GPUs first, best fit by free units; -1 if none fits.
+int place_single(int units, const std::vector<int> &gs, int F, std::vector<int> &free_units) {
+  int pick = -1;
+  for (int pass = 0; pass < 2 && pick < 0; ++pass)
+    for (int g : gs) {
+      const bool occupied = free_units[g] < F;
+      if ((pass == 0) != occupied || free_units[g] < units) continue;
+      if (pick < 0 || free_units[g] < free_units[pick]) pick = g;
+    }
+  if (pick >= 0) free_units[pick] -= units;
+  return pick;
+}
+}  // namespace
+
 alp_status alp_place(int32_t G, int32_t F, const int32_t *gpu_node, const int32_t *gpu_domain, int32_t M,
                      const int32_t *share_units, const int32_t *tp, const int32_t *replicas, int32_t *shard_gpu) {
   if (G < 1 || F < 1) return fail(ALP_EINVAL, "need G >= 1 GPUs and F >= 1 units per GPU");
@@ -1765,10 +1826,7 @@ alp_status alp_place(int32_t G, int32_t F, const int32_t *gpu_node, const int32_
       return fail(ALP_EINVAL, "NVLink domain %d spans nodes", gpu_domain[g]);
     dom_node[gpu_domain[g]] = gpu_node[g];
   }
-  struct Group {
-    int m, r, tp, units, first;  // first = index of the group's first shard in shard_gpu
-  };
-  std::vector<Group> groups;
+  std::vector<PlaceGroup> groups;
   int shards = 0;
   long long demand = 0;
   for (int m = 0; m < M; ++m) {
@@ -1782,66 +1840,80 @@ alp_status alp_place(int32_t G, int32_t F, const int32_t *gpu_node, const int32_
   }
   if (demand > (long long)G * F)
     return fail(ALP_EINFEASIBLE, "demand %lld units exceeds the cluster's %lld", demand, (long long)G * F);
-  std::stable_sort(groups.begin(), groups.end(), [](const Group &a, const Group &b) {
+  std::stable_sort(groups.begin(), groups.end(), [](const PlaceGroup &a, const PlaceGroup &b) {
     const bool ta = a.tp > 1, tb = b.tp > 1;
     if (ta != tb) return ta;
     const long long ua = (long long)a.tp * a.units, ub = (long long)b.tp * b.units;
     if (ua != ub) return ua > ub;
     return a.m != b.m ? a.m < b.m : a.r < b.r;
   });
-  std::vector<int> free_units(G, F);
-  // domains in (node, domain id) order with their GPUs in index order
+  // domains in (node, domain id) order with their GPUs in index order; nodes with their GPUs
   std::map<std::pair<int, int>, std::vector<int>> domains;
-  for (int g = 0; g < G; ++g) domains[{gpu_node[g], gpu_domain[g]}].push_back(g);
-  for (const Group &grp : groups) {
+  std::map<int, std::vector<int>> nodes;
+  for (int g = 0; g < G; ++g) {
+    domains[{gpu_node[g], gpu_domain[g]}].push_back(g);
+    nodes[gpu_node[g]].push_back(g);
+  }
+  // ---- inter-node stage: a node for every group (GPUs tentatively, for the capacity accounting)
+  std::vector<int> free_units(G, F), group_node(groups.size());
+  std::vector<int> gpus;
+  for (size_t i = 0; i < groups.size(); ++i) {
+    const PlaceGroup &grp = groups[i];
     if (grp.tp > 1) {
-      const std::vector<int> *best = nullptr;
-      long long best_imb = 0, best_cap = 0;
-      for (const auto &kv : domains) {
-        const std::vector<int> &gs = kv.second;
-        int fit = 0, mx = 0, mn = F;
-        long long cap = 0;
-        for (int g : gs) {
-          fit += free_units[g] >= grp.units;
-          mx = std::max(mx, free_units[g]);
-          mn = std::min(mn, free_units[g]);
-          cap += free_units[g];
-        }
-        if (fit < grp.tp) continue;
-        const long long imb = mx - mn;
-        if (!best || imb < best_imb || (imb == best_imb && cap < best_cap)) {
-          best = &gs;
-          best_imb = imb;
-          best_cap = cap;
-        }
-      }
-      if (!best)
+      if (!place_tensor(grp, domains, -1, F, free_units, gpus))
         return fail(ALP_EINFEASIBLE, "no NVLink domain fits LLM %d replica %d (tp %d x %d units)", grp.m, grp.r,
                     grp.tp, grp.units);
-      std::vector<int> cand;
-      for (int g : *best)
-        if (free_units[g] >= grp.units) cand.push_back(g);
-      std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return free_units[a] < free_units[b]; });
-      std::vector<int> chosen(cand.begin(), cand.begin() + grp.tp);
-      std::sort(chosen.begin(), chosen.end());
-      for (int s = 0; s < grp.tp; ++s) {
-        shard_gpu[grp.first + s] = chosen[s];
-        free_units[chosen[s]] -= grp.units;
-      }
+      for (int s = 0; s < grp.tp; ++s) shard_gpu[grp.first + s] = gpus[s];
+      group_node[i] = gpu_node[gpus[0]];
     } else {
-      int pick = -1;
-      for (int pass = 0; pass < 2 && pick < 0; ++pass) {  // occupied GPUs first, then empty ones
-        for (int g = 0; g < G; ++g) {
-          const bool occupied = free_units[g] < F;
-          if ((pass == 0) != occupied || free_units[g] < grp.units) continue;
-          if (pick < 0 || free_units[g] < free_units[pick]) pick = g;
+      int best = -1;
+      long long best_free = 0;
+      for (const auto &kv : nodes) {
+        long long fr = 0;
+        bool fits = false;
+        for (int g : kv.second) {
+          fr += free_units[g];
+          fits |= free_units[g] >= grp.units;
+        }
+        if (fits && (best < 0 || fr < best_free)) {
+          best = kv.first;
+          best_free = fr;
         }
       }
-      if (pick < 0)
-        return fail(ALP_EINFEASIBLE, "no GPU fits LLM %d replica %d (%d units)", grp.m, grp.r, grp.units);
-      shard_gpu[grp.first] = pick;
-      free_units[pick] -= grp.units;
+      const int g = best < 0 ? -1 : place_single(grp.units, nodes[best], F, free_units);
+      if (g < 0) return fail(ALP_EINFEASIBLE, "no GPU fits LLM %d replica %d (%d units)", grp.m, grp.r, grp.units);
+      shard_gpu[grp.first] = g;
+      group_node[i] = best;
     }
+  }
+  // ---- intra-node stage: every node re-places its groups; kept when all of them fit
+  for (const auto &kv : nodes) {
+    const int n = kv.first;
+    std::vector<int> fu(G, 0);
+    for (int g : kv.second) fu[g] = F;
+    std::vector<std::pair<size_t, std::vector<int>>> mine;  // (group, GPUs)
+    bool ok = true;
+    std::vector<size_t> singles;
+    for (size_t i = 0; i < groups.size() && ok; ++i) {
+      if (group_node[i] != n) continue;
+      if (groups[i].tp > 1) {
+        ok = place_tensor(groups[i], domains, n, F, fu, gpus);
+        if (ok) mine.push_back({i, gpus});
+      } else {
+        singles.push_back(i);
+      }
+    }
+    std::stable_sort(singles.begin(), singles.end(),
+                     [&](size_t a, size_t b) { return groups[a].units > groups[b].units; });
+    for (size_t i : singles) {
+      if (!ok) break;
+      const int g = place_single(groups[i].units, kv.second, F, fu);
+      ok = g >= 0;
+      if (ok) mine.push_back({i, {g}});
+    }
+    if (!ok) continue;  // keep the inter-node stage's GPUs for this node
+    for (const auto &x : mine)
+      for (int s = 0; s < (int)x.second.size(); ++s) shard_gpu[groups[x.first].first + s] = x.second[s];
   }
   return ALP_OK;
 }
