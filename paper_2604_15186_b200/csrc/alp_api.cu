@@ -762,6 +762,10 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.n_groups = h->n_groups; a.nQ = h->nQ; a.A = h->A; a.item_lo = lo; a.item_hi = hi;
   a.fd_nQ = make_fastdiv(h->nQ);
   a.fd_ng = make_fastdiv(h->n_groups);
+  const bool fine = (uint64_t)h->n_chunks * h->L * (uint64_t)h->Ka < 0xffffffffull;  // segment per a option
+  a.seg_q = fine ? (uint32_t)h->Ka : h->nQ;
+  a.seg_A = fine ? 1u : h->A;
+  a.seg_mul = fine ? h->A : 1u;
   a.budget = (int)Reff;
   a.n_targets = n_targets;
   a.D = (int)(std::upper_bound(h->dv.begin(), h->dv.end(), (int)Reff) - h->dv.begin());
@@ -1158,6 +1162,12 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
         for (int i = 0; i < 5; ++i) v[i].push_back(ts[b * 8 + i] ? (ts[b * 8 + i] - t0) * 1e-3 : 0.0);
       for (auto &x : v) std::sort(x.begin(), x.end());
       auto q = [&](int i, double f) { return v[i][(size_t)(f * (v[i].size() - 1))]; };
+      if (const char *dump = getenv("ALP_DBG_DUMP")) {  // raw stamps (tools/block_hist.py)
+        if (FILE *f = fopen(dump, "ab")) {
+          fwrite(ts.data(), 8, ts.size(), f);
+          fclose(f);
+        }
+      }
       fprintf(stderr, "[alp dbg] grid %d us: start med %.1f max %.1f | terms med %.1f max %.1f | tables med %.1f "
               "max %.1f | loop-end min %.1f med %.1f max %.1f | end max %.1f\n", dgrid, q(0, .5), q(0, 1), q(4, .5),
               q(4, 1), q(1, .5), q(1, 1), q(2, 0), q(2, .5), q(2, 1), q(3, 1));

@@ -33,8 +33,8 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   const bool found = key != kKeyNone && val < __int_as_float(0x7f800000);
   uint32_t q = 0, chunk = 0, e = 0;
   if (found) {
-    q = seg % P.nQ;
-    const uint32_t row = seg / P.nQ;
+    q = seg % P.seg_q;  // segment slot: first a option = q * seg_A
+    const uint32_t row = seg / P.seg_q;
     chunk = row / P.L;
     e = row % P.L;
     // digits of the row's LLMs 0..g1-1 (chunk digits, then sort-group digits; LLM 0 most
@@ -72,7 +72,7 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
     // the segment starts at a-range q and runs to the end of the row (see fold_rows)
     const float Qrow = s_Q;
     const int Urow = s_U;
-    const int a0 = (int)(q * P.A), a1 = P.Ka;
+    const int a0 = (int)(q * P.seg_A), a1 = P.Ka;
     const unsigned long long n = (unsigned long long)(a1 - a0) * P.Kb;
     unsigned long long mine = ~0ull;
     for (unsigned long long li = (unsigned long long)part * blockDim.x + threadIdx.x; li < n;
@@ -116,7 +116,7 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   // the winner's a and b digits, then its per-LLM FP64 terms gathered in parallel (one thread per LLM)
   const bool win = found && s_best != ~0ull;
   if (win && threadIdx.x == 0) {
-    const int a = (int)(q * P.A) + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
+    const int a = (int)(q * P.seg_A) + (int)(s_best / P.Kb), b = (int)(s_best % P.Kb);
     if (P.a_llm >= 0) s_k[P.a_llm] = a;
     s_k[P.b_llm] = b;
   }

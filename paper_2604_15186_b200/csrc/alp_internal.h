@@ -117,6 +117,9 @@ struct SearchArgs {
   int grab, grab2;       // items per dynamic work grab: tickets [0, grab_t1) take grab, later ones grab2
   unsigned long long grab_t1;
   FastDiv fd_nQ, fd_ng;  // item -> (chunk, group, a-range) decode when item_hi < 2^31
+  // segment ids (key low word): row * seg_q + (first a option evaluated) / seg_A, where seg_A = 1
+  // (single-option granularity) when rows * Ka < 2^32, else seg_A = A; seg_mul = A / seg_A
+  uint32_t seg_q, seg_A, seg_mul;
   int budget;            // R (capped at the total max units); max over queries when q_budget is set
   const int *q_budget;   // [n_targets] per-query budgets (capped) or nullptr (all = budget)
   int n_targets;

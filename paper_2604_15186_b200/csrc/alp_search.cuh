@@ -237,11 +237,12 @@ __device__ __forceinline__ void eval_row(uint32_t rp, const float (&Qa)[T], floa
 }
 
 // Fold a lane tile's per-row minima into the thread's best (value, segment).  Segment of a row =
-// row * nQ + q0, q0 = first a-range this warp evaluated for the row; K3 re-scans from there.
+// row * seg_q + qs, qs = (first a option this warp evaluated for the row) / seg_A; K3 re-scans from
+// there to the end of the row.
 // The row's canonical within-group index is read only when the row can improve the best.
 template <int T>
 __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc)[T], uint32_t tile, uint32_t chunk,
-                                          uint32_t q0, float &best, uint32_t &best_seg) {
+                                          uint32_t qs, float &best, uint32_t &best_seg) {
   // tile minimum first (FMNMX3 tree); the rows' canonical indices are read only when it can
   // improve the best (value, segment)
   float m = acc[0];
@@ -254,7 +255,7 @@ __device__ __forceinline__ void fold_rows(const SearchArgs &P, const float (&acc
   for (int i = 0; i < T; ++i) {
     if (acc[i] == m) {
       const uint32_t ec = __ldg(P.tile_e + (size_t)tile * T + i);  // canonical within-group index
-      bs = min(bs, (chunk * P.L + ec) * P.nQ + q0);
+      bs = min(bs, (chunk * P.L + ec) * P.seg_q + qs);
     }
   }
   if (m < best) {
@@ -376,7 +377,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
     // advance to the next item (q fastest); fold when the lane tile changes
     if (++q == P.nQ) {
       q = 0;
-      fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
+      fold_rows<T>(P, acc, ttile, tchunk, q0 * P.seg_mul, best, best_seg);
       loaded = false;
       if (++grp == P.n_groups) {
         grp = 0;
@@ -384,7 +385,7 @@ __device__ void process_items(const SearchArgs &P, const Smem &s, unsigned char 
       }
     }
   }
-  if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0, best, best_seg);
+  if (loaded) fold_rows<T>(P, acc, ttile, tchunk, q0 * P.seg_mul, best, best_seg);
   tk = __shfl_sync(0xffffffffu, tk, 0);
   }
 }

@@ -292,13 +292,14 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
     for (;;) {
       const uint32_t k = __reduce_min_sync(0xffffffffu, tnext);
       if (k >= n) break;
-      if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
+      if (P.dbg_ts && lane == 0 && blockIdx.x > 0) P.dbg_ts[blockIdx.x * 8 + 6] += 1;  // tickets taken (diagnostics)
       const uint32_t it = (uint32_t)P.item_lo + k;
       const uint32_t tq = fdiv(it, P.fd_nQ);
       const uint32_t q = it - tq * P.nQ;           // a-range of the row
       const uint32_t chunk = fdiv(tq, P.fd_ng);
       const uint32_t grp = tq - chunk * P.n_groups;
       const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
+      const uint32_t qs = q * P.seg_mul;             // segment slot of a0
       const float2 pf = cv.pfx(chunk);
       const int upfx = __float_as_int(pf.y);       // clamped at R + 1
       const uint32_t tile = grp * kWarpTiles + lane;
@@ -367,8 +368,12 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
           if constexpr (TAIL2) eval2<T>(__ldg(reinterpret_cast<const float2 *>(rb + 4 * NB4)), Qa, acc);
         }
       }
+      // the next ticket only now, not prefetched at the item's start: the warp scheduler favours the
+      // oldest warps, and a starved warp holding a prefetched ticket delays that item to the end of
+      // the kernel (C4: 0.4709 -> 0.4669 ms; 8-rank shard 0.0819 -> 0.0778 ms, tools/shard_timing.py)
+      if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
       cnt += (unsigned long long)c32 * nfin;
-      fold_rows<T>(P, acc, tile, chunk, q, best, best_seg);  // segment: from a-range q to the row's end
+      fold_rows<T>(P, acc, tile, chunk, qs, best, best_seg);  // segment: from a option a0 to the row's end
     }
     }
     unsigned long long key = (best < __int_as_float(0x7f800000))
