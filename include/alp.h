@@ -211,6 +211,36 @@ alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int
                                  const int64_t *d_gathered, int32_t world, void *d_workspace, void *stream,
                                  alp_result *out);
 
+/* ---- fused peer exchange: the cross-GPU reduction inside the search kernel ----
+ * Instead of a collective and a finalize launch, the last block of every rank's search kernel
+ * finalizes its own shard (its key's segment lies in its shard), stores its (key, count, result)
+ * rows into every rank's exchange buffer over NVLink peer memory (release flag per destination),
+ * waits for all ranks' rows in its own buffer (acquire), and reduces them: MIN key, SUM count, the
+ * winning rank's result — the same result as alp_finalize on the all-reduced pair, on every rank.
+ * Each rank owns one exchange buffer of alp_peer_bytes(n, world) bytes from alp_peer_alloc on its
+ * device; the ranks share them by IPC handles (alp_peer_ipc_handle / alp_peer_open, e.g. through
+ * the process group) or, inside one process, by plain device pointers.  All ranks must call
+ * alp_search_peer the same number of times with the same (targets, budget, world) and their own
+ * buffer at d_bufs[rank]: the buffers count exchanges (epochs) and alternate two row slots. */
+size_t alp_peer_bytes(int32_t n_targets, int32_t world);     /* 0 if n_targets < 1 or world < 1 */
+/* Zero-filled device allocation of its own (IPC-shareable) on the current device. */
+alp_status alp_peer_alloc(size_t bytes, void **d_buf);
+alp_status alp_peer_free(void *d_buf);
+/* 64-byte cudaIpcMemHandle_t of a buffer from alp_peer_alloc (written to handle). */
+alp_status alp_peer_ipc_handle(void *d_buf, void *handle);
+/* Map another process's buffer into this one (cudaIpcOpenMemHandle; not for this process's own). */
+alp_status alp_peer_open(const void *handle, void **d_peer);
+alp_status alp_peer_close(void *d_peer);
+/* Search items [lo, hi) (alp_shard_range(rank, world) in a real run) and exchange with the other
+ * world-1 ranks; n <= 8 targets, a fused-size problem (M*K <= 1024, Ka*Kb <= 65536: C1, C2, C4,
+ * the hand case; others ALP_EINVAL — use alp_search_shard + a collective).  d_bufs[world]: every
+ * rank's buffer as mapped in this process.  Synchronous: returns with out[n] (identical on every
+ * rank) on the host.  ALP_EINTERNAL if the other ranks do not arrive within ALP_PEER_TIMEOUT_MS
+ * (default 30000).  d_workspace / stream as in alp_search_shard. */
+alp_status alp_search_peer(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
+                           uint64_t hi, int32_t rank, int32_t world, void *const *d_bufs, void *d_workspace,
+                           void *stream, alp_result *out);
+
 /* Device time (ms) of the last search kernel launched through this handle (CUDA events on the
  * launching stream), and the number of kernels the last search/finalize launched.  Searches with
  * short b rows and a common budget run the uniform-register pair (option terms + constant-bank

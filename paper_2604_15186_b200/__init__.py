@@ -54,7 +54,9 @@ EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidat
            "alp_option_table", "alp_predict", "alp_search", "alp_search_batch", "alp_num_items", "alp_shard_range",
            "alp_search_shard", "alp_finalize", "alp_finalize_gathered", "alp_last_kernel_ms", "alp_last_launches",
            "alp_last_step_ms", "alp_last_path", "alp_last_error", "alp_plan_cache_clear", "alp_search_queries",
-           "alp_schedule_egalitarian", "alp_workflow_stats", "alp_place", "alp_workspace_bytes"]
+           "alp_schedule_egalitarian", "alp_workflow_stats", "alp_place", "alp_workspace_bytes",
+           "alp_peer_bytes", "alp_peer_alloc", "alp_peer_free", "alp_peer_ipc_handle", "alp_peer_open",
+           "alp_peer_close", "alp_search_peer"]
 
 _lib = None
 
@@ -86,6 +88,10 @@ def lib():
             "alp_schedule_egalitarian": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp]),
             "alp_workflow_stats": (i32, [i32, i32, i64, vp, vp, vp, vp, vp, vp]),
             "alp_place": (i32, [i32, i32, vp, vp, i32, vp, vp, vp, vp]),
+            "alp_peer_bytes": (ctypes.c_size_t, [i32, i32]), "alp_peer_alloc": (i32, [ctypes.c_size_t, vp]),
+            "alp_peer_free": (i32, [vp]), "alp_peer_ipc_handle": (i32, [vp, vp]), "alp_peer_open": (i32, [vp, vp]),
+            "alp_peer_close": (i32, [vp]),
+            "alp_search_peer": (i32, [vp, vp, i32, i64, u64, u64, i32, i32, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -148,6 +154,40 @@ def place(gpu_node, gpu_domain, F: int, share_units, tp, replicas):
     _check(lib().alp_place(len(gn), F, gn.ctypes.data, gd.ctypes.data, len(s), s.ctypes.data, t.ctypes.data,
                            r.ctypes.data, out.ctypes.data))
     return out.tolist()
+
+
+class PeerBuffer:
+    """An exchange buffer of the fused peer exchange (alp_peer_alloc on the current device), or a
+    mapping of another process's buffer (from_ipc).  Frees / unmaps on close."""
+
+    def __init__(self, ptr: int, owned: bool):
+        self.ptr, self._owned = ptr, owned
+
+    @staticmethod
+    def nbytes(n_targets: int, world: int) -> int:
+        return int(lib().alp_peer_bytes(n_targets, world))
+
+    @classmethod
+    def alloc(cls, n_targets: int, world: int) -> "PeerBuffer":
+        p = ctypes.c_void_p()
+        _check(lib().alp_peer_alloc(cls.nbytes(n_targets, world), ctypes.byref(p)))
+        return cls(p.value, True)
+
+    def ipc_handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        _check(lib().alp_peer_ipc_handle(ctypes.c_void_p(self.ptr), h))
+        return h.raw
+
+    @classmethod
+    def from_ipc(cls, handle: bytes) -> "PeerBuffer":
+        p = ctypes.c_void_p()
+        _check(lib().alp_peer_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
+        return cls(p.value, False)
+
+    def close(self):
+        if self.ptr:
+            (lib().alp_peer_free if self._owned else lib().alp_peer_close)(ctypes.c_void_p(self.ptr))
+        self.ptr = 0
 
 
 def _check(st: int, ok=(ALP_OK,)) -> int:
@@ -389,6 +429,17 @@ class Alp:
         out = (_Result * len(t))()
         _check(lib().alp_finalize_gathered(self._h, t.ctypes.data, len(t), budget, gathered_ptr, world,
                                            workspace_ptr, _stream(stream_ptr), out), (ALP_OK, ALP_EINFEASIBLE))
+        return [Result._from(x) for x in out]
+
+    def search_peer(self, targets: Sequence[float], budget: int, lo: int, hi: int, rank: int, bufs: Sequence[int],
+                    stream_ptr: int | None = None, workspace_ptr: int | None = None) -> list[Result]:
+        """alp_search_peer: search items [lo, hi) and reduce across the len(bufs) ranks inside the
+        kernel over peer memory (bufs = every rank's exchange buffer pointer in this process)."""
+        t = _arr(targets, np.float64)
+        b = (ctypes.c_void_p * len(bufs))(*bufs)
+        out = (_Result * len(t))()
+        _check(lib().alp_search_peer(self._h, t.ctypes.data, len(t), budget, lo, hi, rank, len(bufs), b,
+                                     workspace_ptr, _stream(stream_ptr), out), (ALP_OK, ALP_EINFEASIBLE))
         return [Result._from(x) for x in out]
 
     @property

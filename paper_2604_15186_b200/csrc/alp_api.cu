@@ -1031,12 +1031,19 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
     ua.off_btab = off;
     off = a16(off + rows0 * cstride * 4);
   }
+  // room for the fused finalize's staged inputs (the epilogue reuses the search's shared memory;
+  // up to 8 KB keeps 24 one-warp blocks per SM)
+  const int stage = (int)finalize_stage_bytes(h->M, h->K, h->nS, h->nT, h->nR);
+  ua.fin.stage = stage <= 8192 ? 1 : 0;
+  if (ua.fin.stage && stage > off) off = a16(stage);
   ua.smem_bytes = off;
   const long long okey = (1ll << 60) | ((long long)ua.smem_bytes << 8) | ua.bchunk_wpad;
   auto oit = h->occ_cache.find(okey);
   const int bps = (oit != h->occ_cache.end()) ? oit->second : (h->occ_cache[okey] = search_u_max_blocks_per_sm(ua));
   if (bps < 1) return false;
-  int use = bps;
+  // 24 one-warp blocks per SM (6 per SMSP): more when ptxas allocates fewer registers was slower
+  // (C4 0.4507 vs 0.4362 ms at 28 blocks/SM with 71 registers, tools/shard_timing.py)
+  int use = std::min(bps, 24);
   if (const char *v = getenv("ALP_U_BPS")) use = std::max(1, std::min(bps, atoi(v)));  // tuning knob
   grid = h->sm_count * use;
   return true;
@@ -1063,7 +1070,8 @@ int ur_batch_group(alp_s *h, int64_t budget) {
 alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *budgets, int n, int64_t budget,
                              uint64_t lo, uint64_t hi, cudaStream_t st, unsigned long long *keys,
                              unsigned long long *counts, bool fuse_finalize = false,
-                             alp_result *fused_out = nullptr, bool first_of_batch = true, void *ws = nullptr) {
+                             alp_result *fused_out = nullptr, bool first_of_batch = true, void *ws = nullptr,
+                             const PeerArgs *peer = nullptr) {
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
   CU(cudaSetDevice(h->device));
@@ -1072,6 +1080,10 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   if (first_of_batch) CU(cudaEventRecord(h->evs0, st));  // step start (a batch of launches: the first)
   s = select_scratch(h, ws, n, st);
   if (s != ALP_OK) return s;
+  if (peer) {  // the rank's own (key, count) stay in the call's scratch
+    keys = h->sc.keys;
+    counts = h->sc.counts;
+  }
   s = prepare_budgets(h, budgets, n, st, &budget);
   if (s != ALP_OK) return s;
   const bool fused = use_fused(h, n, budgets);
@@ -1087,7 +1099,17 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
   // (same keys and counts), so searches on distinct workspaces and streams overlap.
   SearchArgs ua;
   int ugrid = 0;
-  const bool ur = !budgets && ur_path(h, g.a, n, hi, ua, ugrid) && !(h->sc.ws && search_u_busy());
+  // (a peer search never waits for the bank either: the search holding it may be another rank of
+  // the same exchange on this device, which waits for this one)
+  bool ur = !budgets && ur_path(h, g.a, n, hi, ua, ugrid);
+  if (ur && peer) ur = search_u_claim();             // released by the launch (or below on an error)
+  else if (ur && h->sc.ws) ur = !search_u_busy();
+  struct Claim {
+    bool on;
+    ~Claim() {
+      if (on) search_u_release();  // no-op after the launch
+    }
+  } claim{ur && peer};
   const bool accum = fused || ur;  // self-resetting accumulators + last-block epilogue (no K1)
   const size_t nctr = (size_t)n * (ur ? ua.u_nch : g.a.n_bchunks);
   int launches = 0;
@@ -1096,7 +1118,12 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     if (nctr > kFusedWork) return fail(ALP_EINTERNAL, "fused search: %zu work counters", nctr);
     FusedArgs &z = g.a.fz;
     z.on = 1;
-    z.finalize = (fuse_finalize && fused) ? 1 : 0;
+    z.finalize = ((fuse_finalize || peer) && fused) ? 1 : 0;
+    if (peer) {
+      if (!fused) return fail(ALP_EINVAL, "peer exchange needs a fused search (<= %d targets, M*K <= %d, Ka*Kb <= %llu)",
+                              kInlineTargets, kFusedMaxTerms, (unsigned long long)kFusedMaxRescan);
+      z.peer = *peer;
+    }
     if (!h->from_terms) z.prof = h->dprof();
     for (int i = 0; i < kInlineTargets; ++i) z.tgt[i] = i < n ? targets[i] : 0.0;
     z.tau_fixed = h->from_terms ? h->d_tau_fixed : nullptr;
@@ -1137,13 +1164,14 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     if (ur && !ur_path(h, g.a, n, hi, ua, ugrid)) return fail(ALP_EINTERNAL, "uniform-register geometry changed");
     const int dgrid = ur ? ugrid : g.grid;
     if (dbg) {
-      CU(h->g_dbg.ensure((size_t)dgrid * 8));
-      CU(cudaMemsetAsync(h->g_dbg.p, 0, (size_t)dgrid * 8 * sizeof(unsigned long long), st));
+      CU(h->g_dbg.ensure((size_t)(dgrid + 2) * 8));  // + one row of epilogue stamps
+      CU(cudaMemsetAsync(h->g_dbg.p, 0, (size_t)(dgrid + 2) * 8 * sizeof(unsigned long long), st));
       g.a.dbg_ts = ua.dbg_ts = h->g_dbg.p;
     }
     if (ur) {  // option terms + tables, then the UR search
       // the kernel-time events bracket the search kernel itself (ev0 re-recorded after the prep)
       CU(launch_search_u(ua, ugrid, st, first_of_batch ? h->ev0 : nullptr));
+      claim.on = false;  // the launch ended the claim
       launches += 2;
       h->last_ur = true;
     } else {
@@ -1152,7 +1180,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
       h->last_ur = false;
     }
     if (dbg) {
-      std::vector<unsigned long long> ts((size_t)dgrid * 8);
+      std::vector<unsigned long long> ts((size_t)(dgrid + 2) * 8);
       CU(cudaMemcpyAsync(ts.data(), h->g_dbg.p, ts.size() * 8, cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
       unsigned long long t0 = ~0ull;
@@ -1579,6 +1607,89 @@ alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int
   if (s != ALP_OK) return s;
   return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_gathered),
                        nullptr, stream ? (cudaStream_t)stream : h->stream, out, world, d_workspace);
+}
+
+size_t alp_peer_bytes(int32_t n_targets, int32_t world) {
+  if (n_targets < 1 || world < 1) return 0;
+  return kPeerHdr + 2 * (size_t)world * n_targets * sizeof(PeerRow);
+}
+
+alp_status alp_peer_alloc(size_t bytes, void **d_buf) {
+  if (!d_buf || bytes < kPeerHdr) return fail(ALP_EINVAL, "d_buf is NULL or bytes < alp_peer_bytes");
+  *d_buf = nullptr;
+  void *p = nullptr;
+  CU(cudaMalloc(&p, bytes));  // a whole allocation of its own: IPC handles name allocations
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(ALP_ECUDA, "alp_peer_alloc: %s", cudaGetErrorString(e));
+  }
+  *d_buf = p;
+  return ALP_OK;
+}
+
+alp_status alp_peer_free(void *d_buf) {
+  if (d_buf) CU(cudaFree(d_buf));
+  return ALP_OK;
+}
+
+alp_status alp_peer_ipc_handle(void *d_buf, void *handle) {
+  if (!d_buf || !handle) return fail(ALP_EINVAL, "d_buf/handle is NULL");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handles");
+  cudaIpcMemHandle_t hd;
+  CU(cudaIpcGetMemHandle(&hd, d_buf));
+  memcpy(handle, &hd, sizeof(hd));
+  return ALP_OK;
+}
+
+alp_status alp_peer_open(const void *handle, void **d_peer) {
+  if (!handle || !d_peer) return fail(ALP_EINVAL, "handle/d_peer is NULL");
+  *d_peer = nullptr;
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  CU(cudaIpcOpenMemHandle(d_peer, hd, cudaIpcMemLazyEnablePeerAccess));
+  return ALP_OK;
+}
+
+alp_status alp_peer_close(void *d_peer) {
+  if (d_peer) CU(cudaIpcCloseMemHandle(d_peer));
+  return ALP_OK;
+}
+
+alp_status alp_search_peer(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
+                           uint64_t hi, int32_t rank, int32_t world, void *const *d_bufs, void *d_workspace,
+                           void *stream, alp_result *out) {
+  NvtxRange nv("alp_search_peer");
+  if (!h) return fail(ALP_EINVAL, "handle is NULL");
+  if (!out) return fail(ALP_EINVAL, "out is NULL");
+  if (!d_bufs) return fail(ALP_EINVAL, "d_bufs is NULL");
+  if (world < 1 || world > kMaxPeers) return fail(ALP_EINVAL, "world must be in [1, %d]", kMaxPeers);
+  if (rank < 0 || rank >= world) return fail(ALP_EINVAL, "rank %d outside [0, %d)", rank, world);
+  alp_status s = check_targets(targets, n);
+  if (s != ALP_OK) return s;
+  if (n > kInlineTargets) return fail(ALP_EINVAL, "peer exchange: at most %d targets per call", kInlineTargets);
+  PeerArgs pa{};
+  pa.on = 1;
+  pa.rank = rank;
+  pa.world = world;
+  for (int j = 0; j < world; ++j) {
+    if (!d_bufs[j]) return fail(ALP_EINVAL, "d_bufs[%d] is NULL", j);
+    pa.buf[j] = static_cast<unsigned char *>(d_bufs[j]);
+  }
+  static const long long timeout_ms = getenv("ALP_PEER_TIMEOUT_MS") ? atoll(getenv("ALP_PEER_TIMEOUT_MS")) : 30000;
+  pa.timeout_ns = timeout_ms * 1000000ll;
+  alp_result *hzc = nullptr, *zc = zero_copy_out(n, &hzc);
+  if (!zc) return fail(ALP_ECUDA, "no mapped pinned memory for %d results", n);
+  pa.out = zc;
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  s = search_shard_impl(h, targets, nullptr, n, budget_units, lo, hi, st, nullptr, nullptr, false, nullptr, true,
+                        d_workspace, &pa);
+  if (s != ALP_OK) return s;
+  s = collect_results(h, n, st, out, hzc);
+  for (int t = 0; t < n; ++t)
+    if (out[t].found < 0) return fail(ALP_EINTERNAL, "peer exchange timed out (rank %d of %d)", rank, world);
+  return s;
 }
 
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,

@@ -13,14 +13,35 @@ namespace alp {
 // winning segment, the winner's (share, tp, replicas) and its FP64 Eq. 1 / Eq. 2 prediction.
 // Blocks [part] of [nparts] split the re-scan of the segment; with nparts > 1 the last block to
 // finish (ticket) assembles the result and resets the target's scratch.  Called by every thread
-// of a block (K3, or the last block of the fused search).
+// of a block (K3, or the last block of the fused search).  stage: the block's dynamic shared
+// memory is free and holds finalize_stage_bytes — every input (option terms, units, FP64 terms,
+// grids) is copied there in one wave of loads first, so the dependent steps (digits, re-scan,
+// winner terms) read shared memory instead of waiting on L2 / DRAM one round trip each.
 __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long long key, unsigned long long count,
-                                       int part, int nparts, const float *tau_s = nullptr) {
+                                       int part, int nparts, const float *tau_s = nullptr,
+                                       alp_result *out_row = nullptr, bool stage = false) {
   const FinalizeExtra &F = P.fin;
-  const int K = P.K;
-  // option terms of target t: the caller's shared-memory copy (fused kernel) or the global table
-  const float *tau_g = P.tau + (size_t)t * P.M * K;
-  auto tau = [&](int i) { return tau_s ? tau_s[i] : __ldcg(tau_g + i); };
+  const int K = P.K, MK = P.M * K, nG = F.nS + F.nT + F.nR;
+  auto stamp = [&](int i) {  // ALP_DBG_TS (fused epilogue only): phases in the second extra row
+    if (P.dbg_ts && threadIdx.x == 0 && P.fz.on) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      P.dbg_ts[(size_t)gridDim.x * 8 + 8 + i] = g;
+    }
+  };
+  stamp(0);
+  // option terms of target t: the caller's shared-memory copy (fused kernel) or the global tables
+  const float *tau_g = P.tau + (size_t)t * MK;
+  const double *term_g = F.term + (size_t)t * MK, *b_g = F.b + (size_t)t * MK;
+  extern __shared__ __align__(16) unsigned char fin_stage[];  // the block's dynamic shared memory
+  double *st_term = reinterpret_cast<double *>(fin_stage), *st_b = st_term + MK;
+  float *st_tau = reinterpret_cast<float *>(st_b + MK);
+  int *st_u = reinterpret_cast<int *>(st_tau + MK), *st_g = st_u + MK;
+  auto tau = [&](int i) { return stage ? st_tau[i] : (tau_s ? tau_s[i] : __ldcg(tau_g + i)); };
+  auto uni = [&](int i) { return stage ? st_u[i] : P.u[i]; };
+  auto term = [&](int i) { return stage ? st_term[i] : __ldcg(term_g + i); };
+  auto bterm = [&](int i) { return stage ? st_b[i] : __ldcg(b_g + i); };
+  auto grid = [&](int i) { return stage ? st_g[i] : (i < F.nS ? F.S[i] : i < F.nS + F.nT ? F.T[i - F.nS] : F.R[i - F.nS - F.nT]); };
   __shared__ unsigned long long s_best;
   __shared__ int s_k[ALP_MAX_M], s_u[ALP_MAX_M], s_grid[3][ALP_MAX_M];
   __shared__ float s_tq[ALP_MAX_M];
@@ -31,6 +52,18 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   const uint32_t seg = (uint32_t)(key & 0xffffffffull);
   const float val = __uint_as_float((uint32_t)(key >> 32));
   const bool found = key != kKeyNone && val < __int_as_float(0x7f800000);
+  if (found && stage) {
+    for (int i = threadIdx.x; i < MK; i += blockDim.x) {
+      st_term[i] = __ldcg(term_g + i);
+      st_b[i] = __ldcg(b_g + i);
+      st_tau[i] = tau_s ? tau_s[i] : __ldcg(tau_g + i);
+      st_u[i] = P.u[i];
+    }
+    if (F.S)
+      for (int i = threadIdx.x; i < nG; i += blockDim.x)
+        st_g[i] = i < F.nS ? F.S[i] : i < F.nS + F.nT ? F.T[i - F.nS] : F.R[i - F.nS - F.nT];
+    __syncthreads();
+  }
   uint32_t q = 0, chunk = 0, e = 0;
   if (found) {
     q = seg % P.seg_q;  // segment slot: first a option = q * seg_A
@@ -51,11 +84,12 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
       }
       s_k[m] = (int)d;
       s_tq[m] = tau(m * K + (int)d);
-      s_u[m] = P.u[m * K + (int)d];
+      s_u[m] = uni(m * K + (int)d);
     }
   }
   if (threadIdx.x == 0) s_best = ~0ull;
   __syncthreads();
+  stamp(1);
   if (found && threadIdx.x == 0) {
     // canonical partial sum over LLMs 0..g1-1: ((0 + tau_0) + tau_1) + ...
     float Q = 0.f;
@@ -69,7 +103,7 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   }
   __syncthreads();
   if (found) {
-    // the segment starts at a-range q and runs to the end of the row (see fold_rows)
+    // the segment starts at a option q * seg_A and runs to the end of the row (see fold_rows)
     const float Qrow = s_Q;
     const int Urow = s_U;
     const int a0 = (int)(q * P.seg_A), a1 = P.Ka;
@@ -83,10 +117,10 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
       int ua = 0;
       if (P.a_llm >= 0) {
         ta = tau(P.a_llm * K + a);
-        ua = P.u[P.a_llm * K + a];
+        ua = uni(P.a_llm * K + a);
       }
       const float v = __fadd_rn(__fadd_rn(Qrow, ta), tau(P.b_llm * K + b));
-      const int units = Urow + ua + P.u[P.b_llm * K + b];
+      const int units = Urow + ua + uni(P.b_llm * K + b);
       if (v == val && units <= qbudget(P, t)) {
         mine = li;
         break;
@@ -95,6 +129,7 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
     atomicMin(&s_best, mine);
   }
   __syncthreads();
+  stamp(2);
   if (nparts > 1) {
     // combine the blocks of this target: global min, then only the last block continues
     __shared__ unsigned s_last;
@@ -123,16 +158,17 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   __syncthreads();
   if (win && (int)threadIdx.x < P.M) {
     const int m = threadIdx.x, km = s_k[m];
-    s_term[m] = __ldcg(F.term + ((size_t)t * P.M + m) * K + km);
-    s_bterm[m] = __ldcg(F.b + ((size_t)t * P.M + m) * K + km);
-    s_u[m] = P.u[m * K + km];
+    s_term[m] = term(m * K + km);
+    s_bterm[m] = bterm(m * K + km);
+    s_u[m] = uni(m * K + km);
     if (F.S) {
-      s_grid[0][m] = F.S[km / (F.nR * F.nT)];
-      s_grid[1][m] = F.T[(km / F.nR) % F.nT];
-      s_grid[2][m] = F.R[km % F.nR];
+      s_grid[0][m] = grid(km / (F.nR * F.nT));
+      s_grid[1][m] = grid(F.nS + (km / F.nR) % F.nT);
+      s_grid[2][m] = grid(F.nS + F.nT + km % F.nR);
     }
   }
   __syncthreads();
+  stamp(3);
   if (threadIdx.x == 0) {
     alp_result &r = s_res;
     memset(&r, 0, sizeof(r));
@@ -171,9 +207,10 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   // one coalesced copy of the result (device memory, or mapped host memory for the fused search)
   static_assert(sizeof(alp_result) % 4 == 0, "alp_result is copied as 32-bit words");
   const uint32_t *src = reinterpret_cast<const uint32_t *>(&s_res);
-  uint32_t *dst = reinterpret_cast<uint32_t *>(F.out + t);
+  uint32_t *dst = reinterpret_cast<uint32_t *>(out_row ? out_row : F.out + t);
   for (int i = threadIdx.x; i < (int)(sizeof(alp_result) / 4); i += blockDim.x) dst[i] = src[i];
   __syncthreads();  // shared scratch reused by the next target
+  stamp(4);
 }
 
 }  // namespace alp

@@ -81,7 +81,35 @@ struct FinalizeExtra {
   alp_result *out;       // [n_t] device
   unsigned long long *best;  // [n_t] scratch: complemented minimum, 0 between calls (self-resetting)
   unsigned *done;            // [n_t] scratch: 0 between calls (self-resetting)
+  int stage;                 // the fused epilogue may stage the finalize inputs in dynamic smem
 };
+
+// Peer exchange (alp_search_peer): the fused epilogue of every rank's search finalizes its own
+// shard, writes the (key, count, local result) rows into every rank's exchange buffer over
+// NVLink peer memory, and waits for all ranks' rows in its own buffer; then it reduces them (MIN
+// key, SUM count) and stores the winner's result.  Exchange buffer of a rank (alp_peer_bytes):
+//   [0, 8)    epoch of the last completed exchange (read / written by the owner only)
+//   [64, ...) u64 flags[2][kMaxPeers]: flags[p][j] = epoch of rank j's rows in slot p
+//   [kPeerHdr, ...) PeerRow rows[2][world][n]: slot p = epoch & 1 (double-buffered: a rank may
+//   start epoch e + 1 while a slower rank still reads epoch e)
+constexpr int kMaxPeers = 16;
+constexpr size_t kPeerHdr = 512;
+struct PeerRow {
+  unsigned long long key, count;  // the rank's reduced key (kKeyNone: nothing feasible) and count
+  alp_result res;                 // the rank's finalize of its key (its own shard)
+};
+struct PeerArgs {
+  int on, rank, world;
+  unsigned char *buf[kMaxPeers];  // every rank's exchange buffer as mapped in this process
+  alp_result *out;                // [n] final results (mapped host memory)
+  long long timeout_ns;           // give up waiting for the other ranks after this long
+};
+
+// Bytes of the finalize's optional shared-memory staging (see finalize_target): FP64 Eq. 1 and
+// Eq. 2 terms, binary32 terms and units of every option, and the share / TP / replica grids.
+__host__ __device__ inline size_t finalize_stage_bytes(int M, int K, int nS, int nT, int nR) {
+  return (size_t)M * K * (8 + 8 + 4 + 4) + (size_t)(nS + nT + nR) * 4;
+}
 
 // Fused single-launch search (targets <= kInlineTargets): every block computes the option terms of
 // the phase's target in its prologue (no K1), blocks accumulate into self-resetting scratch, and
@@ -99,6 +127,7 @@ struct FusedArgs {
   unsigned long long *work;        // [n_t * n_bchunks] 0 at rest
   unsigned *ticket;                // 0 at rest
   int off_opt;                // smem offset of the phase's option terms [M*K] floats
+  PeerArgs peer;              // peer exchange in the epilogue (peer.on)
 };
 
 // Search kernel (K2) arguments: the static plan + per-search values.
@@ -204,6 +233,8 @@ cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search);
 int search_u_max_blocks_per_sm(const SearchArgs &a);
 bool search_u_busy();  // a uniform-register search launched on this device has not completed yet
+bool search_u_claim(); // take the bank for a peer search if it is free (see alp_search_u.cu)
+void search_u_release();
 size_t uprep_smem_bytes(const SearchArgs &a);  // k_uprep dynamic shared memory (<= kUPrepSmemMax)
 constexpr size_t kUPrepSmemMax = 200 * 1024;
 constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path

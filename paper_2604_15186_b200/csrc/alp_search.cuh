@@ -415,9 +415,163 @@ __device__ inline void fused_terms(const SearchArgs &P, const Smem &s, int t, bo
   __syncthreads();
 }
 
+// ------------------------------------------------------------------ peer exchange (alp_search_peer)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long globaltimer_ns() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return (long long)g;
+}
+
+// The cross-GPU reduction inside the search kernel's last block, over peer
+// memory instead of a collective + K3 launch.  The epilogue (inlined: kernel parameters come from
+// the constant bank) finalizes this rank's own (key, count) into its row of slot p = epoch & 1 (its
+// key's segment lies in its own shard, so the local re-scan is the global one if this key wins);
+// then peer_exchange stores the (key, count, result) rows into slot p of every rank's buffer
+// (NVLink stores), publishes them with one system-scope fence + a flag per destination, waits for
+// all ranks' flags in the own buffer (acquire), and takes the MIN over the keys, the SUM over the
+// counts and the winning rank's result.  Keys carry global segment ids and whole rows live on one
+// rank, so equal keys never come from two ranks.  Buffer layout: PeerRow, kPeerHdr (alp_internal.h).
+__device__ __forceinline__ PeerRow *peer_rows(unsigned char *b, unsigned long long e, int W, int n, int j) {
+  return reinterpret_cast<PeerRow *>(b + kPeerHdr) + ((size_t)(e & 1) * W + j) * n;
+}
+__device__ __forceinline__ unsigned long long *peer_flag(unsigned char *b, unsigned long long e, int j) {
+  return reinterpret_cast<unsigned long long *>(b + 64) + (size_t)(e & 1) * kMaxPeers + j;
+}
+
+// Not inlined (ptxas keeps the search loops' uniform datapath only while this code stays out of the
+// kernel body); everything it needs comes in as scalars or from shared memory (a reference to the
+// kernel parameters would turn every field access into a generic load).
+static __device__ __noinline__ void peer_exchange(unsigned char *const *s_buf, int me, int W, int n,
+                                                  unsigned long long e, alp_result *out, long long timeout_ns,
+                                                  unsigned long long *dbg) {
+  static_assert(sizeof(PeerRow) % 8 == 0 && sizeof(alp_result) % 8 == 0, "rows move as 64-bit words");
+  auto stamp = [&](int i) {  // ALP_DBG_TS: the exchange's phases
+    if (dbg && threadIdx.x == 0) dbg[i] = (unsigned long long)globaltimer_ns();
+  };
+  __shared__ int s_fail;
+  unsigned char *own = s_buf[me];
+  const PeerRow *mine = peer_rows(own, e, W, n, me);
+  const int words = n * (int)(sizeof(PeerRow) / 8);
+  const unsigned long long *src = reinterpret_cast<const unsigned long long *>(mine);
+  for (int i = threadIdx.x; i < (W - 1) * words; i += blockDim.x) {
+    int j = i / words;
+    const int w = i - j * words;
+    j += (j >= me) ? 1 : 0;
+    reinterpret_cast<unsigned long long *>(peer_rows(s_buf[j], e, W, n, me))[w] = src[w];
+  }
+  if (threadIdx.x == 0) s_fail = 0;
+  // publish: every thread's row stores precede thread 0's system-scope fence (bar.sync orders them),
+  // then relaxed flag stores (the grid-barrier release pattern, at system scope)
+  __syncthreads();
+  stamp(2);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int j = 0; j < W; ++j)
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(peer_flag(s_buf[j], e, me)), "l"(e) : "memory");
+  }
+  stamp(3);
+  for (int j = threadIdx.x; j < W; j += blockDim.x) {
+    const unsigned long long *f = peer_flag(own, e, j);
+    const long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(f) != e) {
+      __nanosleep(64);
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        s_fail = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  stamp(4);
+  // reduce, one warp per target: lane j reads rank j's (key, count) (one parallel round trip), MIN
+  // (lowest rank on equal keys: only kKeyNone repeats) and SUM by shuffles; then the lanes copy the
+  // winning row's result, one 64-bit word each, into the final (mapped host) results
+  constexpr int kResW = (int)(sizeof(alp_result) / 8);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int t = warp; t < n; t += nw) {
+    unsigned long long k = ~0ull, c = 0ull;
+    if (lane < W) {
+      const PeerRow *r = peer_rows(own, e, W, n, lane) + t;
+      k = ld_relaxed_sys(&r->key);
+      c = ld_relaxed_sys(&r->count);
+    }
+    int jw = lane < W ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, jw, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (ok < k || (ok == k && oj < jw)) {
+        k = ok;
+        jw = oj;
+      }
+    }
+    const unsigned long long *rw = reinterpret_cast<const unsigned long long *>(&(peer_rows(own, e, W, n, jw) + t)->res);
+    unsigned long long *dw = reinterpret_cast<unsigned long long *>(out + t);
+    constexpr int kCnt = (int)(offsetof(alp_result, feasible_count) / 8), kFound = (int)(offsetof(alp_result, found) / 8);
+    for (int w = lane; w < kResW; w += 32) {
+      unsigned long long v = ld_relaxed_sys(rw + w);
+      if (w == kCnt) v = c;
+      if (w == kFound && s_fail) v = (v & ~0xffffffffull) | 0xffffffffull;  // found = -1: the host reports the timeout
+      dw[w] = v;
+    }
+  }
+  __syncthreads();
+  stamp(5);
+  if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long *>(own) = e;
+}
+
+// The peer epilogue (not inlined, see peer_exchange): a shared-memory copy of the kernel
+// parameters first (through the reference every field access would be a generic load, one
+// dependent round trip each in the finalize), then this rank's finalize into its own row, then the
+// exchange.
+static __device__ __noinline__ void peer_epilogue(const SearchArgs &Pg, const unsigned long long *s_key,
+                                                  const unsigned long long *s_cnt, const float *tau_last,
+                                                  bool stage) {
+  __shared__ __align__(16) unsigned char s_args[sizeof(SearchArgs)];
+  __shared__ unsigned char *s_buf[kMaxPeers];
+  __shared__ unsigned long long s_e;
+  static_assert(sizeof(SearchArgs) % 8 == 0, "SearchArgs copied as 64-bit words");
+  const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&Pg);
+  for (int i = threadIdx.x; i < (int)(sizeof(SearchArgs) / 8); i += blockDim.x)
+    reinterpret_cast<unsigned long long *>(s_args)[i] = src[i];
+  __syncthreads();
+  const SearchArgs &P = *reinterpret_cast<const SearchArgs *>(s_args);
+  const PeerArgs &X = P.fz.peer;
+  const int n = P.n_targets, W = X.world, me = X.rank;
+  unsigned long long *dbg = P.dbg_ts ? P.dbg_ts + (size_t)gridDim.x * 8 : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = (unsigned long long)globaltimer_ns();
+  for (int j = threadIdx.x; j < W; j += blockDim.x) s_buf[j] = X.buf[j];
+  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned long long *>(X.buf[me]) + 1;  // this epoch
+  __syncthreads();
+  const unsigned long long e = s_e;
+  PeerRow *mine = peer_rows(X.buf[me], e, W, n, me);
+  for (int t = 0; t < n; ++t)
+    finalize_target(P, t, s_key[t], s_cnt[t], 0, 1, t + 1 == n ? tau_last : nullptr, &mine[t].res, stage);
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    mine[t].key = s_key[t];
+    mine[t].count = s_cnt[t];
+  }
+  __syncthreads();
+  if (dbg && threadIdx.x == 0) dbg[1] = (unsigned long long)globaltimer_ns();
+  peer_exchange(s_buf, me, W, n, e, X.out, X.timeout_ns, dbg);
+}
+
 // Fused epilogue: the last block to finish writes the reduced (key, count) of every target, resets
-// the scratch to its rest state and (fz.finalize) finalizes every target.
-__device__ inline void fused_epilogue(const SearchArgs &P, const float *tau_last) {
+// the scratch to its rest state and (fz.finalize) finalizes every target, or (fz.peer.on) runs the
+// cross-GPU exchange.  stage: the finalize may stage its re-scan rows at the start of the block's
+// dynamic shared memory (the caller's search no longer uses it).
+__device__ inline void fused_epilogue(const SearchArgs &P, const float *tau_last, bool stage = false) {
   __shared__ unsigned s_last;
   __shared__ unsigned long long s_key[kInlineTargets], s_cnt[kInlineTargets];
   __syncthreads();
@@ -446,9 +600,13 @@ __device__ inline void fused_epilogue(const SearchArgs &P, const float *tau_last
       P.fin.done[t] = 0u;
     }
   __syncthreads();
+  if (P.fz.peer.on) {
+    peer_epilogue(P, s_key, s_cnt, tau_last, stage);
+    return;
+  }
   if (P.fz.finalize)  // the last target's option terms are still in shared memory (tau_last)
     for (int t = 0; t < P.n_targets; ++t)
-      finalize_target(P, t, s_key[t], s_cnt[t], 0, 1, t + 1 == P.n_targets ? tau_last : nullptr);
+      finalize_target(P, t, s_key[t], s_cnt[t], 0, 1, t + 1 == P.n_targets ? tau_last : nullptr, nullptr, stage);
 }
 
 // T = rows per lane; MB = minimum resident blocks per SM (register cap 65536 / (256 * MB)).

@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
   }
   stamp(2);
   pdl_trigger();
-  fused_epilogue(P, nullptr);
+  // the search's shared memory is free now: the finalize stages its inputs in it
+  fused_epilogue(P, nullptr, P.fin.stage);
   stamp(3);
 }
 
@@ -422,6 +423,7 @@ struct UState {
   cudaStream_t cap = nullptr, cap2 = nullptr;  // capture streams (cap2: the event branch)
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<UGraph> graphs;
+  bool claimed = false;  // a peer search took the bank (search_u_claim) and has not launched yet
 };
 static std::mutex g_u_mu;
 static UState &ustate() {
@@ -614,6 +616,7 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
     }
     if ((e = set_node_args(*gr, a, u.staging, before_search)) != cudaSuccess) return e;
     if ((e = cudaGraphLaunch(gr->exec, st)) != cudaSuccess) return e;
+    u.claimed = false;
     return cudaEventRecord(u.done, st);
   }
   k_uprep<<<1, threads, prep_smem, st>>>(a, u.staging);
@@ -621,12 +624,35 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
   if ((e = cudaMemcpyToSymbolAsync(cu_mem, u.staging, used, 0, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
   if (before_search && (e = cudaEventRecord(before_search, st)) != cudaSuccess) return e;
   if ((e = launch_u_search(a, grid, st)) != cudaSuccess) return e;
+  u.claimed = false;
   return cudaEventRecord(u.done, st);
+}
+
+// The bank for a peer search: taken only when free and not claimed, atomically with the check, so
+// two ranks of one exchange sharing a device never both take it (the second would wait for the
+// first, which waits for the second).  The claim ends at the launch (or search_u_release).
+bool search_u_claim() {
+  std::lock_guard<std::mutex> lock(g_u_mu);
+  UState &u = ustate();
+  if (u.claimed) return false;
+  const cudaError_t e = cudaEventQuery(u.done);
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();
+    return false;
+  }
+  u.claimed = true;
+  return true;
+}
+
+void search_u_release() {
+  std::lock_guard<std::mutex> lock(g_u_mu);
+  ustate().claimed = false;
 }
 
 bool search_u_busy() {
   std::lock_guard<std::mutex> lock(g_u_mu);
   UState &u = ustate();
+  if (u.claimed) return true;
   const cudaError_t e = cudaEventQuery(u.done);
   if (e == cudaErrorNotReady) {
     cudaGetLastError();  // not an error: clear it

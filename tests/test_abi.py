@@ -116,3 +116,32 @@ def test_gloo_two_rank_key_reduction():
         rows = [g[0:6], g[6:12]]
         assert [min(rows[0][i], rows[1][i]) for i in range(3)] == k
         assert [rows[0][3 + i] + rows[1][3 + i] for i in range(3)] == c
+
+
+def test_search_u_keeps_uniform_datapath():
+    """ptxas keeps k_search_u's b operands in uniform registers only while nothing perturbs its
+    analysis (a __syncwarp before the epilogue, an inlined exchange, a register cap each dropped it
+    silently: DESIGN.md §5).  Guard on the built object: every uniform-register search variant has
+    FADD2 with a uniform-register operand, no spills and <= 80 registers (24 one-warp blocks/SM)."""
+    import re
+    import shutil
+    import subprocess
+
+    from paper_2604_15186_b200 import build
+    build.build()
+    obj = os.path.join(os.path.dirname(build.LIB), "alp_search_u.o")
+    if not shutil.which("cuobjdump") or not os.path.exists(obj):
+        pytest.skip("cuobjdump or the object file is missing")
+    out = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
+    funcs = {f.split("\n", 1)[0].strip(): f for f in re.split(r"\n\s*Function : ", out)[1:]}
+    names = [n for n in funcs if "k_search_u" in n]
+    assert len(names) >= 18
+    for n in names:
+        ins = [ln.split("*/", 1)[1] for ln in funcs[n].split("\n") if re.match(r"\s*/\*[0-9a-f]{4,}\*/", ln)]
+        fadd2 = [i for i in ins if "FADD2" in i]
+        if fadd2:
+            assert any(re.search(r"\bUR\d", i) for i in fadd2), n
+        assert not any("STL" in i for i in ins), n
+    ptx = open(obj + ".ptxas.txt").read()
+    for m in re.finditer(r"Function properties for (\S*k_search_u\S*)\n.*\n.*Used (\d+) registers", ptx):
+        assert int(m.group(2)) <= 80, m.group(1)

@@ -26,20 +26,28 @@ B, t = d["budget_units"], list(d["targets"])
 keys = torch.empty(len(t), dtype=torch.int64, device="cuda")
 cnts = torch.empty(len(t), dtype=torch.int64, device="cuda")
 lo, hi = alp.shard_range(B, rank, world)
+mode = os.environ.get("SHARD_MODE", "nccl")
+buf = P.PeerBuffer.alloc(len(t), 1) if mode == "peer" else None
 for rep in range(4):
     if os.path.exists(dump):
         os.remove(dump)
-    alp.search_shard(t, B, lo, hi, keys.data_ptr(), cnts.data_ptr(), torch.cuda.current_stream().cuda_stream)
-    alp.finalize(t, B, keys.data_ptr(), cnts.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    if mode == "peer":
+        alp.search_peer(t, B, lo, hi, 0, [buf.ptr])
+    else:
+        alp.search_shard(t, B, lo, hi, keys.data_ptr(), cnts.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        alp.finalize(t, B, keys.data_ptr(), cnts.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
 ts = np.fromfile(dump, dtype=np.uint64).reshape(-1, 8)
+ep = ts[-2].astype(np.int64)  # peer epilogue phase stamps (extra rows)
+fz = ts[-1].astype(np.int64)  # finalize phase stamps
+ts = ts[:-2]
 g = ts.shape[0]
 t0 = ts[:, 0].min()
 rel = lambda c: (ts[:, c].astype(np.int64) - int(t0)) / 1e3
 start, tables, lend, end = rel(0), rel(1), rel(2), rel(3)
 tk = ts[:, 6].astype(np.int64)
 tk[0] = -1
-print(f"{name} world {world} rank {rank}: grid {g}, items {hi - lo}, kernel span {end.max():.1f} us, "
+print(f"[{mode}] {name} world {world} rank {rank}: grid {g}, items {hi - lo}, kernel span {end.max():.1f} us, "
       f"tables med {np.median(tables):.1f}, loop-end min/med/p90/max {lend.min():.1f}/{np.median(lend):.1f}/"
       f"{np.percentile(lend, 90):.1f}/{lend.max():.1f}")
 by = collections.defaultdict(list)
@@ -50,3 +58,11 @@ for k in sorted(by):
     print(f"  tickets {k:3d}: warps {len(v):5d}  loop-end min {v.min():6.1f} med {np.median(v):6.1f} max {v.max():6.1f}")
 h = np.histogram(lend[1:], bins=20)
 print("  loop-end histogram:", " ".join(f"{int(e):d}:{c}" for c, e in zip(h[0], h[1])))
+if ep[0]:
+    e0 = int(ts[:, 0].min())
+    print("  peer epilogue (us from kernel start):", " ".join(f"{(x - e0) / 1e3:.1f}" for x in ep[:6]),
+          "| phases: start, local finalize done, rows + fence, flags, all flags seen, reduced")
+if fz[0]:
+    e0 = int(ts[:, 0].min())
+    print("  finalize (us from kernel start):", " ".join(f"{(x - e0) / 1e3:.1f}" for x in fz[:5]),
+          "| phases: start, digits + row terms, re-scan, winner terms, result stored")

@@ -26,6 +26,8 @@ keys = torch.empty(len(t), dtype=torch.int64, device="cuda")
 cnts = torch.empty(len(t), dtype=torch.int64, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.Stream()
+mode = os.environ.get("SHARD_MODE", "nccl")  # nccl: shard search + K3 finalize; peer: alp_search_peer (1-rank exchange)
+buf = P.PeerBuffer.alloc(len(t), 1) if mode == "peer" else None
 ref = alp.search_batch(t, B)[-1]
 for world in worlds:
     per = []
@@ -35,8 +37,11 @@ for world in worlds:
         for rep in range(reps + 3):
             with torch.cuda.stream(st):
                 flush.zero_()
-                alp.search_shard(t, B, lo, hi, keys.data_ptr(), cnts.data_ptr(), st.cuda_stream)
-                alp.finalize(t, B, keys.data_ptr(), cnts.data_ptr(), st.cuda_stream)
+                if mode == "peer":  # search + in-kernel exchange (with itself) over the rank's range
+                    alp.search_peer(t, B, lo, hi, 0, [buf.ptr], st.cuda_stream)
+                else:
+                    alp.search_shard(t, B, lo, hi, keys.data_ptr(), cnts.data_ptr(), st.cuda_stream)
+                    alp.finalize(t, B, keys.data_ptr(), cnts.data_ptr(), st.cuda_stream)
             torch.cuda.synchronize()
             if rep >= 3:
                 ks.append(alp.last_kernel_ms)
@@ -48,5 +53,5 @@ for world in worlds:
            "step_ms_rank0": per[0][1], "kernel_ms_max": kmax, "step_ms_max": smax,
            "slowest_rank": max(range(world), key=lambda r: per[r][1]),
            "projected_cand_per_s": alp.num_candidates * len(t) / (smax * 1e-3),
-           "split": os.environ.get("ALP_U_SPLIT", "default")}
+           "mode": mode}
     print(json.dumps(out), flush=True)
