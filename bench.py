@@ -149,11 +149,18 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _config(d, N, world):
+def _config(d, N, world, exchange=None):
+    if world == 1:
+        par = "one GPU: the whole index space"
+    elif exchange == "peer":
+        par = f"index-space shard x{world} + fused peer exchange in the search kernel (NVLink stores, no collective)"
+    else:
+        par = f"index-space shard x{world} + NCCL all-gather of (key, count) pairs" + (
+            f" [{exchange}]" if exchange and exchange != "nccl" else "")
     return {"workload": f"{d['name']}: {d['description']}", "candidates": N * len(d["targets"]), "M": d["M"],
             "options_per_llm": len(d["share_units"]) * len(d["tp"]) * len(d["replicas"]),
             "budget_units": d["budget_units"], "F": d["F"], "target_req_s": d["targets"][0],
-            "n_targets": len(d["targets"]), "parallelism": f"index-space shard x{world} + NCCL all-gather of (key, count) pairs",
+            "n_targets": len(d["targets"]), "parallelism": par,
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -182,7 +189,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     import paper_2604_15186_b200 as P
-    from paper_2604_15186_b200.dist import gather_pairs
+    from paper_2604_15186_b200.dist import PeerExchange, gather_pairs
 
     d = load_workload(args.workload)
     B = int(d["budget_units"])
@@ -196,12 +203,25 @@ def run_ours(args):
     gathered = torch.empty(world * 2 * nt, dtype=torch.int64, device=dev)  # every rank's pairs
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    exchange = args.exchange if world > 1 else "none"
+    px = None
+    if exchange == "peer":
+        try:
+            px = PeerExchange(nt)  # IPC handles of every rank's exchange buffer over the group
+        except Exception as e:  # no peer access between these GPUs: the NCCL exchange instead
+            exchange = f"nccl (peer unavailable: {str(e)[:120]})"
+    ws = torch.zeros(alp.workspace_bytes(nt), dtype=torch.uint8, device=dev) if px is not None else None
+
     def run_step(a, lo_, hi_):
-        """One search step through the public API: at N=1 the single-GPU call (one fused kernel:
-        option terms + exhaustive search + finalize); at N>1 shard search, NCCL all-reduce of the
-        (key, count) pairs, device finalize."""
+        """One search step through the public API: at N=1 the single-GPU call (option terms +
+        exhaustive search + finalize); at N>1 shard search, then the exchange: the fused peer
+        exchange inside the search kernel (--exchange peer), or ONE NCCL all-gather of the
+        (key, count) pairs + the device finalize (--exchange nccl)."""
         if world == 1:
             return a.search_batch(targets, B)[-1]
+        if px is not None:
+            w2 = ws if a is alp else torch.zeros(a.workspace_bytes(nt), dtype=torch.uint8, device=dev)
+            return a.search_peer(targets, B, lo_, hi_, rank, px.ptrs, stream.cuda_stream, w2.data_ptr())[-1]
         with torch.cuda.stream(stream):
             a.search_shard(targets, B, lo_, hi_, pairs.data_ptr(), pairs.data_ptr() + 8 * nt, stream.cuda_stream)
             w = gather_pairs(pairs, gathered)  # ONE all-gather of the 16-byte (key, count) pairs
@@ -277,20 +297,27 @@ def run_ours(args):
         cand_rank = N * nt * (hi - lo) / max(1, alp.num_items(B))
         achieved = cand_rank / (kern_max / len(kern_ms) * 1e-3)  # per GPU, dominant kernel
         peak = sm_count * ISSUE_LANES_PER_SM_PER_CLK * f_max / INSTR_PER_CANDIDATE_MIN
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        # DRAM traffic and pipe utilisation of the search kernel cannot be measured inside a timed run
+        # (ncu replays kernels): they come from this round's committed `ncu --set full` capture of the
+        # same kernel on the same workload (profiles/ncu_summary.json, tools/collect_profiles.sh)
+        traffic, pipes = None, None
+        tp = os.path.join(ROOT, "profiles", "ncu_summary.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(args.workload)
+                ent = json.load(open(tp)).get(args.workload)
+                if ent:
+                    traffic = ent.get("dram_bytes")
+                    pipes = {k: ent[k] for k in ("fma_pipe_frac", "alu_pipe_frac", "issue_active_frac",
+                                                 "sass_instr_per_candidate", "kernel_us", "source") if k in ent}
             except Exception:
-                traffic = None
+                traffic, pipes = None, None
         line = {
             "metric": METRIC, "value": N * nt * args.steps / (tot_ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": tot_ms / args.steps,
             "time_to_optimum_ms": host_tot / args.steps, "host_ms_per_step": host_tot / args.steps,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded profile tables, workloads/instances)",
-            "config": _config(d, N, world),
+            "config": {**_config(d, N, world, exchange if world > 1 else None)},
             "result": {"index": res.index, "latency_key": res.latency_key, "latency_s": res.latency,
                        "throughput_req_s": res.throughput, "units": res.units,
                        "feasible_count": res.feasible_count},
@@ -299,7 +326,7 @@ def run_ours(args):
                          "kernel": {"k_search_u": "k_search_u (uniform-register search; after k_uprep: option "
                                                   "terms + constant-bank tables)",
                                     "k_search": "k_search (fused option terms + search)"}[alp.last_path],
-                         "kernel_ms": kern_max / len(kern_ms),
+                         "kernel_ms": kern_max / len(kern_ms), "pipes_ncu": pipes,
                          "peak_def": f"{sm_count} SMs x 128 issue lanes/clk x {f_max / 1e6:.0f} MHz / 1 instr per candidate"},
             "e2e": {"value": N * nt * len(e2e_ms) / (e2e_tot * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(P.ctypes.sizeof(P._Result)),
@@ -336,6 +363,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="N>1 cross-GPU reduction: NCCL all-gather + finalize kernel, or the fused peer exchange")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Copy the outputs of tools/run_final.sh (gpurun_out/) into profiles/ under the round prefix.
 set -e
-R=${1:-r01}
+R=${1:-r02}
 G=gpurun_out
 cp $G/bench_C4.json profiles/${R}_bench_C4.json
 cp $G/bench_C3.json profiles/${R}_bench_C3.json
@@ -21,17 +21,4 @@ python tools/sass_blocks.py $G/sass_C4.csv --candidates 11019960576 --top 30 > p
 cp $G/shard_timing.jsonl profiles/${R}_shard_scaling.jsonl
 cp $G/mb_pipes5.txt profiles/${R}_microbench_pipes5.txt
 cp $G/pytest_gpu.txt profiles/${R}_pytest_gpu.txt
-python - <<PY
-import csv, json
-out = {"_note": "dram__bytes_read.sum + dram__bytes_write.sum of one k_search launch (ncu --set full; profiles/${R}_C4_k_search_ncu_raw.csv, ${R}_C3_k_search_ncu_raw.csv)"}
-for w in ("C4", "C3"):
-    rows = list(csv.reader(open(f"profiles/${R}_{w}_k_search_ncu_raw.csv")))
-    h, u, v = rows[0], rows[1], rows[2]
-    tot = 0.0
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        x = float(v[h.index(k)]); unit = u[h.index(k)]
-        tot += x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-    out[w] = int(round(tot))
-json.dump(out, open("profiles/ncu_traffic.json", "w"))
-print(out)
-PY
+python tools/ncu_summary.py C4=profiles/${R}_C4_k_search_ncu_raw.csv C3=profiles/${R}_C3_k_search_ncu_raw.csv
