@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libscepsy_alp.so")
 SOURCES = ["alp_api.cu", "alp_kernels.cu", "alp_search_t8.cu", "alp_search_t12.cu", "alp_search_t16.cu",
-           "alp_search_u.cu"]
+           "alp_search_u.cu", "alp_levels.cu"]
 # every file under csrc/ (sources and headers) plus the public header is a dependency
 HEADERS = [os.path.join("..", "..", "include", "alp.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -320,6 +320,7 @@ struct alp_s {
   DBuf<unsigned char> g_ws;
   int g_ws_cap = 0;
   DBuf<unsigned long long> g_dbg;
+  DBuf<unsigned char> g_lv;  // one-pass budget sweep scratch (levels, level keys, histograms)
   cudaEvent_t evs0 = nullptr, evs1 = nullptr;  // step events: search start .. result D2H enqueued
   float last_step_ms = 0.f;
   int *s_qb = nullptr;  // per-query budgets (device) when the current search uses them, else nullptr
@@ -360,6 +361,7 @@ struct alp_s {
     for (auto *b : {&d_opts, &d_pfeas}) b->release();
     g_ws.release();
     g_dbg.release();
+    g_lv.release();
     d_punits.release();
     // stream-ordered release: after the last work on the handle's stream and on the last caller
     // stream (alp_search_shard may run on a caller's stream), without a host synchronisation
@@ -1692,6 +1694,74 @@ alp_status alp_search_peer(alp_t *h, const double *targets, int32_t n, int64_t b
   return s;
 }
 
+// One target, n budgets: the one-pass budget-indexed search (alp_levels.cu) — every candidate with
+// units <= the largest budget evaluated once (instead of one exhaustive pass per budget), then K3
+// per budget.  Returns ALP_EINTERNAL + no error message when the plan does not allow it (the caller
+// falls back to the per-query passes): non-default rows per lane, coarse segments, > 4096 distinct
+// budgets or a largest budget above 16384 units.
+static alp_status budget_sweep(alp_s *h, double target, const int64_t *budgets, int n, alp_result *out, bool *done) {
+  *done = false;
+  static const bool off = getenv("ALP_NO_LEVELS") != nullptr;  // A/B switch: per-query passes
+  if (off || h->from_terms || h->rows_per_lane != 12 || n < 2 ||
+      (uint64_t)h->n_chunks * h->L * (uint64_t)h->Ka >= 0xffffffffull)
+    return ALP_OK;
+  std::vector<int> lv;
+  for (int i = 0; i < n; ++i) {
+    if (budgets[i] < 0) return fail(ALP_EINVAL, "budgets[%d] < 0", i);
+    lv.push_back((int)std::min<int64_t>(budgets[i], h->umax_total));
+  }
+  std::sort(lv.begin(), lv.end());
+  lv.erase(std::unique(lv.begin(), lv.end()), lv.end());
+  const int L = (int)lv.size(), bmax = lv.back();
+  if (L > 4096 || bmax > 16384) return ALP_OK;
+  std::vector<int> ql(n);
+  for (int i = 0; i < n; ++i)
+    ql[i] = (int)(std::lower_bound(lv.begin(), lv.end(), (int)std::min<int64_t>(budgets[i], h->umax_total)) - lv.begin());
+  std::vector<double> tg(n, target);
+  cudaStream_t st = h->stream;
+  alp_status s = use_stream(h, st);
+  if (s != ALP_OK) return s;
+  CU(cudaEventRecord(h->evs0, st));
+  s = ensure_scratch(h, n, st);
+  if (s != ALP_OK) return s;
+  h->s_qb = nullptr;
+  s = option_tables(h, tg.data(), n, st, h->sc.keys, h->sc.counts);  // K1: the terms of every query (= target)
+  if (s != ALP_OK) return s;
+  Geometry g;
+  s = make_geometry(h, 1, bmax, 0, 0, g);
+  if (s != ALP_OK) return s;
+  const uint64_t items = (uint64_t)h->n_chunks * h->n_groups * h->nQ;
+  g.a.item_lo = 0;
+  g.a.item_hi = items;
+  g.a.tau = h->sc.tau;
+  // scratch: level keys [L], ticket, histograms 2 x [bmax + 1], levels [L], query levels [n]
+  const size_t nb = 8 * (size_t)L + 8 + 16 * (size_t)(bmax + 1) + 4 * (size_t)L + 4 * (size_t)n + 64;
+  CU(h->g_lv.ensure(nb));
+  unsigned char *p = h->g_lv.p;
+  auto take = [&](size_t bytes) {
+    unsigned char *r = p;
+    p += (bytes + 7) & ~size_t(7);
+    return r;
+  };
+  auto *lkeys = reinterpret_cast<unsigned long long *>(take(8 * (size_t)L));
+  auto *ticket = reinterpret_cast<unsigned long long *>(take(8));
+  auto *h0 = reinterpret_cast<unsigned long long *>(take(8 * (size_t)(bmax + 1)));
+  auto *h1 = reinterpret_cast<unsigned long long *>(take(8 * (size_t)(bmax + 1)));
+  auto *d_lv = reinterpret_cast<int *>(take(4 * (size_t)L));
+  auto *d_ql = reinterpret_cast<int *>(take(4 * (size_t)n));
+  CU(cudaMemcpyAsync(d_lv, lv.data(), 4 * (size_t)L, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_ql, ql.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  CU(cudaEventRecord(h->ev0, st));
+  CU(launch_levels(g.a, d_lv, L, bmax, lkeys, ticket, d_ql, n, h->sc.keys, h->sc.counts, h0, h1, h->sm_count, st));
+  CU(cudaEventRecord(h->ev1, st));
+  h->ev_pending = true;
+  h->last_ur = false;
+  s = finalize_impl(h, tg.data(), budgets, n, 0, h->sc.keys, h->sc.counts, st, out);
+  h->last_launches = 4;  // K1, search, finish, K3
+  if (s == ALP_OK || s == ALP_EINFEASIBLE) *done = true;
+  return s;
+}
+
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
                                  int64_t budget_units, alp_result *out) {
   NvtxRange nv("alp_search");
@@ -1702,6 +1772,15 @@ static alp_status search_queries(alp_t *h, const double *targets, const int64_t 
   CU(cudaSetDevice(h->device));
   s = ensure_scratch(h, n, h->stream);
   if (s != ALP_OK) return s;
+  if (budgets && n >= 2) {  // one target, several budgets: the one-pass budget-indexed search
+    bool same = true;
+    for (int i = 1; i < n; ++i) same &= targets[i] == targets[0];
+    if (same) {
+      bool done = false;
+      s = budget_sweep(h, targets[0], budgets, n, out, &done);
+      if (done || (s != ALP_OK && s != ALP_EINFEASIBLE)) return s;
+    }
+  }
   const uint64_t items = alp_num_items(h, budget_units);
   const int ug = budgets ? 0 : ur_batch_group(h, budget_units);
   if (n > kInlineTargets && ug > 0) {

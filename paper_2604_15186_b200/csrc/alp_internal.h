@@ -239,6 +239,12 @@ size_t uprep_smem_bytes(const SearchArgs &a);  // k_uprep dynamic shared memory 
 constexpr size_t kUPrepSmemMax = 200 * 1024;
 constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
+// One-pass budget-indexed search (alp_levels.cu): per-level best keys over the candidates with
+// units <= bmax, then per-query keys (prefix minimum over levels) and exact counts.
+cudaError_t launch_levels(const SearchArgs &s, const int *d_levels, int L, int bmax, unsigned long long *lvl_keys,
+                          unsigned long long *ticket, const int *d_q_level, int n, unsigned long long *keys,
+                          unsigned long long *counts, unsigned long long *h0, unsigned long long *h1, int sm_count,
+                          cudaStream_t st);
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st);
 int search_max_blocks_per_sm(const SearchArgs &a);
 cudaError_t launch_egalitarian(const double *lat, int W, int G, long long *best_idx, double *best_min,
