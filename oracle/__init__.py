@@ -264,3 +264,34 @@ def lambda_star(I: Instance, budget: int | None = None) -> float:
         if tot is not None and tot <= B:
             return float(v)
     return 0.0
+
+
+def floor_ok(I: Instance, m: int, k: int) -> bool:
+    """Memory floor of option k of LLM m: share units >= min_units[m][tp index]."""
+    if I.min_units is None:
+        return True
+    nT, nR = len(I.T), len(I.R)
+    return int(I.S[k // (nT * nR)]) >= int(np.asarray(I.min_units).reshape(I.M, nT)[m][(k // nR) % nT])
+
+
+def max_throughput(I: Instance, budget: int | None = None):
+    """SPEC.md:374 "no feasible candidate -> returns the candidate with maximal T_w": by its plain
+    definition, a brute force over every candidate within the budget whose options clear their
+    memory floors, T_w = min_m b_m (Eq. 2, FP64; the Eq. 2 terms do not depend on the target),
+    the lowest canonical index among equal T_w.  Small instances only (pure-Python loop).
+    Returns None when no candidate fits the budget, else dict(index, throughput, units)."""
+    import itertools
+    B = I.budget if budget is None else budget
+    tab = option_table(I, 1.0)
+    ok = [[floor_ok(I, m, k) for k in range(I.K)] for m in range(I.M)]
+    best = None
+    for idx, ks in enumerate(itertools.product(range(I.K), repeat=I.M)):  # canonical order, LLM 0 first
+        if not all(ok[m][k] for m, k in enumerate(ks)):
+            continue
+        units = sum(int(tab["u"][m][k]) for m, k in enumerate(ks))
+        if units > B:
+            continue
+        tw = min(float(tab["b"][m][k]) for m, k in enumerate(ks))
+        if best is None or tw > best["throughput"]:
+            best = {"index": idx, "throughput": tw, "units": units}
+    return best

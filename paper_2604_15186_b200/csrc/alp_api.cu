@@ -296,7 +296,7 @@ struct alp_s {
   // the smallest tile sum of a mixed group (all its lanes are over budget when that one is)
   std::vector<int> gsum;
   uint32_t n_groups_u = 0;
-  std::vector<uint32_t> tile_e, tile_off;
+  std::vector<uint32_t> tile_e;
   int rows_per_lane = 8;
   int nq_force = 0;    // ALP_NQ: a-ranges per row (tuning), 0 = automatic
   int min_blocks = 0;  // 0: per rows-per-lane default (T = 8: 3 blocks/SM, T = 16: 2); ALP_BLOCKS_PER_SM overrides
@@ -416,88 +416,77 @@ alp_status make_plan(alp_s *h) {
   // sort list: entries of the sort group ordered by unit sum (stable in canonical order), padded
   // so every lane tile holds T entries of one unit sum.
   // unit sum of every entry, built digit by digit (entry e = sum_j d_j K^(ng-1-j))
+  // (odometer over the ng digits, last digit fastest: no divisions)
   std::vector<int> sum(L, 0);
-  for (int j = 0; j < ng; ++j) {
-    uint32_t stride = 1;
-    for (int q = j + 1; q < ng; ++q) stride *= (uint32_t)K;
-    for (uint32_t e = 0; e < L; ++e) sum[e] += U(h->g0 + j, (int)((e / stride) % (uint32_t)K));
+  {
+    int dg[4] = {0, 0, 0, 0}, cur = 0;
+    for (int j = 0; j < ng; ++j) cur += U(h->g0 + j, 0);
+    for (uint32_t e = 0; e < L; ++e) {
+      sum[e] = cur;
+      for (int j = ng - 1; j >= 0; --j) {
+        cur -= U(h->g0 + j, dg[j]);
+        if (++dg[j] < K) {
+          cur += U(h->g0 + j, dg[j]);
+          break;
+        }
+        dg[j] = 0;
+        cur += U(h->g0 + j, 0);
+      }
+    }
   }
   int smax = 0;
   for (uint32_t e = 0; e < L; ++e) smax = std::max(smax, sum[e]);
-  // stable counting sort by unit sum
-  std::vector<uint32_t> start(smax + 2, 0), order(L);
-  for (uint32_t e = 0; e < L; ++e) ++start[sum[e] + 1];
-  for (int s = 0; s <= smax; ++s) start[s + 1] += start[s];
-  for (uint32_t e = 0; e < L; ++e) order[start[sum[e]]++] = e;
-  h->tile_s.clear();
-  h->tile_e.clear();
+  // stable counting sort by unit sum, written straight into the final tile layout: per sum s its
+  // entries fill ceil(c_s / T) lane tiles (T rows, the last one padded with kDummy rows); the first
+  // whole multiple of 32 of them go to the uniform warp groups (all sums in order), the leftover
+  // tiles of every sum after them (mixed groups), padded to a multiple of 32 tiles
   const int T = h->rows_per_lane;
-  for (size_t i = 0; i < order.size();) {
-    const int s = sum[order[i]];
-    h->tile_s.push_back(s);
-    for (int r = 0; r < T; ++r) {
-      if (i < order.size() && sum[order[i]] == s) {
-        h->tile_e.push_back(order[i]);  // canonical within-group index (LLM g0 most significant)
-        ++i;
-      } else {
-        h->tile_e.push_back(kDummy);
-      }
+  std::vector<uint32_t> cnt(smax + 1, 0);
+  for (uint32_t e = 0; e < L; ++e) ++cnt[sum[e]];
+  std::vector<uint64_t> full(smax + 1), uoff(smax + 1), roff(smax + 1);
+  uint64_t nfull = 0, nrest = 0;
+  for (int v = 0; v <= smax; ++v) {
+    const uint64_t tiles = (cnt[v] + T - 1) / T;
+    full[v] = tiles / kWarpTiles * kWarpTiles;
+    uoff[v] = nfull;
+    nfull += full[v];
+  }
+  for (int v = 0; v <= smax; ++v) {
+    const uint64_t tiles = (cnt[v] + T - 1) / T;
+    roff[v] = nfull + nrest;
+    nrest += tiles - full[v];
+  }
+  const uint64_t ntiles = (nfull + nrest + kWarpTiles - 1) / kWarpTiles * kWarpTiles;
+  h->tile_s.assign(ntiles, 0);
+  h->tile_e.assign(ntiles * T, kDummy);
+  // per sum: its next slot (tile, row) — no divisions in the pass over the entries
+  std::vector<uint64_t> nt(smax + 1), ntile(smax + 1);
+  std::vector<int> nrow(smax + 1, 0);
+  for (int v = 0; v <= smax; ++v) {
+    nt[v] = 0;
+    ntile[v] = full[v] > 0 ? uoff[v] : roff[v];
+  }
+  uint32_t *te = h->tile_e.data();
+  int *tsum = h->tile_s.data();
+  for (uint32_t e = 0; e < L; ++e) {
+    const int v = sum[e];
+    const uint64_t tile = ntile[v];
+    te[tile * T + nrow[v]] = e;  // canonical within-group index (LLM g0 most significant)
+    tsum[tile] = v;
+    if (++nrow[v] == T) {
+      nrow[v] = 0;
+      ++nt[v];
+      ntile[v] = nt[v] < full[v] ? uoff[v] + nt[v] : roff[v] + (nt[v] - full[v]);
     }
   }
-  // warp groups of 32 lane tiles: first every group whose 32 tiles share one unit sum (a
-  // warp-uniform remaining budget), then the leftover tiles of all sums (mixed groups), padded
-  {
-    const size_t nt = h->tile_s.size();
-    std::vector<int> ts;
-    std::vector<uint32_t> te;
-    std::vector<size_t> rest;
-    ts.reserve(nt + kWarpTiles);
-    te.reserve((nt + kWarpTiles) * T);
-    h->gsum.clear();
-    for (size_t i = 0; i < nt;) {
-      size_t j = i;
-      while (j < nt && h->tile_s[j] == h->tile_s[i]) ++j;  // tiles of one sum are consecutive
-      const size_t full = (j - i) / kWarpTiles * kWarpTiles;
-      for (size_t k = i; k < i + full; ++k) {
-        ts.push_back(h->tile_s[k]);
-        te.insert(te.end(), h->tile_e.begin() + k * T, h->tile_e.begin() + (k + 1) * T);
-      }
-      for (size_t g = 0; g < full / kWarpTiles; ++g) h->gsum.push_back(h->tile_s[i]);
-      for (size_t k = i + full; k < j; ++k) rest.push_back(k);
-      i = j;
-    }
-    h->n_groups_u = (uint32_t)h->gsum.size();
-    for (size_t k : rest) {
-      ts.push_back(h->tile_s[k]);
-      te.insert(te.end(), h->tile_e.begin() + k * T, h->tile_e.begin() + (k + 1) * T);
-    }
-    while (ts.size() % kWarpTiles) {
-      ts.push_back(ts.back());
-      for (int r = 0; r < T; ++r) te.push_back(kDummy);
-    }
-    for (size_t g = h->n_groups_u * (size_t)kWarpTiles; g < ts.size(); g += kWarpTiles)
-      h->gsum.push_back(*std::min_element(ts.begin() + g, ts.begin() + g + kWarpTiles));
-    h->tile_s.swap(ts);
-    h->tile_e.swap(te);
-  }
+  for (uint64_t t = nfull + nrest; t < ntiles; ++t) h->tile_s[t] = h->tile_s[nfull + nrest - 1];  // padding tiles
+  h->n_groups_u = (uint32_t)(nfull / kWarpTiles);
+  h->gsum.resize(ntiles / kWarpTiles);
+  for (uint64_t g = 0; g < ntiles / kWarpTiles; ++g)  // uniform: the group's sum; mixed: its smallest tile sum
+    h->gsum[g] = *std::min_element(h->tile_s.begin() + g * kWarpTiles, h->tile_s.begin() + (g + 1) * kWarpTiles);
   h->n_groups = (uint32_t)(h->tile_s.size() / kWarpTiles);
-  // smem byte offsets of each row's sort-group terms (tau of LLM g0+j lives at ((g0+j)*K + d)*4;
-  // slot g1*K holds 0.0f for unused digits, slot g1*K+1 holds +inf for padded rows)
-  const uint32_t zero_off = (uint32_t)(h->g1 * K) * 4u, inf_off = zero_off + 4u;
-  h->tile_off.assign(h->tile_e.size() * 4, 0u);
-  for (size_t i = 0; i < h->tile_e.size(); ++i) {
-    uint32_t off[4] = {zero_off, zero_off, zero_off, zero_off};
-    if (h->tile_e[i] == kDummy) {
-      off[0] = inf_off;
-    } else {
-      uint32_t rem = h->tile_e[i];
-      for (int j = ng - 1; j >= 0; --j) {
-        off[j] = (uint32_t)((h->g0 + j) * K + (int)(rem % (uint32_t)K)) * 4u;
-        rem /= (uint32_t)K;
-      }
-    }
-    for (int j = 0; j < 4; ++j) h->tile_off[4 * i + j] = off[j];
-  }
+  // (the four shared-memory byte offsets of each row's sort-group terms, tile_off, are expanded from
+  // tile_e on the device after the upload: launch_plan_offsets)
   // b columns sorted by units (stable): the feasible set for a remaining budget is a prefix.
   h->bperm.resize(K);
   std::iota(h->bperm.begin(), h->bperm.end(), 0);
@@ -566,6 +555,7 @@ alp_status make_plan(alp_s *h);
 
 // Build (or fetch from the process-wide cache) the static plan and its device tables.
 alp_status get_plan(alp_s *h) {
+  Trace tr;
   const std::string key = plan_key(h);
   std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.find(key);
@@ -582,13 +572,17 @@ alp_status get_plan(alp_s *h) {
     A.add(h->u, &P->d_u);
     A.add(h->tile_s, &P->d_tile_s);
     A.add(h->tile_e, &P->d_tile_e);
-    A.add(h->tile_off, &P->d_tile_off);
     A.add(h->bperm, &P->d_bperm);
     A.add(h->dv, &P->d_dv);
     A.add(h->dcnt, &P->d_dcnt);
     A.add(h->gsum, &P->d_gsum);
+    A.scratch(h->tile_e.size() * 4, &P->d_tile_off);  // not uploaded: expanded on the device
+    tr.mark("make_plan");
     CU(A.commit(&P->dev->mem, h->h2d, h->stream));
+    tr.mark("plan upload");
+    CU(launch_plan_offsets(P->d_tile_e, h->tile_e.size(), h->g0, h->g1, h->ng, h->K, P->d_tile_off, h->stream));
     CU(cudaStreamSynchronize(h->stream));  // shared by handles on other streams (cold path only)
+    tr.mark("plan sync");
     P->N = h->N; P->a_llm = h->a_llm; P->b_llm = h->b_llm; P->Ka = h->Ka; P->Kb = h->Kb; P->g0 = h->g0;
     P->g1 = h->g1; P->ng = h->ng; P->umax_a = h->umax_a; P->umax_b = h->umax_b;
     P->L = h->L; P->n_chunks = h->n_chunks; P->n_groups = h->n_groups; P->nQ = h->nQ; P->A = h->A;
@@ -599,7 +593,7 @@ alp_status get_plan(alp_s *h) {
     P->gsum = h->gsum;
     P->n_groups_u = h->n_groups_u;
     g_plans[key] = P;
-    h->tile_s.clear(); h->tile_e.clear(); h->tile_off.clear(); h->bperm.clear(); h->bu.clear();
+    h->tile_s.clear(); h->tile_e.clear(); h->bperm.clear(); h->bu.clear();
   }
   h->N = P->N; h->a_llm = P->a_llm; h->b_llm = P->b_llm; h->Ka = P->Ka; h->Kb = P->Kb; h->g0 = P->g0;
   h->g1 = P->g1; h->ng = P->ng; h->umax_a = P->umax_a; h->umax_b = P->umax_b;

@@ -239,6 +239,10 @@ size_t uprep_smem_bytes(const SearchArgs &a);  // k_uprep dynamic shared memory 
 constexpr size_t kUPrepSmemMax = 200 * 1024;
 constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
+// Static plan: tile_off[4 * row] (shared-memory byte offsets of the row's sort-group terms) from
+// tile_e (canonical within-group index or kDummy) on the device.
+cudaError_t launch_plan_offsets(const uint32_t *tile_e, size_t rows, int g0, int g1, int ng, int K, uint32_t *tile_off,
+                                cudaStream_t st);
 // One-pass budget-indexed search (alp_levels.cu): per-level best keys over the candidates with
 // units <= bmax, then per-query keys (prefix minimum over levels) and exact counts.
 cudaError_t launch_levels(const SearchArgs &s, const int *d_levels, int L, int bmax, unsigned long long *lvl_keys,

@@ -61,6 +61,35 @@ __global__ void k_option_table(const __grid_constant__ OptionArgs A) {
   if (t == 0) A.u[mk] = u;
 }
 
+// tau of LLM g0+j, option d lives at ((g0+j)*K + d)*4 in the search kernels' shared memory; slot
+// g1*K holds 0.0f (unused digit), slot g1*K+1 holds +inf (padded row): four offsets per row, the
+// row's sort-group digits most significant first.
+__global__ void k_plan_offsets(const uint32_t *tile_e, size_t rows, int g0, int g1, int ng, int K, uint4 *tile_off) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const uint32_t zero_off = (uint32_t)(g1 * K) * 4u, inf_off = zero_off + 4u;
+  uint32_t off[4] = {zero_off, zero_off, zero_off, zero_off};
+  const uint32_t e = tile_e[i];
+  if (e == kDummy) {
+    off[0] = inf_off;
+  } else {
+    uint32_t rem = e;
+    for (int j = ng - 1; j >= 0; --j) {
+      off[j] = (uint32_t)((g0 + j) * K + (int)(rem % (uint32_t)K)) * 4u;
+      rem /= (uint32_t)K;
+    }
+  }
+  tile_off[i] = make_uint4(off[0], off[1], off[2], off[3]);
+}
+
+cudaError_t launch_plan_offsets(const uint32_t *tile_e, size_t rows, int g0, int g1, int ng, int K, uint32_t *tile_off,
+                                cudaStream_t st) {
+  if (!rows) return cudaSuccess;
+  k_plan_offsets<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(tile_e, rows, g0, g1, ng, K,
+                                                                 reinterpret_cast<uint4 *>(tile_off));
+  return cudaGetLastError();
+}
+
 __global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
                             int n_work, unsigned long long *fbest, unsigned *fdone) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -571,3 +571,68 @@ def test_egalitarian_identical_workflows_split_evenly():
     u = lat[8] / lat[4]
     assert mn == u and sm == u + u
     assert all(a >= b for a, b in zip(lat, lat[1:]))  # more GPUs never hurt (budget monotone)
+
+
+# ----------------------------------------------------------------------------- max-throughput fallback
+def test_max_throughput_hand_case():
+    """SPEC.md:374 fallback on the App. A hand case, derived by hand: Eq. 2 terms d*f*T/n are
+    {1, 2, 1.75, 3.5, 2, 4, 3.5, 7} for both LLMs (options k = (s*2 + tp)*2 + d), units
+    {1, 2, 2, 4, 2, 4, 4, 8}.  B = 8: T_w = 4 needs option 5 (4 units) for both LLMs (7 would need
+    16 units) -> index 5*8 + 5 = 45, the App. A row lambda = 4 (lambda = 5 infeasible).  B = 7:
+    T_w = 3.5 needs 8 units, T_w = 2 needs 2 + 2 -> index 1*8 + 1 = 9.  B = 3: only T_w = 1
+    (1 + 1 units) -> index 0.  B = 1: two LLMs need 2 units -> none."""
+    I = oracle.from_json(generate.load("hand"))
+    assert oracle.max_throughput(I, 8) == {"index": 45, "throughput": 4.0, "units": 8}
+    assert oracle.max_throughput(I, 7) == {"index": 9, "throughput": 2.0, "units": 4}
+    assert oracle.max_throughput(I, 3) == {"index": 0, "throughput": 1.0, "units": 2}
+    assert oracle.max_throughput(I, 1) is None
+
+
+@pytest.mark.parametrize("name", ["hand", "C1", "C2"])
+def test_max_throughput_equals_lambda_star(name):
+    """The largest T_w within the budget bounds lambda*, the largest target at which some candidate
+    is feasible (oracle.lambda_star, the full R4 test of the C oracle at lambda = v), from above: a
+    candidate feasible at lambda has every b_m >= lambda.  At the configs' budgets they are equal;
+    at B = 3 on C1/C2 the max-T_w candidate has b = lambda exactly but x = ((lambda*n)/d)/f lands one
+    ulp above T, so R4 rejects it at lambda = T_w (reading R17: the fallback maximises Eq. 2 alone)."""
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    for B in (d["budget_units"], d["budget_units"] // 2, 3):
+        r = oracle.max_throughput(I, B)
+        ls = oracle.lambda_star(I, B)
+        assert (r is None and ls == 0.0) or ls <= r["throughput"], (name, B)
+        if B != 3:
+            assert r["throughput"] == ls, (name, B)
+
+
+def test_max_throughput_separable_closed_form():
+    """Against the separable construction (max-min over independent per-LLM choices): theta* = max
+    over Eq. 2 values v with sum_m min{u : b >= v, floor ok} <= B; lowest index by digits, each the
+    smallest option whose completion still fits — on random instances with memory floors."""
+    for seed in range(12):
+        d = generate.random_instance(500 + seed, M=3, F=4, S=[1, 2, 4], T=[1, 2], R=[1, 2], budget=14,
+                                     min_units=bool(seed % 2))
+        I = oracle.from_json(d)
+        tab = oracle.option_table(I, 1.0)
+        ok = [[oracle.floor_ok(I, m, k) for k in range(I.K)] for m in range(I.M)]
+        for B in (2, 5, 9, 14, 40):
+            def minu(m, v):
+                c = [int(tab["u"][m][k]) for k in range(I.K) if ok[m][k] and tab["b"][m][k] >= v]
+                return min(c) if c else None
+            best = None
+            for v in sorted(set(tab["b"].ravel().tolist())):
+                mus = [minu(m, v) for m in range(I.M)]
+                if all(x is not None for x in mus) and sum(mus) <= B:
+                    best = v
+            r = oracle.max_throughput(I, B)
+            if best is None:
+                assert r is None
+                continue
+            idx, used = 0, 0
+            for m in range(I.M):
+                rest = sum(minu(j, best) for j in range(m + 1, I.M))
+                k = next(k for k in range(I.K) if ok[m][k] and tab["b"][m][k] >= best
+                         and used + int(tab["u"][m][k]) + rest <= B)
+                used += int(tab["u"][m][k])
+                idx = idx * I.K + k
+            assert r == {"index": idx, "throughput": best, "units": used}, (seed, B)
