@@ -99,6 +99,12 @@ typedef struct {
   uint64_t feasible_count;      /* number of feasible candidates (R10) */
   uint64_t candidates;          /* candidates evaluated = N (exhaustive) */
   int32_t share_units[ALP_MAX_M], tp[ALP_MAX_M], replicas[ALP_MAX_M]; /* winner, per LLM */
+  /* 1 when found = 0 but some candidate fits the budget: index, share_units / tp / replicas, units
+   * and throughput then describe the candidate with the maximal Eq. 2 T_w among those within the
+   * budget whose options clear their memory floors (lowest canonical index on ties; SPEC.md:374
+   * "no feasible candidate -> returns the candidate with maximal T_w flagged INFEASIBLE-rate");
+   * latency stays +inf.  0 otherwise. */
+  int32_t fallback;
 } alp_result;
 
 /* Validate, copy and plan.  Uploads the profile tables and the static search plan to the

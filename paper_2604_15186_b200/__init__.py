@@ -47,7 +47,7 @@ class _Result(ctypes.Structure):
                 ("latency_key", ctypes.c_float), ("latency", ctypes.c_double), ("throughput", ctypes.c_double),
                 ("units", ctypes.c_int64), ("feasible_count", ctypes.c_uint64), ("candidates", ctypes.c_uint64),
                 ("share_units", ctypes.c_int32 * MAX_M), ("tp", ctypes.c_int32 * MAX_M),
-                ("replicas", ctypes.c_int32 * MAX_M)]
+                ("replicas", ctypes.c_int32 * MAX_M), ("fallback", ctypes.c_int32)]
 
 
 EXPORTS = ["alp_build", "alp_build_from_terms", "alp_destroy", "alp_num_candidates", "alp_h2d_bytes", "alp_decode",
@@ -209,13 +209,17 @@ class Result:
     share_units: list = field(default_factory=list)
     tp: list = field(default_factory=list)
     replicas: list = field(default_factory=list)
+    # found = False but fallback = True: index / share_units / tp / replicas / units / throughput are
+    # the candidate with the maximal Eq. 2 T_w within the budget ("INFEASIBLE-rate")
+    fallback: bool = False
 
     @staticmethod
     def _from(r: _Result) -> "Result":
         M = r.M
-        return Result(bool(r.found), int(r.index) if r.found else -1, float(np.float32(r.latency_key)), r.latency,
+        shown = r.found or r.fallback
+        return Result(bool(r.found), int(r.index) if shown else -1, float(np.float32(r.latency_key)), r.latency,
                       r.throughput, int(r.units), int(r.feasible_count), int(r.candidates),
-                      list(r.share_units[:M]), list(r.tp[:M]), list(r.replicas[:M]))
+                      list(r.share_units[:M]), list(r.tp[:M]), list(r.replicas[:M]), bool(r.fallback))
 
 
 def _arr(x, dt):

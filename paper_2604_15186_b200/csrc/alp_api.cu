@@ -1570,6 +1570,40 @@ size_t alp_workspace_bytes(const alp_t *h, int32_t n_targets) {
   return ws_layout(h, n_targets, nullptr, nullptr);
 }
 
+// every result of the call that found nothing gets the candidate with the maximal
+// Eq. 2 T_w within its budget (k_max_throughput on the call's option table; once per budget).
+static alp_status apply_fallbacks(alp_s *h, int n, const int64_t *budgets, int64_t budget, alp_result *out,
+                                  cudaStream_t st, alp_status s) {
+  if (s != ALP_OK && s != ALP_EINFEASIBLE) return s;
+  if (h->from_terms) return s;
+  std::map<long long, alp_result> memo;
+  for (int i = 0; i < n; ++i) {
+    if (out[i].found) continue;
+    const long long B = budgets ? budgets[i] : budget;
+    auto it = memo.find(B);
+    if (it == memo.end()) {
+      alp_result *host = nullptr, *dres = zero_copy_out(1, &host);
+      if (!dres) return fail(ALP_ECUDA, "no mapped pinned memory for the fallback result");
+      CU(launch_max_throughput(h->sc.b, h->d_u, h->dprof(), B, h->N, dres, st));
+      CU(cudaStreamSynchronize(st));
+      it = memo.emplace(B, *host).first;
+    }
+    const alp_result &f = it->second;
+    out[i].fallback = f.fallback;
+    if (f.fallback) {
+      out[i].index = f.index;
+      out[i].units = f.units;
+      out[i].throughput = f.throughput;
+      for (int m = 0; m < ALP_MAX_M; ++m) {
+        out[i].share_units[m] = f.share_units[m];
+        out[i].tp[m] = f.tp[m];
+        out[i].replicas[m] = f.replicas[m];
+      }
+    }
+  }
+  return s;
+}
+
 alp_status alp_search_shard(alp_t *h, const double *targets, int32_t n, int64_t budget_units, uint64_t lo,
                             uint64_t hi, void *d_workspace, void *stream, int64_t *d_keys, int64_t *d_counts) {
   NvtxRange nv("alp_search_shard");
@@ -1587,9 +1621,10 @@ alp_status alp_finalize(alp_t *h, const double *targets, int32_t n, int64_t budg
   if (!d_keys || !d_counts) return fail(ALP_EINVAL, "d_keys/d_counts is NULL");
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
-  return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
-                       reinterpret_cast<const unsigned long long *>(d_counts),
-                       stream ? (cudaStream_t)stream : h->stream, out, 0, d_workspace);
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  s = finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_keys),
+                    reinterpret_cast<const unsigned long long *>(d_counts), st, out, 0, d_workspace);
+  return apply_fallbacks(h, n, nullptr, budget_units, out, st, s);
 }
 
 alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int64_t budget_units,
@@ -1601,8 +1636,10 @@ alp_status alp_finalize_gathered(alp_t *h, const double *targets, int32_t n, int
   if (world < 1) return fail(ALP_EINVAL, "world must be >= 1");
   alp_status s = check_targets(targets, n);
   if (s != ALP_OK) return s;
-  return finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_gathered),
-                       nullptr, stream ? (cudaStream_t)stream : h->stream, out, world, d_workspace);
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  s = finalize_impl(h, targets, nullptr, n, budget_units, reinterpret_cast<const unsigned long long *>(d_gathered),
+                    nullptr, st, out, world, d_workspace);
+  return apply_fallbacks(h, n, nullptr, budget_units, out, st, s);
 }
 
 size_t alp_peer_bytes(int32_t n_targets, int32_t world) {
@@ -1685,7 +1722,7 @@ alp_status alp_search_peer(alp_t *h, const double *targets, int32_t n, int64_t b
   s = collect_results(h, n, st, out, hzc);
   for (int t = 0; t < n; ++t)
     if (out[t].found < 0) return fail(ALP_EINTERNAL, "peer exchange timed out (rank %d of %d)", rank, world);
-  return s;
+  return apply_fallbacks(h, n, nullptr, budget_units, out, st, s);
 }
 
 // One target, n budgets: the one-pass budget-indexed search (alp_levels.cu) — every candidate with
@@ -1756,8 +1793,18 @@ static alp_status budget_sweep(alp_s *h, double target, const int64_t *budgets, 
   return s;
 }
 
+static alp_status search_queries_core(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
+                                      int64_t budget_units, alp_result *out);
+
 static alp_status search_queries(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
                                  int64_t budget_units, alp_result *out) {
+  alp_status s = search_queries_core(h, targets, budgets, n, budget_units, out);
+  if (s != ALP_OK && s != ALP_EINFEASIBLE) return s;
+  return apply_fallbacks(h, n, budgets, budget_units, out, h->stream, s);
+}
+
+static alp_status search_queries_core(alp_t *h, const double *targets, const int64_t *budgets, int32_t n,
+                                      int64_t budget_units, alp_result *out) {
   NvtxRange nv("alp_search");
   if (!h) return fail(ALP_EINVAL, "handle is NULL");
   if (!out) return fail(ALP_EINVAL, "out is NULL");

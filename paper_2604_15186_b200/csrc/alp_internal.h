@@ -239,6 +239,9 @@ size_t uprep_smem_bytes(const SearchArgs &a);  // k_uprep dynamic shared memory 
 constexpr size_t kUPrepSmemMax = 200 * 1024;
 constexpr int kUBytes = 60 * 1024;      // constant-bank table space of the uniform-register path
 cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st);
+// SPEC.md:374 fallback: the max-T_w candidate within budget B into *out (device or mapped memory).
+cudaError_t launch_max_throughput(const double *b, const int *u, const DevProfiles &pr, long long B, uint64_t N,
+                                  alp_result *out, cudaStream_t st);
 // Static plan: tile_off[4 * row] (shared-memory byte offsets of the row's sort-group terms) from
 // tile_e (canonical within-group index or kDummy) on the device.
 cudaError_t launch_plan_offsets(const uint32_t *tile_e, size_t rows, int g0, int g1, int ng, int K, uint32_t *tile_off,

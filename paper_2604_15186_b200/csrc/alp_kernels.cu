@@ -90,6 +90,85 @@ cudaError_t launch_plan_offsets(const uint32_t *tile_e, size_t rows, int g0, int
   return cudaGetLastError();
 }
 
+// SPEC.md:374 fallback (no candidate meets the target): the candidate with the maximal Eq. 2
+// T_w = min_m b_m among those within the budget whose options clear their memory floors, lowest
+// canonical index on ties.  The Eq. 2 terms b (FP64, from the option table of the search) do not
+// depend on the target.  One block: every thread tests thresholds theta = b of one option (a
+// candidate with T_w >= theta exists iff sum_m min{u : b >= theta, floor ok} <= B; the answer is
+// the largest such theta, an atomicMax on the bits of the positive double), then thread 0 picks
+// the digits from LLM 0 on, each the smallest option whose completion still fits.
+__global__ void k_max_throughput(const double *b, const int *u, DevProfiles pr, long long B, uint64_t N,
+                                 alp_result *out) {
+  const int M = pr.M, K = pr.K, MK = M * K;
+  __shared__ unsigned long long s_theta;
+  __shared__ int s_minu[ALP_MAX_M];
+  auto ok = [&](int m, int k) {
+    if (!pr.min_units) return true;
+    const int si = k / (pr.nT * pr.nR), ti = (k / pr.nR) % pr.nT;
+    return pr.S[si] >= pr.min_units[m * pr.nT + ti];
+  };
+  auto minu = [&](int m, double th) {
+    int mn = 0x7fffffff;
+    for (int k = 0; k < K; ++k)
+      if (ok(m, k) && b[m * K + k] >= th) mn = min(mn, u[m * K + k]);
+    return mn;
+  };
+  if (threadIdx.x == 0) s_theta = 0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < MK; i += blockDim.x) {
+    if (!ok(i / K, i % K)) continue;
+    const double th = b[i];
+    long long tot = 0;
+    for (int m = 0; m < M && tot <= B; ++m) {
+      const int mn = minu(m, th);
+      tot = (mn == 0x7fffffff) ? B + 1 : tot + mn;
+    }
+    if (tot <= B) atomicMax(&s_theta, (unsigned long long)__double_as_longlong(th));
+  }
+  __syncthreads();
+  const double th = __longlong_as_double((long long)s_theta);
+  const bool any = s_theta != 0ull;
+  if (any && (int)threadIdx.x < M) s_minu[threadIdx.x] = minu(threadIdx.x, th);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  alp_result r;
+  memset(&r, 0, sizeof(r));
+  r.M = M;
+  r.candidates = N;
+  r.index = ~0ull;
+  r.latency = CUDART_INF;
+  r.latency_key = __int_as_float(0x7f800000);
+  if (any) {
+    long long used = 0, rest = 0;
+    for (int m = 0; m < M; ++m) rest += s_minu[m];
+    unsigned long long idx = 0;
+    double tw = CUDART_INF;
+    for (int m = 0; m < M; ++m) {
+      rest -= s_minu[m];
+      int kk = -1;
+      for (int k = 0; k < K && kk < 0; ++k)
+        if (ok(m, k) && b[m * K + k] >= th && used + u[m * K + k] + rest <= B) kk = k;
+      used += u[m * K + kk];
+      idx = idx * (unsigned long long)K + (unsigned long long)kk;
+      tw = b[m * K + kk] < tw ? b[m * K + kk] : tw;
+      r.share_units[m] = pr.S[kk / (pr.nT * pr.nR)];
+      r.tp[m] = pr.T[(kk / pr.nR) % pr.nT];
+      r.replicas[m] = pr.R[kk % pr.nR];
+    }
+    r.index = idx;
+    r.units = used;
+    r.throughput = tw;
+    r.fallback = 1;
+  }
+  *out = r;
+}
+
+cudaError_t launch_max_throughput(const double *b, const int *u, const DevProfiles &pr, long long B, uint64_t N,
+                                  alp_result *out, cudaStream_t st) {
+  k_max_throughput<<<1, 256, 0, st>>>(b, u, pr, B, N, out);
+  return cudaGetLastError();
+}
+
 __global__ void k_init_keys(unsigned long long *keys, unsigned long long *counts, int n, unsigned long long *work,
                             int n_work, unsigned long long *fbest, unsigned *fdone) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;

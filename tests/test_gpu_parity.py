@@ -459,11 +459,84 @@ def test_finalize_gathered_matches_allreduce(P):
 
 def test_infeasible_and_zero_budget(P):
     d = generate.load("C1")
+    I = oracle.from_json(d)
     alp = P.Alp.from_instance(d)
-    r = alp.search(1e6, 16)
-    assert not r.found and r.feasible_count == 0 and r.index == -1
-    r = alp.search(d["targets"][0], 0)
-    assert not r.found and r.feasible_count == 0
+    r = alp.search(1e6, 16)  # no candidate meets the target: the max-T_w fallback
+    fb = oracle.max_throughput(I, 16)
+    assert not r.found and r.feasible_count == 0 and r.fallback and r.index == fb["index"]
+    assert r.throughput == fb["throughput"] and r.units == fb["units"] and r.latency == float("inf")
+    r = alp.search(d["targets"][0], 0)  # nothing fits a zero budget: no fallback either
+    assert not r.found and r.feasible_count == 0 and not r.fallback and r.index == -1
+
+
+def _fallback_closed_form(I, B):
+    """Separable construction of the max-T_w candidate (pinned against the brute-force definition in
+    tests/test_oracle.py::test_max_throughput_separable_closed_form), for spaces too large to enumerate."""
+    tab = oracle.option_table(I, 1.0)
+    ok = [[oracle.floor_ok(I, m, k) for k in range(I.K)] for m in range(I.M)]
+
+    def minu(m, v):
+        c = [int(tab["u"][m][k]) for k in range(I.K) if ok[m][k] and tab["b"][m][k] >= v]
+        return min(c) if c else None
+    best = None
+    for v in sorted(set(tab["b"].ravel().tolist())):
+        mus = [minu(m, v) for m in range(I.M)]
+        if all(x is not None for x in mus) and sum(mus) <= B:
+            best = v
+    if best is None:
+        return None
+    idx, used = 0, 0
+    for m in range(I.M):
+        rest = sum(minu(j, best) for j in range(m + 1, I.M))
+        k = next(k for k in range(I.K) if ok[m][k] and tab["b"][m][k] >= best and used + int(tab["u"][m][k]) + rest <= B)
+        used += int(tab["u"][m][k])
+        idx = idx * I.K + k
+    return {"index": idx, "throughput": best, "units": used}
+
+
+def test_infeasible_fallback_hand_case(P):
+    """The App. A hand case at lambda = 5 (infeasible for every budget): B = 8 -> index 45, T_w 4,
+    8 units; B = 7 -> 9 (T_w 2, 4 units); B = 3 -> 0; B = 1 -> no candidate fits (no fallback)."""
+    d = generate.load("hand")
+    alp = P.Alp.from_instance(d)
+    for B, (idx, tw, units) in {8: (45, 4.0, 8), 7: (9, 2.0, 4), 3: (0, 1.0, 2)}.items():
+        r = alp.search(5.0, B)
+        assert not r.found and r.fallback and (r.index, r.throughput, r.units) == (idx, tw, units), B
+        assert r.feasible_count == 0 and r.latency == float("inf")
+    r = alp.search(5.0, 1)
+    assert not r.found and not r.fallback and r.index == -1
+    # through the batch and the budget-sweep paths too
+    res = alp.search_batch([5.0, 1.0], 8)
+    assert res[0].fallback and res[0].index == 45 and res[1].found and not res[1].fallback
+    res = alp.search_queries([5.0] * 4, [8, 7, 3, 1])
+    assert [(x.fallback, x.index) for x in res] == [(True, 45), (True, 9), (True, 0), (False, -1)]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_infeasible_fallback_vs_oracle(P, name):
+    d = generate.load(name)
+    I = oracle.from_json(d)
+    alp = P.Alp.from_instance(d)
+    lam = 50.0 * d["lambda_star"]
+    for B in (d["budget_units"], d["budget_units"] // 3, 5):
+        r = alp.search(lam, B)
+        fb = oracle.max_throughput(I, B) if I.N <= 70000 else _fallback_closed_form(I, B)
+        assert not r.found and r.feasible_count == 0
+        if fb is None:
+            assert not r.fallback
+            continue
+        assert r.fallback and (r.index, r.throughput, r.units) == (fb["index"], fb["throughput"], fb["units"]), B
+        grid = [oracle.option_grid(I, k) for k in oracle.decode(I, r.index)]
+        assert [g[0] for g in grid] == r.share_units and [g[1] for g in grid] == r.tp and [g[2] for g in grid] == r.replicas
+    # the sharded path (shard search + finalize) reports the same fallback
+    import torch
+    keys = torch.empty(1, dtype=torch.int64, device="cuda")
+    cnts = torch.empty(1, dtype=torch.int64, device="cuda")
+    B = d["budget_units"]
+    lo, hi = alp.shard_range(B, 1, 3)
+    alp.search_shard([lam], B, lo, hi, keys.data_ptr(), cnts.data_ptr())
+    r = alp.finalize([lam], B, keys.data_ptr(), cnts.data_ptr())[0]
+    assert r.fallback and r.index == alp.search(lam, B).index
 
 
 def test_validation_errors(P):
