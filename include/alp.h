@@ -49,7 +49,9 @@ typedef enum {
   ALP_EINVAL = 1,      /* invalid argument (field named by alp_last_error) */
   ALP_EINFEASIBLE = 2, /* search finished but no candidate is feasible (result.found = 0) */
   ALP_EINTERNAL = 3,   /* internal inconsistency */
-  ALP_ECUDA = 4        /* CUDA runtime error (message in alp_last_error) */
+  ALP_ECUDA = 4,       /* CUDA runtime error (message in alp_last_error) */
+  ALP_ENCCL = 5        /* cross-GPU exchange failed (raised by the binding around torch.distributed's
+                          NCCL collectives; the library itself never calls NCCL) */
 } alp_status;
 
 typedef enum { ALP_P_MEAN = 0, ALP_P50 = 1, ALP_P90 = 2, ALP_P99 = 3 } alp_percentile; /* PAPER.md:356 "percentile P" */

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("ALP_LIB") or os.path.join(HERE, "lib", "libscepsy_alp
 MAX_M = 16
 PCT = {"mean": 0, "p50": 1, "p90": 2, "p99": 3}
 
-ALP_OK, ALP_EINVAL, ALP_EINFEASIBLE, ALP_EINTERNAL, ALP_ECUDA = range(5)
+ALP_OK, ALP_EINVAL, ALP_EINFEASIBLE, ALP_EINTERNAL, ALP_ECUDA, ALP_ENCCL = range(6)
 
 
 class AlpError(RuntimeError):

@@ -20,15 +20,18 @@ from typing import Sequence
 import torch
 import torch.distributed as dist
 
-from . import Alp, PeerBuffer, Result
+from . import ALP_ENCCL, Alp, AlpError, PeerBuffer, Result
 
 
 def reduce_keys(keys: torch.Tensor, counts: torch.Tensor, group=None) -> None:
     """In-place cross-rank reduction of per-target (key, count) pairs (no-op for world size 1)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
-    dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    try:
+        dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    except (RuntimeError, dist.DistBackendError) as e:
+        raise AlpError(ALP_ENCCL, f"all-reduce of the (key, count) pairs failed: {e}") from e
 
 
 def gather_pairs(pairs: torch.Tensor, gathered: torch.Tensor, group=None) -> int:
@@ -38,10 +41,13 @@ def gather_pairs(pairs: torch.Tensor, gathered: torch.Tensor, group=None) -> int
         gathered[: pairs.numel()].copy_(pairs)
         return 1
     world = dist.get_world_size(group)  # world 1 still runs the collective (one code path)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(gathered, pairs, group=group)
-    else:  # gloo (CPU tests, several ranks on one GPU): list form
-        dist.all_gather(list(gathered[: world * pairs.numel()].view(world, -1).unbind(0)), pairs, group=group)
+    try:
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(gathered, pairs, group=group)
+        else:  # gloo (CPU tests, several ranks on one GPU): list form
+            dist.all_gather(list(gathered[: world * pairs.numel()].view(world, -1).unbind(0)), pairs, group=group)
+    except (RuntimeError, dist.DistBackendError) as e:  # NCCL / gloo failure -> the library's status
+        raise AlpError(ALP_ENCCL, f"all-gather of the (key, count) pairs failed: {e}") from e
     return world
 
 

@@ -145,3 +145,36 @@ def test_search_u_keeps_uniform_datapath():
     ptx = open(obj + ".ptxas.txt").read()
     for m in re.finditer(r"Function properties for (\S*k_search_u\S*)\n.*\n.*Used (\d+) registers", ptx):
         assert int(m.group(2)) <= 80, m.group(1)
+
+
+def test_collective_failure_maps_to_alp_enccl(monkeypatch):
+    """A failing collective surfaces as AlpError(ALP_ENCCL) from the exchange helpers (§8(b) status
+    5), not as a bare backend exception (one-rank gloo group on 127.0.0.1; the collective is made to
+    fail)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_15186_b200 as P
+    from paper_2604_15186_b200 import dist as pdist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        def boom(*a, **k):
+            raise RuntimeError("simulated transport failure")
+        monkeypatch.setattr(dist, "all_gather", boom)
+        monkeypatch.setattr(dist, "get_world_size", lambda group=None: 2)
+        monkeypatch.setattr(dist, "all_reduce", boom)
+        pairs = torch.zeros(2, dtype=torch.int64)
+        with pytest.raises(P.AlpError) as e:
+            pdist.gather_pairs(pairs, torch.empty(4, dtype=torch.int64))
+        assert e.value.status == P.ALP_ENCCL
+        with pytest.raises(P.AlpError) as e:
+            pdist.reduce_keys(torch.zeros(1, dtype=torch.int64), torch.zeros(1, dtype=torch.int64))
+        assert e.value.status == P.ALP_ENCCL
+    finally:
+        monkeypatch.undo()
+        dist.destroy_process_group()
