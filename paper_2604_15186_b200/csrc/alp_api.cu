@@ -955,7 +955,7 @@ void fill_finalize(alp_s *h, SearchArgs &a) {
 // arguments with its shared-memory layout, lut geometry and grid; false when not applicable.
 bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, int &grid) {
   if (getenv("ALP_NO_UR") || n < 1 || n > kInlineTargets || a.q_budget || h->from_terms ||
-      h->rows_per_lane != 12 || hi >= (1ull << 31) || n * h->M * h->K > 8192)
+      h->rows_per_lane != search_u_rows() || hi >= (1ull << 31) || n * h->M * h->K > 8192)
     return false;
   const int R = a.budget, Kb = h->Kb;
   auto umax = [&](int m) {

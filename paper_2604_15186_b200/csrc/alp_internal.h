@@ -232,6 +232,7 @@ cudaError_t launch_search(const SearchArgs &a, int grid, cudaStream_t st);
 // (before_search, if set, is recorded on st between the prep and the search kernel)
 cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cudaEvent_t before_search);
 int search_u_max_blocks_per_sm(const SearchArgs &a);
+int search_u_rows();   // rows per lane the uniform-register kernel was compiled for (ALP_U_ROWS)
 bool search_u_busy();  // a uniform-register search launched on this device has not completed yet
 bool search_u_claim(); // take the bank for a peer search if it is free (see alp_search_u.cu)
 void search_u_release();

@@ -213,13 +213,16 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
 // scalar vector operand broadcast by .F32; the b pair read from the uniform register file) and one
 // FMNMX3 acc_i = min(acc_i, x, y): 1 issue slot per candidate and half the LDCU of the row-pair form
 // (tools/microbench/pipes7: 96 vs 93 candidates/clk/SM at 18 b per row, 103 vs 98 at 64).
+#ifndef ALP_U_ROWS
+#define ALP_U_ROWS 12  // rows per lane of the uniform-register kernel (the plan's lane tiles)
+#endif
 template <int NB4, bool TAIL2>
-__device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[12], float (&acc)[12]) {
+__device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[ALP_U_ROWS], float (&acc)[ALP_U_ROWS]) {
 #pragma unroll
   for (int j = 0; j < 2 * NB4 + (TAIL2 ? 1 : 0); ++j) {
     const float2 b = rb[j];
 #pragma unroll
-    for (int i = 0; i < 12; ++i) {
+    for (int i = 0; i < ALP_U_ROWS; ++i) {
       float x, y;
       add2(x, y, Qa[i], b.x, b.y);
       acc[i] = min3(acc[i], x, y);
@@ -230,7 +233,7 @@ __device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[1
 // ------------------------------------------------------------------ search: one warp per block
 template <int NB4, bool TAIL2>
 __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchArgs P, const unsigned char *ug) {
-  constexpr int T = 12;
+  constexpr int T = ALP_U_ROWS;
   extern __shared__ __align__(16) unsigned char smem[];
   // per target [g1*K + 2] terms of LLMs 0..g1-1 then {0, +inf}, all targets copied up front: any
   // lane-divergent code inside the target loop makes ptxas give up the uniform datapath there
@@ -631,6 +634,8 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
 // The bank for a peer search: taken only when free and not claimed, atomically with the check, so
 // two ranks of one exchange sharing a device never both take it (the second would wait for the
 // first, which waits for the second).  The claim ends at the launch (or search_u_release).
+int search_u_rows() { return ALP_U_ROWS; }
+
 bool search_u_claim() {
   std::lock_guard<std::mutex> lock(g_u_mu);
   UState &u = ustate();
