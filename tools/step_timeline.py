@@ -1,7 +1,7 @@
 """Device timeline of one search step (CUPTI via torch.profiler): every kernel / memcpy of the step
 with its start offset and duration, so gaps between launches are visible.
 
-    python tools/step_timeline.py [--workload C4] [--mode shard|search]
+    python tools/step_timeline.py [--workload C4] [--mode shard|search|peer]
 """
 import argparse
 import os
@@ -30,11 +30,14 @@ def main():
     keys = torch.empty(len(targets), dtype=torch.int64, device="cuda")
     counts = torch.empty(len(targets), dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    buf = P.PeerBuffer.alloc(len(targets), 1) if args.mode == "peer" else None
 
     def step():
         with torch.cuda.stream(st):
             if args.mode == "search":
                 return alp.search_batch(targets, B)
+            if args.mode == "peer":  # search + in-kernel exchange (one rank, the whole range)
+                return alp.search_peer(targets, B, lo, hi, 0, [buf.ptr], st.cuda_stream)
             alp.search_shard(targets, B, lo, hi, keys.data_ptr(), counts.data_ptr(), st.cuda_stream)
             return alp.finalize(targets, B, keys.data_ptr(), counts.data_ptr(), st.cuda_stream)
 
