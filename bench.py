@@ -204,28 +204,65 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     exchange = args.exchange if world > 1 else "none"
-    px = None
-    if exchange == "peer":
+    px, probe = None, None
+    if exchange in ("peer", "auto"):
         try:
             px = PeerExchange(nt)  # IPC handles of every rank's exchange buffer over the group
         except Exception as e:  # no peer access between these GPUs: the NCCL exchange instead
-            exchange = f"nccl (peer unavailable: {str(e)[:120]})"
+            probe = {"peer_unavailable": str(e)[:160]}
+        ok = torch.tensor([1 if px is not None else 0], dtype=torch.int64, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            px = None
     ws = torch.zeros(alp.workspace_bytes(nt), dtype=torch.uint8, device=dev) if px is not None else None
+    use_peer = px is not None and exchange == "peer"
 
-    def run_step(a, lo_, hi_):
+    def run_step(a, lo_, hi_, peer=None):
         """One search step through the public API: at N=1 the single-GPU call (option terms +
         exhaustive search + finalize); at N>1 shard search, then the exchange: the fused peer
-        exchange inside the search kernel (--exchange peer), or ONE NCCL all-gather of the
-        (key, count) pairs + the device finalize (--exchange nccl)."""
+        exchange inside the search kernel, or ONE NCCL all-gather of the (key, count) pairs + the
+        device finalize."""
         if world == 1:
             return a.search_batch(targets, B)[-1]
-        if px is not None:
+        if use_peer if peer is None else peer:
             w2 = ws if a is alp else torch.zeros(a.workspace_bytes(nt), dtype=torch.uint8, device=dev)
             return a.search_peer(targets, B, lo_, hi_, rank, px.ptrs, stream.cuda_stream, w2.data_ptr())[-1]
         with torch.cuda.stream(stream):
             a.search_shard(targets, B, lo_, hi_, pairs.data_ptr(), pairs.data_ptr() + 8 * nt, stream.cuda_stream)
             w = gather_pairs(pairs, gathered)  # ONE all-gather of the 16-byte (key, count) pairs
             return a.finalize_gathered(targets, B, gathered.data_ptr(), w, stream.cuda_stream)[-1]
+
+    if exchange == "auto" and px is not None:
+        # measured choice: both exchanges on this box (device step, max over ranks, median of 10 after
+        # 3 warm-ups, L2 flushed); they must return the same result; the faster one is timed below
+        probe = {}
+        got = {}
+        for mode in ("nccl", "peer"):
+            ms, good = [], 1
+            try:
+                for i in range(13):
+                    with torch.cuda.stream(stream):
+                        flush.zero_()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    r = run_step(alp, lo, hi, mode == "peer")
+                    if i >= 3:
+                        ms.append(alp.last_step_ms)
+                got[mode] = (r.found, r.index, r.feasible_count)
+            except Exception as e:  # e.g. a peer-exchange timeout: the NCCL exchange is timed
+                good = 0
+                probe[f"{mode}_error"] = str(e)[:160]
+            t = torch.tensor([sorted(ms)[len(ms) // 2] if ms else 1e9, good], dtype=torch.float64, device=dev)
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.MIN)
+            probe[f"{mode}_step_ms"] = float(t[0]) if int(t[1]) else None
+        agree = torch.tensor([1 if got.get("peer") is not None and got.get("peer") == got.get("nccl") else 0],
+                             dtype=torch.int64, device=dev)
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+        probe["results_agree"] = bool(agree.item())
+        use_peer = bool(agree.item()) and probe["peer_step_ms"] is not None and \
+            probe["peer_step_ms"] < (probe["nccl_step_ms"] or 1e9)
+    exchange = "peer" if use_peer else ("nccl" if world > 1 else "none")
 
     def step():
         return run_step(alp, lo, hi)
@@ -317,7 +354,8 @@ def run_ours(args):
             "time_to_optimum_ms": host_tot / args.steps, "host_ms_per_step": host_tot / args.steps,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded profile tables, workloads/instances)",
-            "config": {**_config(d, N, world, exchange if world > 1 else None)},
+            "config": {**_config(d, N, world, exchange if world > 1 else None),
+                       **({"exchange_probe": probe} if probe else {})},
             "result": {"index": res.index, "latency_key": res.latency_key, "latency_s": res.latency,
                        "throughput_req_s": res.throughput, "units": res.units,
                        "feasible_count": res.feasible_count},
@@ -363,8 +401,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
-                    help="N>1 cross-GPU reduction: NCCL all-gather + finalize kernel, or the fused peer exchange")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "peer"], default="auto",
+                    help="N>1 cross-GPU reduction: NCCL all-gather + finalize kernel, the fused peer exchange, or "
+                         "auto = both probed on this box (same result required), the faster one timed")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
 #pragma unroll
         for (int i = 0; i < T; ++i) acc[i] = finf();
       };
-      for (int j = 0; j < P.Kb; ++j) {
+      for (int j = 0; j < P.Kb;) {
         const float2 bv = s_tb[j];
         const int U = ubase + __float_as_int(bv.y);
         if (U > A.bmax) break;  // u-sorted: the rest is over every budget
@@ -144,8 +144,25 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
           if (cur >= 0) fold();
           cur = l;
         }
+        if (j + 1 < P.Kb) {  // two columns of the same level: FADD2 per row pair + FMNMX3
+          const float2 bw = s_tb[j + 1];
+          const int U2 = ubase + __float_as_int(bw.y);
+          if (U2 <= A.bmax && s_lvl[U2] == cur) {
+#pragma unroll
+            for (int i = 0; i < T; i += 2) {
+              float x0, x1, y0, y1;
+              add2b(x0, x1, Qa[i], Qa[i + 1], bv.x);  // {Q_i + b_j, Q_i+1 + b_j}
+              add2b(y0, y1, Qa[i], Qa[i + 1], bw.x);  // {Q_i + b_j+1, Q_i+1 + b_j+1}
+              acc[i] = min3(acc[i], x0, y0);
+              acc[i + 1] = min3(acc[i + 1], x1, y1);
+            }
+            j += 2;
+            continue;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < T; ++i) acc[i] = fminf(acc[i], __fadd_rn(Qa[i], bv.x));
+        ++j;
       }
       if (cur >= 0) fold();
     }
