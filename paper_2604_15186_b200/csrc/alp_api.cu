@@ -762,6 +762,10 @@ alp_status make_geometry(alp_s *h, int n_targets, int64_t budget, uint64_t lo, u
   a.seg_q = fine ? (uint32_t)h->Ka : h->nQ;
   a.seg_A = fine ? 1u : h->A;
   a.seg_mul = fine ? h->A : 1u;
+  a.u_nbulk = 0xffffffffu;  // k_search_u: no tail split unless u_tail_split sets one
+  a.u_S = 1;
+  a.u_As = h->A;
+  a.fd_S = make_fastdiv(1);
   a.budget = (int)Reff;
   a.n_targets = n_targets;
   a.D = (int)(std::upper_bound(h->dv.begin(), h->dv.end(), (int)Reff) - h->dv.begin());
@@ -1045,6 +1049,30 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   return true;
 }
 
+// k_search_u tail split: the last items of the rank's range are handed out as S sub-items of
+// ceil(A / S) a options (needs single-option segments), so the warps' last tickets are short.
+// Default: the last warps/2 items in 3 parts (C4 8-rank shard kernel 0.0758 -> 0.0737 ms, whole C4
+// 0.4383 -> 0.4362 ms; with the tickets prefetched this had not helped).  ALP_U_SPLIT="x,S": split
+// the last x * warps items (x = 0: off).
+void u_tail_split(SearchArgs &ua, uint64_t warps, uint64_t n_items) {
+  static double xw = 0.5;
+  static int S = 3;
+  static bool once = [] {
+    if (const char *v = getenv("ALP_U_SPLIT")) sscanf(v, "%lf,%d", &xw, &S);
+    return true;
+  }();
+  (void)once;
+  if (ua.seg_A != 1 || S < 2 || xw <= 0.0) return;
+  const int As = ((int)ua.A + S - 1) / S;
+  const int Sx = ((int)ua.A + As - 1) / As;
+  const uint64_t x = std::min<uint64_t>(n_items, (uint64_t)(xw * (double)warps));
+  if (x == 0 || Sx < 2 || n_items + x * (uint64_t)(Sx - 1) >= 0x7fffffffull) return;
+  ua.u_nbulk = (uint32_t)(n_items - x);
+  ua.u_S = (uint32_t)Sx;
+  ua.u_As = (uint32_t)As;
+  ua.fd_S = make_fastdiv((uint32_t)Sx);
+}
+
 // Targets per uniform-register launch for a large batch (0: the path does not apply): the most
 // (<= kInlineTargets) whose tables fit the constant bank.
 int ur_batch_group(alp_s *h, int64_t budget) {
@@ -1158,6 +1186,7 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
     g.a.grab_t1 = (n_items - n_items / 8) / (uint64_t)g.a.grab;
     static const bool dbg = getenv("ALP_DBG_TS") != nullptr;  // per-block timeline (diagnostics)
     if (ur && !ur_path(h, g.a, n, hi, ua, ugrid)) return fail(ALP_EINTERNAL, "uniform-register geometry changed");
+    if (ur) u_tail_split(ua, (uint64_t)ugrid, n_items);
     const int dgrid = ur ? ugrid : g.grid;
     if (dbg) {
       CU(h->g_dbg.ensure((size_t)(dgrid + 2) * 8));  // + one row of epilogue stamps

@@ -149,6 +149,10 @@ struct SearchArgs {
   // segment ids (key low word): row * seg_q + (first a option evaluated) / seg_A, where seg_A = 1
   // (single-option granularity) when rows * Ka < 2^32, else seg_A = A; seg_mul = A / seg_A
   uint32_t seg_q, seg_A, seg_mul;
+  // k_search_u tail split: tickets [0, u_nbulk) are whole items, then the rank's remaining items are
+  // cut into u_S sub-items of u_As a options (ticket -> item nbulk + j / u_S, part j % u_S)
+  uint32_t u_nbulk, u_S, u_As;
+  FastDiv fd_S;
   int budget;            // R (capped at the total max units); max over queries when q_budget is set
   const int *q_budget;   // [n_targets] per-query budgets (capped) or nullptr (all = budget)
   int n_targets;

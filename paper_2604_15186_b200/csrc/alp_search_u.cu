@@ -292,17 +292,29 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
     const float2 *rows_u = cu_pairs + ((P.u_tbase + t * P.u_tstride + P.u_off_btab_c[c]) >> 3);
     unsigned tnext = 0xffffffffu;
     if (lane == 0) tnext = (unsigned)atomicAdd(ctr, 1ull);
+    // tickets [0, nbulk) are whole items; the rank's last items are handed out as u_S sub-items of
+    // u_As a options each (single-option segments), so the warps finish within a sub-item's time
+    const uint32_t nbulk = min(P.u_nbulk, n);
+    const uint32_t ntk = nbulk + (n - nbulk) * P.u_S;
     for (;;) {
       const uint32_t k = __reduce_min_sync(0xffffffffu, tnext);
-      if (k >= n) break;
+      if (k >= ntk) break;
       if (P.dbg_ts && lane == 0 && blockIdx.x > 0) P.dbg_ts[blockIdx.x * 8 + 6] += 1;  // tickets taken (diagnostics)
-      const uint32_t it = (uint32_t)P.item_lo + k;
+      uint32_t kk = k, part = 0;
+      if (k >= nbulk) {
+        const uint32_t j = k - nbulk, ji = fdiv(j, P.fd_S);
+        part = j - ji * P.u_S;
+        kk = nbulk + ji;
+      }
+      const uint32_t it = (uint32_t)P.item_lo + kk;
       const uint32_t tq = fdiv(it, P.fd_nQ);
       const uint32_t q = it - tq * P.nQ;           // a-range of the row
       const uint32_t chunk = fdiv(tq, P.fd_ng);
       const uint32_t grp = tq - chunk * P.n_groups;
-      const int a0 = (int)(q * P.A), a1 = min(a0 + (int)P.A, P.Ka);
-      const uint32_t qs = q * P.seg_mul;             // segment slot of a0
+      const int q0 = (int)(q * P.A), q1 = min(q0 + (int)P.A, P.Ka);
+      const int a0 = k >= nbulk ? min(q0 + (int)(part * P.u_As), q1) : q0;
+      const int a1 = k >= nbulk ? min(a0 + (int)P.u_As, q1) : q1;
+      const uint32_t qs = k >= nbulk ? (uint32_t)a0 : q * P.seg_mul;  // segment slot of a0
       const float2 pf = cv.pfx(chunk);
       const int upfx = __float_as_int(pf.y);       // clamped at R + 1
       const uint32_t tile = grp * kWarpTiles + lane;
