@@ -9,6 +9,16 @@
 
 namespace alp {
 
+// asynchronous global -> shared copies (the staging wave: every load in flight at once)
+__device__ __forceinline__ void fin_cp4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void fin_cp8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
 // Finalize of target t from its reduced (key, count): the lowest canonical index inside the
 // winning segment, the winner's (share, tp, replicas) and its FP64 Eq. 1 / Eq. 2 prediction.
 // Blocks [part] of [nparts] split the re-scan of the segment; with nparts > 1 the last block to
@@ -23,11 +33,8 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   const FinalizeExtra &F = P.fin;
   const int K = P.K, MK = P.M * K, nG = F.nS + F.nT + F.nR;
   auto stamp = [&](int i) {  // ALP_DBG_TS (fused epilogue only): phases in the second extra row
-    if (P.dbg_ts && threadIdx.x == 0 && P.fz.on) {
-      unsigned long long g;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-      P.dbg_ts[(size_t)gridDim.x * 8 + 8 + i] = g;
-    }
+    if (P.dbg_ts && threadIdx.x == 0 && P.fz.on)  // SM clock cycles (same SM: exact phase deltas)
+      P.dbg_ts[(size_t)gridDim.x * 8 + 8 + i] = (unsigned long long)clock64();
   };
   stamp(0);
   // option terms of target t: the caller's shared-memory copy (fused kernel) or the global tables
@@ -52,16 +59,20 @@ __device__ inline void finalize_target(const SearchArgs &P, int t, unsigned long
   const uint32_t seg = (uint32_t)(key & 0xffffffffull);
   const float val = __uint_as_float((uint32_t)(key >> 32));
   const bool found = key != kKeyNone && val < __int_as_float(0x7f800000);
-  if (found && stage) {
+  if (found && stage) {  // cp.async: one wave of loads in flight, not one round trip per element
     for (int i = threadIdx.x; i < MK; i += blockDim.x) {
-      st_term[i] = __ldcg(term_g + i);
-      st_b[i] = __ldcg(b_g + i);
-      st_tau[i] = tau_s ? tau_s[i] : __ldcg(tau_g + i);
-      st_u[i] = P.u[i];
+      fin_cp8(st_term + i, term_g + i);
+      fin_cp8(st_b + i, b_g + i);
+      if (tau_s)
+        st_tau[i] = tau_s[i];
+      else
+        fin_cp4(st_tau + i, tau_g + i);
+      fin_cp4(st_u + i, P.u + i);
     }
     if (F.S)
       for (int i = threadIdx.x; i < nG; i += blockDim.x)
-        st_g[i] = i < F.nS ? F.S[i] : i < F.nS + F.nT ? F.T[i - F.nS] : F.R[i - F.nS - F.nT];
+        fin_cp4(st_g + i, i < F.nS ? F.S + i : i < F.nS + F.nT ? F.T + (i - F.nS) : F.R + (i - F.nS - F.nT));
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
   }
   uint32_t q = 0, chunk = 0, e = 0;

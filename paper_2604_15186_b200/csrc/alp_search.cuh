@@ -455,8 +455,8 @@ static __device__ __noinline__ void peer_exchange(unsigned char *const *s_buf, i
                                                   unsigned long long e, alp_result *out, long long timeout_ns,
                                                   unsigned long long *dbg) {
   static_assert(sizeof(PeerRow) % 8 == 0 && sizeof(alp_result) % 8 == 0, "rows move as 64-bit words");
-  auto stamp = [&](int i) {  // ALP_DBG_TS: the exchange's phases
-    if (dbg && threadIdx.x == 0) dbg[i] = (unsigned long long)globaltimer_ns();
+  auto stamp = [&](int i) {  // ALP_DBG_TS: the exchange's phases (SM clock cycles)
+    if (dbg && threadIdx.x == 0) dbg[i] = (unsigned long long)clock64();
   };
   __shared__ int s_fail;
   unsigned char *own = s_buf[me];
@@ -550,7 +550,7 @@ static __device__ __noinline__ void peer_epilogue(const SearchArgs &Pg, const un
   const PeerArgs &X = P.fz.peer;
   const int n = P.n_targets, W = X.world, me = X.rank;
   unsigned long long *dbg = P.dbg_ts ? P.dbg_ts + (size_t)gridDim.x * 8 : nullptr;
-  if (dbg && threadIdx.x == 0) dbg[0] = (unsigned long long)globaltimer_ns();
+  if (dbg && threadIdx.x == 0) dbg[0] = (unsigned long long)clock64();
   for (int j = threadIdx.x; j < W; j += blockDim.x) s_buf[j] = X.buf[j];
   if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned long long *>(X.buf[me]) + 1;  // this epoch
   __syncthreads();
@@ -563,7 +563,7 @@ static __device__ __noinline__ void peer_epilogue(const SearchArgs &Pg, const un
     mine[t].count = s_cnt[t];
   }
   __syncthreads();
-  if (dbg && threadIdx.x == 0) dbg[1] = (unsigned long long)globaltimer_ns();
+  if (dbg && threadIdx.x == 0) dbg[1] = (unsigned long long)clock64();
   peer_exchange(s_buf, me, W, n, e, X.out, X.timeout_ns, dbg);
 }
 

@@ -58,11 +58,10 @@ for k in sorted(by):
     print(f"  tickets {k:3d}: warps {len(v):5d}  loop-end min {v.min():6.1f} med {np.median(v):6.1f} max {v.max():6.1f}")
 h = np.histogram(lend[1:], bins=20)
 print("  loop-end histogram:", " ".join(f"{int(e):d}:{c}" for c, e in zip(h[0], h[1])))
+CLK = 1.965e3  # SM cycles per us (clocks.max.sm; the epilogue stamps are clock64 on one SM)
 if ep[0]:
-    e0 = int(ts[:, 0].min())
-    print("  peer epilogue (us from kernel start):", " ".join(f"{(x - e0) / 1e3:.1f}" for x in ep[:6]),
-          "| phases: start, local finalize done, rows + fence, flags, all flags seen, reduced")
+    print("  peer epilogue phases (us):", " ".join(f"{(ep[i + 1] - ep[i]) / CLK:.2f}" for i in range(5)),
+          "| local finalize, rows, fence + flags, wait for all flags, reduce + result")
 if fz[0]:
-    e0 = int(ts[:, 0].min())
-    print("  finalize (us from kernel start):", " ".join(f"{(x - e0) / 1e3:.1f}" for x in fz[:5]),
-          "| phases: start, digits + row terms, re-scan, winner terms, result stored")
+    print("  finalize phases (us):", " ".join(f"{(fz[i + 1] - fz[i]) / CLK:.2f}" for i in range(4)),
+          "| stage + digits + row terms, re-scan, winner terms, result stored")
