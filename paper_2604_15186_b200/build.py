@@ -33,8 +33,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
-    """Build the library (out/defines: tuning variants, e.g. defines=("ALP_A_UNROLL=2",))."""
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = (),
+          extra: tuple = ()) -> str:
+    """Build the library (out/defines/extra: tuning variants, e.g. defines=("ALP_A_UNROLL=2",),
+    extra=("-Xptxas", "-O2"))."""
     lib = out or LIB
     if not force and out is None and not _stale():
         return LIB
@@ -43,7 +45,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     def compile_one(src):
         obj = os.path.join(os.path.dirname(lib), src.replace(".cu", ".o") if out is None else
                            os.path.basename(lib) + "." + src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
