@@ -1,8 +1,10 @@
 """Randomised parity sweep of the CUDA path against the oracle (more cases than the test suite):
 seeded random instances (2-8 LLMs, 1-48 options per LLM, random budgets, memory floors on a third
-of them), three targets each plus one batch and one per-query-budget call of 2-19 targets; every
-result against the DP oracle (O2) and, for the single searches in small spaces, the brute-force
-oracle (O1).  Run once per launch path:
+of them), three targets each plus one batch and one per-query-budget call of 2-19 targets, a
+one-target budget sweep of 2-11 budgets (the one-pass k_search_levels; infeasible budgets also
+check the SPEC.md:374 fallback against its brute-force definition on small spaces) and a
+one-rank peer exchange; every result against the DP oracle (O2) and, for the single searches in
+small spaces, the brute-force oracle (O1).  Run once per launch path:
 
     python tests/sweep_parity.py [n_instances] [seed0]            # default path choice
     ALP_NO_UR=1 python tests/sweep_parity.py ...                  # fused k_search
@@ -74,6 +76,42 @@ def main():
                 else:
                     bad += 1
                     print("MISMATCH", kind, s, lam, bj, r.index, idx, r.feasible_count, cnt, flush=True)
+        # one target, several budgets: the one-pass budget sweep (k_search_levels), vs the DP oracle
+        lam = float(rng.uniform(0.05, 2.0))
+        sweep = sorted(int(x) for x in rng.integers(0, 8 * M * 4, size=int(rng.integers(2, 12))))
+        paths["sweep"] = paths.get("sweep", 0) + len(sweep)
+        tab = oracle.option_table(I, lam)
+        for bj, r in zip(sweep, alp.search_queries([lam] * len(sweep), sweep)):
+            f, v, idx, cnt = dp.search(tab["tau"], tab["u"], bj)
+            good = (r.found == f and r.feasible_count == cnt and
+                    (not f or (r.index == idx and np.float32(r.latency_key) == np.float32(v))))
+            if not f and I.N <= 2_000_000:  # the SPEC.md:374 fallback vs its brute-force definition
+                fb = oracle.max_throughput(I, bj) if I.N <= 200_000 else None
+                if fb is not None or I.N <= 200_000:
+                    good = good and (r.fallback == (fb is not None)) and (
+                        fb is None or (r.index == fb["index"] and r.throughput == fb["throughput"]))
+            if good:
+                ok += 1
+            else:
+                bad += 1
+                print("MISMATCH sweep", s, lam, bj, r.index, idx, r.feasible_count, cnt, flush=True)
+        # the fused peer exchange with one rank over the whole range (search + in-kernel reduction)
+        if not hasattr(main, "_buf"):
+            main._buf = P.PeerBuffer.alloc(1, 1)
+        lo, hi = alp.shard_range(budget, 0, 1)
+        try:
+            r = alp.search_peer([lam], budget, lo, hi, 0, [main._buf.ptr])[0]
+            f, v, idx, cnt = dp.search(tab["tau"], tab["u"], budget)
+            good = (r.found == f and r.feasible_count == cnt and
+                    (not f or (r.index == idx and np.float32(r.latency_key) == np.float32(v))))
+            paths["peer"] = paths.get("peer", 0) + 1
+            if good:
+                ok += 1
+            else:
+                bad += 1
+                print("MISMATCH peer", s, lam, budget, r.index, idx, r.feasible_count, cnt, flush=True)
+        except P.AlpError:  # not a fused-size problem: the peer exchange does not apply
+            paths["peer_n/a"] = paths.get("peer_n/a", 0) + 1
     print({"instances": n, "searches": ok + bad, "match": ok, "mismatch": bad, "also_brute_force": brute,
            "paths": paths, "env": {k: v for k, v in os.environ.items() if k.startswith("ALP_")}})
 
