@@ -222,7 +222,8 @@ __global__ void k_finalize(const __grid_constant__ SearchArgs P) {
     key = P.fin.keys[t];
     count = P.fin.counts[t];
   }
-  finalize_target(P, t, key, count, blockIdx.x, gridDim.x);
+  // one block per target: its inputs staged in dynamic shared memory in one wave of loads
+  finalize_target(P, t, key, count, blockIdx.x, gridDim.x, nullptr, nullptr, P.fin.stage != 0 && gridDim.x == 1);
 }
 
 // ------------------------------------------------------------------ multi-workflow split (NEXT-1)
@@ -343,7 +344,12 @@ cudaError_t launch_finalize(const SearchArgs &a, cudaStream_t st) {
   const long long cand = (long long)a.Ka * a.Kb;
   const int nb = (int)std::min<long long>(64, std::max<long long>(1, cand / (256 * 16)));
   max_carveout(reinterpret_cast<const void *>(k_finalize));
-  return launch_pdl(k_finalize, dim3(nb, a.n_targets), dim3(256), 0, st, a);
+  // a one-block re-scan stages the finalize inputs (option terms, units, FP64 terms, grids) in
+  // dynamic shared memory by one wave of cp.async: C4's K3 8.0 -> see profiles
+  SearchArgs b = a;
+  const size_t stage = finalize_stage_bytes(a.M, a.K, a.fin.nS, a.fin.nT, a.fin.nR);
+  b.fin.stage = (nb == 1 && a.fin.S && stage <= 48 * 1024) ? 1 : 0;
+  return launch_pdl(k_finalize, dim3(nb, a.n_targets), dim3(256), b.fin.stage ? stage : 0, st, b);
 }
 
 cudaError_t launch_predict(const PredictArgs &a, cudaStream_t st) {

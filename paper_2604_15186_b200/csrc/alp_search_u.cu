@@ -111,8 +111,15 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   for (int i = tid; i < P.g0 * K; i += nt) cp_async4(s_u + i, P.u + i);
   if (P.a_llm >= 0)
     for (int i = tid; i < P.Ka; i += nt) cp_async4(s_ua + i, P.u + P.a_llm * K + i);
-  // group unit sums, clamped at R + 1 (an over-budget sum only has to keep r negative)
-  for (uint32_t g = tid; g < P.n_groups; g += nt) reinterpret_cast<int *>(T)[g] = min(P.gsum[g], R + 1);
+  // group unit sums, clamped at R + 1 (an over-budget sum only has to keep r negative): the first
+  // 4 per thread loaded now, in flight with the staging wave, and stored after the option terms (a
+  // load -> store loop here put its DRAM round trips in front of the wait)
+  int gv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t g = tid + (uint32_t)(j * nt);
+    gv[j] = g < P.n_groups ? __ldg(P.gsum + g) : 0;
+  }
   cp_async_wait();
   __syncthreads();
   for (int i = tid; i < NT * MK; i += nt) {
@@ -127,6 +134,12 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     P.fz.o_b[i] = b;
   }
   stamp(6);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t g = tid + (uint32_t)(j * nt);
+    if (g < P.n_groups) reinterpret_cast<int *>(T)[g] = min(gv[j], R + 1);
+  }
+  for (uint32_t g = tid + 4u * nt; g < P.n_groups; g += nt) reinterpret_cast<int *>(T)[g] = min(P.gsum[g], R + 1);
   for (int i = tid; i <= D; i += nt) s_len[i] = min(s_len[i], Kb);
   __syncthreads();
   stamp(7);
