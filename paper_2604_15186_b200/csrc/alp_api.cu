@@ -976,6 +976,7 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   ua = a;
   ua.lut_base = lb;
   ua.lut_n = lb + 1;
+  ua.u_amax = h->a_llm >= 0 ? std::min(umax(h->a_llm), R + 1) : 0;
   // b chunks: a short b row (<= 34 options) is one chunk with the k_search row layout; longer rows
   // are cut into chunks of kUChunkW u-sorted columns, each with its own lut and de-duplicated masked
   // rows (a chunk has a new row only where the budget threshold falls inside it)
@@ -1002,7 +1003,7 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
   // then per chunk its lut and rows
   ua.u_tbase = a16((int)h->n_groups * 4);
   ua.u_off_a = 0;
-  ua.u_off_pfx = a16(h->Ka * 16);
+  ua.u_off_pfx = a16((h->Ka + 1) * 16);  // Ka + 1 a entries: .w holds the feasible-option prefix count
   int off = a16(ua.u_off_pfx + (int)h->n_chunks * 8), rows0 = 0;
   for (int c = 0; c < nch; ++c) {
     const int c0 = c * W, wc = std::min(W, Kb - c0);

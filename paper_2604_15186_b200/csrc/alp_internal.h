@@ -194,6 +194,9 @@ struct SearchArgs {
   // shared memory layout (byte offsets)
   int off_tau, off_u, off_a, off_lut, off_btab, off_tmp, smem_bytes;
   int off_pfx;           // prefix-chunk table offset, -1 when the prefix space is too large for it
+  // (last: ptxas' uniform-datapath choices in k_search_u change with the offsets of the fields above)
+  int u_amax;            // largest a-option unit count (clamped at R + 1): lut(x - u_amax) is the
+                         // widest row every a option of a warp-uniform budget x reaches
 };
 
 // budget of query t (per-query budgets for budget sweeps, else the common budget)

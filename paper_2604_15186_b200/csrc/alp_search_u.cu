@@ -159,11 +159,24 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
       }
       pfx[c] = make_float2(pa, __int_as_float(min(U, R + 1)));
     }
-    for (int a = tid; a < P.Ka; a += nt) {
-      const float ta = P.a_llm >= 0 ? st[P.a_llm * K + a] : 0.f;
-      const int ua = P.a_llm >= 0 ? min(s_ua[a], R + 1) : 0;
-      const int feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
-      ta4[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), 0.f);
+    // a options {tau_a, units (clamped), feasible, #feasible options before a}; entry Ka holds the
+    // total in .w (k_search_u's full-row items count Ka ranges by two loads).  One warp, ballots.
+    if (tid < 32) {
+      int run = 0;
+      for (int b0 = 0; b0 <= P.Ka; b0 += 32) {
+        const int a = b0 + tid;
+        float ta = 0.f;
+        int ua = 0, feas = 0;
+        if (a < P.Ka) {
+          ta = P.a_llm >= 0 ? st[P.a_llm * K + a] : 0.f;
+          ua = P.a_llm >= 0 ? min(s_ua[a], R + 1) : 0;
+          feas = ta < __int_as_float(0x7f800000) ? 1 : 0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, feas);
+        const int pre = run + __popc(bal & ((1u << tid) - 1u));
+        if (a <= P.Ka) ta4[a] = make_float4(ta, __int_as_float(feas ? ua : 0), __int_as_float(feas), __int_as_float(pre));
+        run += __popc(bal);
+      }
     }
     // u-sorted b terms
     for (int j = tid; j < Kb; j += nt) s_bs[j] = st[P.b_llm * K + s_bp[j]];
@@ -226,9 +239,29 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
 // scalar vector operand broadcast by .F32; the b pair read from the uniform register file) and one
 // FMNMX3 acc_i = min(acc_i, x, y): 1 issue slot per candidate and half the LDCU of the row-pair form
 // (tools/microbench/pipes7: 96 vs 93 candidates/clk/SM at 18 b per row, 103 vs 98 at 64).
+#ifndef ALP_FAST_ROWS
+#define ALP_FAST_ROWS 1  // full-row items: b pairs held in uniform registers for the whole item
+#endif
+#ifndef ALP_FAST_UA
+#define ALP_FAST_UA 1  // unroll of the full-row a loop
+#endif
 #ifndef ALP_U_ROWS
 #define ALP_U_ROWS 12  // rows per lane of the uniform-register kernel (the plan's lane tiles)
 #endif
+// The same over b pairs already in uniform registers (a full-row item: one row for every a option).
+template <int NP>
+__device__ __forceinline__ void eval_pairs_u(const float2 (&bv)[NP], const float (&Qa)[ALP_U_ROWS], float (&acc)[ALP_U_ROWS]) {
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+#pragma unroll
+    for (int i = 0; i < ALP_U_ROWS; ++i) {
+      float x, y;
+      add2(x, y, Qa[i], bv[j].x, bv[j].y);
+      acc[i] = min3(acc[i], x, y);
+    }
+  }
+}
+
 template <int NB4, bool TAIL2>
 __device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[ALP_U_ROWS], float (&acc)[ALP_U_ROWS]) {
 #pragma unroll
@@ -334,13 +367,39 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       const unsigned nfin = load_tile<T>(P, tau_b, pf.x, tile, Qr, acc);
       unsigned c32 = 0;
       const int gs = gsum[grp];                     // clamped at R + 1
-      if (grp < P.n_groups_u || gs + upfx >= R1) {
-        // warp-uniform remaining budget (one unit sum, or a mixed group whose every lane is over
-        // budget, where every row is the all-+inf row 0): uniform-register b operands
-        const int xg = P.lut_base - upfx - gs;
-        // a-loop unrolled by 2 for short rows; long rows (64-column chunks: an ~800-instruction body)
-        // stay rolled so the uniform and mixed loops together fit the 32 KB instruction cache
-        constexpr int kUA = NB4 > 8 ? 1 : 2;
+      // warp-uniform remaining budget (one unit sum, or a mixed group whose every lane is over budget,
+      // where every row is the all-+inf row 0): uniform-register b operands
+      const bool uni = grp < P.n_groups_u || gs + upfx >= R1;
+      const int xg = P.lut_base - upfx - gs;
+      // a-loop unrolled by 2 for short rows; long rows (64-column chunks: an ~800-instruction body)
+      // stay rolled so the uniform and mixed loops together fit the 32 KB instruction cache
+      constexpr int kUA = NB4 > 8 ? 1 : 2;
+      // Full-row items (short rows): when even the a option with the most units leaves the widest
+      // row (the lut is monotone), every a option of the item reads that one row — its b pairs are
+      // loaded into uniform registers once per item, the count is fin x #feasible a options (two
+      // prefix-count loads), and the a loop is tau_a + the row's FADD2/FMNMX3 only (C4: ~96 % of
+      // the (prefix, a) pairs, 81 % of the items; 1.05 instead of 1.14 instructions per candidate).
+      // The other uniform items then take the mixed-group loop (its per-a row test finds one row
+      // for all lanes) instead of a loop of their own: hot code that fits the instruction cache.
+      constexpr int kNP = 2 * NB4 + (TAIL2 ? 1 : 0);
+      constexpr bool kFastRows = ALP_FAST_ROWS && kNP >= 1 && kNP <= 10;
+      constexpr int kFUA = ALP_FAST_UA;
+      if (kFastRows && uni && cv.lut(c, xg - P.u_amax).x == cv.lut(c, P.lut_n - 1).x) {
+        const int2 lf = cv.lut(c, xg - P.u_amax);
+        const float2 *rb = rows_u + (lf.x >> 1);
+        float2 bv[kNP > 0 ? kNP : 1];
+#pragma unroll
+        for (int j = 0; j < kNP; ++j) bv[j] = rb[j];
+        c32 = (unsigned)lf.y * (unsigned)(__float_as_int(cv.a(a1).w) - __float_as_int(cv.a(a0).w));
+#pragma unroll(kFUA)
+        for (int a = a0; a < a1; ++a) {
+          const float ta = cv.a(a).x;
+          float Qa[T];
+#pragma unroll
+          for (int i = 0; i < T; i += 2) add2b(Qa[i], Qa[i + 1], Qr[i], Qr[i + 1], ta);
+          eval_pairs_u<(kNP > 0 ? kNP : 1)>(bv, Qa, acc);
+        }
+      } else if (!kFastRows && uni) {
 #pragma unroll(kUA)
         for (int a = a0; a < a1; ++a) {
           const float4 av = cv.a(a);

@@ -123,7 +123,8 @@ def test_search_u_keeps_uniform_datapath():
     analysis (a __syncwarp before the epilogue, an inlined exchange, a register cap each dropped it
     silently: DESIGN.md §5).  Guard on the built object: every variant for b rows of >= 12 options
     (NB4 >= 3: C4's 18, the 64-column chunks of C3) has FADD2 with a uniform-register operand and
-    <= 80 registers (24 one-warp blocks/SM); no variant spills.  The variants for rows of 2-10
+    <= 88 registers (>= 23 one-warp blocks/SM; the full-row loop holds its b pairs in uniform
+    registers and took C4's variant from 76 to 84); no variant spills.  The variants for rows of 2-10
     options (NB4 <= 2, e.g. the 8-option hand case) may lose it: their rows are short anyway."""
     import re
     import shutil
@@ -148,7 +149,7 @@ def test_search_u_keeps_uniform_datapath():
     ptx = open(obj + ".ptxas.txt").read()
     for m in re.finditer(r"Function properties for (\S*k_search_u\S*)\n.*\n.*Used (\d+) registers", ptx):
         if int(re.search(r"k_search_uILi(\d+)E", m.group(1)).group(1)) >= 3:
-            assert int(m.group(2)) <= 80, m.group(1)
+            assert int(m.group(2)) <= 88, m.group(1)
 
 
 def test_collective_failure_maps_to_alp_enccl(monkeypatch):
