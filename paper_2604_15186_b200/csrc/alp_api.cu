@@ -1226,9 +1226,10 @@ alp_status search_shard_impl(alp_s *h, const double *targets, const int64_t *bud
               "max %.1f | loop-end min %.1f med %.1f max %.1f | end max %.1f\n", dgrid, q(0, .5), q(0, 1), q(4, .5),
               q(4, 1), q(1, .5), q(1, 1), q(2, 0), q(2, .5), q(2, 1), q(3, 1));
       if (ur && ts[5])  // k_uprep phases (us from its start; the search's t0 is later)
-        fprintf(stderr, "[alp dbg] k_uprep us: terms %.2f | plan tables landed %.2f | end %.2f | search t0 %+.2f\n",
-                (ts[6] - ts[5]) * 1e-3, (ts[7] - ts[5]) * 1e-3, (ts[13] - ts[5]) * 1e-3,
-                ((double)t0 - (double)ts[5]) * 1e-3);
+        fprintf(stderr, "[alp dbg] k_uprep us: staged %.2f | terms %.2f | plan tables landed %.2f | a/pfx/b-sorted %.2f | "
+                "b rows + lut %.2f | end %.2f | search t0 %+.2f\n",
+                (ts[15] - ts[5]) * 1e-3, (ts[6] - ts[5]) * 1e-3, (ts[7] - ts[5]) * 1e-3, (ts[21] - ts[5]) * 1e-3,
+                (ts[23] - ts[5]) * 1e-3, (ts[13] - ts[5]) * 1e-3, ((double)t0 - (double)ts[5]) * 1e-3);
     }
   }
   CU(cudaEventRecord(h->ev1, st));
@@ -1598,6 +1599,52 @@ alp_status alp_shard_range(const alp_t *h, int64_t budget_units, int32_t rank, i
   }();
   const uint64_t nq = h->nQ, rows = alp_num_items(h, budget_units) / nq;
   const uint64_t ng = h->n_groups, ngu = std::min<uint64_t>(h->n_groups_u, ng);
+  // Short b rows (k_search_u's full-row loop, Kb <= 20): a uniform group's row is cheaper when even
+  // the a option with the most units leaves it the widest masked row (1.05 vs 1.17 instructions per
+  // candidate), which depends on the chunk's prefix units: per-chunk weights, rows of a uniform
+  // partial group weigh `wp` (ALP_SHARD_PARTIAL, default 1.125).
+  static const int wp16 = [] {
+    const char *v = getenv("ALP_SHARD_PARTIAL");
+    return v ? std::max(1, (int)std::lround(16.0 * atof(v))) : 18;
+  }();
+  if (h->Kb <= 20 && h->g0 >= 1 && ng > 0 && rows % ng == 0 && (uint64_t)h->n_chunks == rows / ng &&
+      h->gsum.size() >= ng && wp16 != 16) {
+    const long long R = std::min<long long>(budget_units, h->umax_total);
+    int ubw = 0;  // widest row: every b option with u <= R
+    for (int k = 0; k < h->K; ++k) {
+      const int ub = h->u[(size_t)h->b_llm * h->K + k];
+      if (ub <= R) ubw = std::max(ubw, ub);
+    }
+    const long long amax = h->a_llm >= 0 ? std::min<long long>(h->umax_a, R + 1) : 0;
+    std::vector<int> gs_sorted(h->gsum.begin(), h->gsum.begin() + ngu);
+    std::sort(gs_sorted.begin(), gs_sorted.end());
+    const uint64_t nc = h->n_chunks;
+    std::vector<long long> thr(nc);
+    std::vector<uint64_t> wcum(nc + 1, 0);
+    for (uint64_t c = 0; c < nc; ++c) {
+      long long upfx = 0;
+      for (int m = 0; m < h->g0; ++m) upfx += h->u[(size_t)m * h->K + (c / h->pw[m]) % (uint64_t)h->K];
+      thr[c] = R - upfx - amax - ubw;  // a uniform group of unit sum gs is full-row iff gs <= thr
+      const uint64_t nfull = thr[c] < 0 ? 0 : (uint64_t)(std::upper_bound(gs_sorted.begin(), gs_sorted.end(), (int)std::min<long long>(thr[c], INT32_MAX)) - gs_sorted.begin());
+      wcum[c + 1] = wcum[c] + 16 * nfull + (uint64_t)wp16 * (ngu - nfull) + (uint64_t)wm16 * (ng - ngu);
+    }
+    auto bound = [&](uint64_t r) -> uint64_t {
+      if (r == 0) return 0;
+      if (r >= (uint64_t)world) return rows;
+      const unsigned __int128 tgt = (unsigned __int128)wcum[nc] * r / (uint64_t)world;
+      const uint64_t c = (uint64_t)(std::upper_bound(wcum.begin(), wcum.end(), (uint64_t)tgt) - wcum.begin()) - 1;
+      if (c >= nc) return rows;
+      uint64_t acc = wcum[c], g = 0;
+      while (g < ng && acc < (uint64_t)tgt) {
+        acc += g >= ngu ? (uint64_t)wm16 : (h->gsum[g] <= thr[c] ? 16u : (uint64_t)wp16);
+        ++g;
+      }
+      return c * ng + g;
+    };
+    *lo = bound((uint64_t)rank) * nq;
+    *hi = bound((uint64_t)rank + 1) * nq;
+    return ALP_OK;
+  }
   const uint64_t wchunk = 16 * ngu + (uint64_t)wm16 * (ng - ngu), total = wchunk * (rows / std::max<uint64_t>(ng, 1));
   auto bound = [&](uint64_t r) -> uint64_t {  // first row whose cumulative cost reaches r / world of the total
     if (r == 0 || ng == 0 || rows % ng != 0) return r * (rows / (uint64_t)world) + std::min<uint64_t>(r, rows % (uint64_t)world);

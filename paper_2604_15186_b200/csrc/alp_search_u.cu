@@ -56,8 +56,9 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   int *s_crow = s_ua + P.Ka;                                // [NC][D+1] chunk row of each budget row
   int *s_clen = s_crow + NC * D1;                           // [NC][D+1] length of each chunk row
   int *s_cfin = s_clen + NC * D1;                           // [NC][D+1] finite entries of each chunk row
+  int *s_pf = s_cfin + NC * D1;                             // [Kb+1] finite u-sorted b terms before j
   __shared__ int s_rows[kUMaxChunks];                       // rows per chunk
-  auto stamp = [&](int slot) {  // ALP_DBG_TS: slots 5-7 of blocks 0 and 1 (k_search_u uses 0-4)
+  auto stamp = [&](int slot) {  // ALP_DBG_TS: slots 5-7 of blocks 0-2 (k_search_u uses 0-4, and 6 of blocks > 0)
     if (P.dbg_ts && tid == 0) {
       unsigned long long g;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -69,10 +70,11 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   // shared memory instead of L2/DRAM)
   const DevProfiles &gp = P.fz.prof;
   const int MT = gp.M * gp.nT;
-  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_cfin + NC * D1) + 7) & ~uintptr_t(7));
+  double *s_pd = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(s_pf + Kb + 1) + 15) & ~uintptr_t(15));
   DevProfiles sp = gp;
   {
     double *d = s_pd;
+    // (8-byte copies: 16-byte cp.async measured slower here, 2.9 vs 2.6 us to the staged tables)
     auto stage_d = [&](const double *src, int n) {
       for (int i = tid; i < n; i += nt) cp_async8(d + i, src + i);
       const double *r = d;
@@ -122,6 +124,7 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
   }
   cp_async_wait();
   __syncthreads();
+  stamp(15);
   for (int i = tid; i < NT * MK; i += nt) {
     const int t = i / MK, j = i % MK;
     float tau;
@@ -181,11 +184,24 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
     // u-sorted b terms
     for (int j = tid; j < Kb; j += nt) s_bs[j] = st[P.b_llm * K + s_bp[j]];
     __syncthreads();
+    if (t == 0) stamp(21);
     // per b chunk: budget row i (the u-sorted columns with u <= dv[i-1]; row 0 none) restricted to
     // the chunk's columns; equal restrictions share one chunk row (the length is non-decreasing in
     // i).  All chunks at once: one thread per chunk de-duplicates, then every (chunk, row) pair,
     // row element and lut entry in parallel (three barriers in all, not three per chunk).
-    for (int c = tid; c < NC; c += nt) {
+    // warp 0: s_pf[j] = finite terms among the first j u-sorted b columns (ballot scan), so a chunk
+    // row's finite count is a difference of two entries; the other warps de-duplicate the rows
+    if (tid < 32) {
+      int run = 0;
+      for (int j0 = 0; j0 <= Kb; j0 += 32) {
+        const int j = j0 + tid;
+        const int fin = j < Kb && s_bs[j] < __int_as_float(0x7f800000) ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, fin);
+        if (j <= Kb) s_pf[j] = run + __popc(bal & ((1u << tid) - 1u));
+        run += __popc(bal);
+      }
+    }
+    for (int c = tid - 32; c >= 0 && c < NC; c += nt - 32) {
       const int c0 = c * P.bchunk_w, wc = min(P.bchunk_w, Kb - c0);
       int rows = 0, prev = -1;
       for (int i = 0; i <= D; ++i) {
@@ -198,14 +214,6 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
         prev = len;
       }
       s_rows[c] = rows;
-    }
-    __syncthreads();
-    for (int i = tid; i < NC * D1; i += nt) {
-      const int c = i / D1, row = i % D1, c0 = c * P.bchunk_w;
-      if (row >= s_rows[c]) continue;
-      int f = 0;
-      for (int j = 0; j < s_clen[i]; ++j) f += (s_bs[c0 + j] < __int_as_float(0x7f800000)) ? 1 : 0;
-      s_cfin[i] = f;
     }
     __syncthreads();
     for (int c = 0; c < NC; ++c) {
@@ -226,9 +234,11 @@ __global__ void k_uprep(const __grid_constant__ SearchArgs P, unsigned char *T) 
         const int mid = (lo + hi) >> 1;
         if (s_dv[mid] <= r) lo = mid + 1; else hi = mid;
       }
-      const int row = s_crow[c * D1 + lo];
-      reinterpret_cast<int2 *>(tb + P.u_off_lut_c[c])[x] = make_int2(row * P.u_cstride, s_cfin[c * D1 + row]);
+      const int row = s_crow[c * D1 + lo], c0 = c * P.bchunk_w;
+      reinterpret_cast<int2 *>(tb + P.u_off_lut_c[c])[x] =
+          make_int2(row * P.u_cstride, s_pf[c0 + s_clen[c * D1 + row]] - s_pf[c0]);
     }
+    if (t == 0) stamp(23);
     __syncthreads();  // s_bs and the chunk tables are reused by the next target
   }
   stamp(8 + 5);
@@ -655,7 +665,9 @@ static cudaError_t build_graph(UGraph &gr, UState &u, const SearchArgs &a, int g
 size_t uprep_smem_bytes(const SearchArgs &a) {
   const DevProfiles &pr = a.fz.prof;
   const int MT = pr.M * pr.nT;
-  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(2 * a.D + 1 + 3 * a.u_nch * (a.D + 1) + a.Kb + a.g0 * a.K + a.Ka) * 4 + 8 +
+  return (size_t)(a.n_targets * a.M * a.K + a.Kb) * 4 + (size_t)(2 * a.D + 1 + 3 * a.u_nch * (a.D + 1) + a.Kb + a.g0 * a.K + a.Ka) * 4 +
+         (size_t)(a.Kb + 1) * 4 + 16 + 16 * 16 +  // s_pf, 16-byte alignment, per-array padding of the staging
+
          (size_t)(2 * pr.M + MT + 2 * pr.n_pts) * 8 +
          (size_t)(pr.nS + pr.nT + pr.nR + MT + 1 + (pr.min_units ? MT : 0)) * 4 +
          (pr.meas_off ? (size_t)(2 * pr.n_mpts + MT * pr.nS) * 8 + (size_t)(MT * pr.nS + 1) * 4 : 0);
@@ -666,7 +678,10 @@ cudaError_t launch_search_u(const SearchArgs &a, int grid, cudaStream_t st, cuda
   UState &u = ustate();
   if (!u.staging) return cudaErrorMemoryAllocation;
   const int MK = a.M * a.K, NTM = a.n_targets * MK;
-  const int threads = NTM >= 512 ? 1024 : (NTM >= 256 ? 512 : 256);
+  // (more threads measured slower at C4: 1024 threads 7.8 vs 6.9 us, tools/uprep_ab.sh)
+  int threads = NTM >= 512 ? 1024 : (NTM >= 256 ? 512 : 256);
+  static const int thr_env = getenv("ALP_UPREP_THREADS") ? atoi(getenv("ALP_UPREP_THREADS")) : 0;  // tuning knob
+  if (thr_env >= 64 && thr_env <= 1024) threads = thr_env & ~31;
   cudaError_t e = cudaStreamWaitEvent(st, u.done, 0);  // the previous search using the constant bank
   if (e != cudaSuccess) return e;
   const size_t prep_smem = uprep_smem_bytes(a);

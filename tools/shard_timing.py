@@ -36,7 +36,8 @@ for world in worlds:
         ks, ss = [], []
         for rep in range(reps + 3):
             with torch.cuda.stream(st):
-                flush.zero_()
+                if not os.environ.get("NO_FLUSH"):
+                    flush.zero_()
                 if mode == "peer":  # search + in-kernel exchange (with itself) over the rank's range
                     alp.search_peer(t, B, lo, hi, 0, [buf.ptr], st.cuda_stream)
                 else:
