@@ -286,6 +286,13 @@ __device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[A
   }
 }
 
+// The search's epilogue (fused_epilogue: last-block detection, finalize or peer exchange) out of
+// line: inlined, the finalize's live values set the kernel's register count (84 -> 20 one-warp
+// blocks per SM); out of line the search loops need 76 (24 blocks per SM): C4 kernel 0.425 ->
+// 0.420 ms.  (A speculative finalize of the running minimum by the first block to finish was
+// measured here too and not kept: on a busy SM it ran longer than the loop's tail, +1.7 us.)
+static __device__ __noinline__ void epilogue_u(const SearchArgs &P) { fused_epilogue(P, nullptr, P.fin.stage != 0); }
+
 // ------------------------------------------------------------------ search: one warp per block
 template <int NB4, bool TAIL2>
 __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchArgs P, const unsigned char *ug) {
@@ -490,7 +497,11 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
   stamp(2);
   pdl_trigger();
   // the search's shared memory is free now: the finalize stages its inputs in it
-  fused_epilogue(P, nullptr, P.fin.stage);
+  // (rows of 12-34 options: out of line — the finalize's registers cost C4 4 one-warp blocks per
+  // SM; long rows (C3) measured 5 % slower out of line, and the 2-option variant spills around the
+  // call: both keep it inline)
+  if constexpr (NB4 >= 3 && NB4 <= 8) epilogue_u(P);
+  else fused_epilogue(P, nullptr, P.fin.stage);
   stamp(3);
 }
 
