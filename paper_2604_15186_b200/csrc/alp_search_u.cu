@@ -401,8 +401,11 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       constexpr int kNP = 2 * NB4 + (TAIL2 ? 1 : 0);
       constexpr bool kFastRows = ALP_FAST_ROWS && kNP >= 1 && kNP <= 10;
       constexpr int kFUA = ALP_FAST_UA;
-      if (kFastRows && uni && cv.lut(c, xg - P.u_amax).x == cv.lut(c, P.lut_n - 1).x) {
-        const int2 lf = cv.lut(c, xg - P.u_amax);
+      // a mixed group's lanes: their own remaining budgets (uniform groups: the group's)
+      const int xl = uni ? xg : P.lut_base - upfx - min(__ldg(P.tile_s + tile), R1);
+      const int xq = uni ? xg : __reduce_min_sync(0xffffffffu, xl);  // the smallest of them
+      if (kFastRows && cv.lut(c, xq - P.u_amax).x == cv.lut(c, P.lut_n - 1).x) {
+        const int2 lf = cv.lut(c, xq - P.u_amax);
         const float2 *rb = rows_u + (lf.x >> 1);
         float2 bv[kNP > 0 ? kNP : 1];
 #pragma unroll
@@ -431,7 +434,6 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
         // mixed group: the lanes' own remaining budgets, rows from the global staging copy of the
         // tables (L1-resident; a different memory space keeps the compiler from merging this loop
         // with the uniform one into a single vector loop)
-        const int xl = P.lut_base - upfx - min(__ldg(P.tile_s + tile), R1);
         if (smem_rows) {
           const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(s_btab);
           // not unrolled: the smaller mixed-group code leaves the instruction cache to the uniform
@@ -439,7 +441,7 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
           // the lanes' lut indices span [xlo, xhi] (uniform, by redux); the lut is monotone in its
           // index, so where lut(xlo - u_a) and lut(xhi - u_a) name the same masked row every lane
           // uses that row: evaluated with uniform-register b operands like a uniform group
-          const int xlo = __reduce_min_sync(0xffffffffu, xl), xhi = __reduce_max_sync(0xffffffffu, xl);
+          const int xlo = xq, xhi = uni ? xg : __reduce_max_sync(0xffffffffu, xl);
 #pragma unroll 1
           for (int a = a0; a < a1; ++a) {
             const float4 av = cv.a(a);
