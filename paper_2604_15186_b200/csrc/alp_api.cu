@@ -1052,12 +1052,13 @@ bool ur_path(alp_s *h, const SearchArgs &a, int n, uint64_t hi, SearchArgs &ua, 
 
 // k_search_u tail split: the last items of the rank's range are handed out as S sub-items of
 // ceil(A / S) a options (needs single-option segments), so the warps' last tickets are short.
-// Default: the last warps/2 items in 3 parts (C4 8-rank shard kernel 0.0758 -> 0.0737 ms, whole C4
-// 0.4383 -> 0.4362 ms; with the tickets prefetched this had not helped).  ALP_U_SPLIT="x,S": split
-// the last x * warps items (x = 0: off).
+// Default: the last warps/2 items in 2 parts (3 parts before the full-row loop: C4 8-rank shard
+// kernel 0.0758 -> 0.0737 ms; with the full-row kernel 2 parts measured 0.0973-0.0993 ms vs 0.0993
+// for 3, profiles/r02_tail_split_fullrow.txt).  ALP_U_SPLIT="x,S": split the last x * warps items
+// (x = 0: off).
 void u_tail_split(SearchArgs &ua, uint64_t warps, uint64_t n_items) {
   static double xw = 0.5;
-  static int S = 3;
+  static int S = 2;
   static bool once = [] {
     if (const char *v = getenv("ALP_U_SPLIT")) sscanf(v, "%lf,%d", &xw, &S);
     return true;
