@@ -293,6 +293,14 @@ __device__ __forceinline__ void eval_row_u(const float2 *rb, const float (&Qa)[A
 // measured here too and not kept: on a busy SM it ran longer than the loop's tail, +1.7 us.)
 static __device__ __noinline__ void epilogue_u(const SearchArgs &P) { fused_epilogue(P, nullptr, P.fin.stage != 0); }
 
+// ALP_CHECK_BOUNDS builds (tests only: compute-sanitizer is unavailable on the GPU pool): every
+// table index of the search loops asserted in range; an out-of-range index traps the kernel.
+#ifdef ALP_CHECK_BOUNDS
+#define ALP_BOUND(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define ALP_BOUND(cond) do { } while (0)
+#endif
+
 // ------------------------------------------------------------------ search: one warp per block
 template <int NB4, bool TAIL2>
 __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchArgs P, const unsigned char *ug) {
@@ -406,6 +414,9 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
       const int xq = uni ? xg : __reduce_min_sync(0xffffffffu, xl);  // the smallest of them
       if (kFastRows && cv.lut(c, xq - P.u_amax).x == cv.lut(c, P.lut_n - 1).x) {
         const int2 lf = cv.lut(c, xq - P.u_amax);
+        ALP_BOUND(xq - P.u_amax >= 0 && xq - P.u_amax < P.lut_n && a0 >= 0 && a0 <= a1 && a1 <= P.Ka &&
+                  P.u_off_btab_c[c] + 4 * (lf.x + 2 * kNP) <= (c + 1 < P.u_nch ? P.u_off_lut_c[c + 1] : P.u_tstride) &&
+                  __float_as_int(cv.a(a1).w) - __float_as_int(cv.a(a0).w) >= 0);
         const float2 *rb = rows_u + (lf.x >> 1);
         float2 bv[kNP > 0 ? kNP : 1];
 #pragma unroll
@@ -445,6 +456,8 @@ __global__ void __launch_bounds__(32) k_search_u(const __grid_constant__ SearchA
 #pragma unroll 1
           for (int a = a0; a < a1; ++a) {
             const float4 av = cv.a(a);
+            ALP_BOUND(xlo - __float_as_int(av.y) >= 0 && xhi - __float_as_int(av.y) < P.lut_n &&
+                      xl - __float_as_int(av.y) >= 0 && xl - __float_as_int(av.y) < P.lut_n);
             const int2 l0 = cv.lut(c, xlo - __float_as_int(av.y));
             const int2 l1 = cv.lut(c, xhi - __float_as_int(av.y));
             float Qa[T];
