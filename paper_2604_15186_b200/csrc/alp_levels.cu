@@ -24,6 +24,7 @@ struct LevelArgs {
   unsigned long long *lvl_keys;  // [L] min key per level (0xFF..FF = none at the start)
   unsigned long long *ticket;    // work counter, 0 at the start
   int off_lvl, off_ta, off_tb, off_best, smem_bytes;  // dynamic shared-memory layout (bytes)
+  int off_runs;  // per ubase (row + a units) the equal-level runs of the u-sorted b columns, or -1
 };
 
 constexpr int kLvlThreads = 256;
@@ -67,6 +68,29 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
   }
   for (int l = tid; l < A.L; l += blockDim.x) s_best[l] = ~0ull;
   __syncthreads();
+  // run table: for every ubase, the u-sorted b columns split where the budget level of ubase + u_b
+  // changes, as (end column << 16 | level) entries ended by 0xffffffff — the boundaries depend only
+  // on ubase, so the loop below walks runs instead of looking up every column's level
+  uint32_t *s_runs = reinterpret_cast<uint32_t *>(smem + (A.off_runs >= 0 ? A.off_runs : 0));
+  const int rw = P.Kb + 1;
+  if (A.off_runs >= 0) {
+    for (int ub = tid; ub <= A.bmax; ub += blockDim.x) {
+      uint32_t *rt = s_runs + (size_t)ub * rw;
+      int n = 0, cur = -1, j = 0;
+      for (; j < P.Kb; ++j) {
+        const int U = ub + __float_as_int(s_tb[j].y);
+        if (U > A.bmax) break;
+        const int l = s_lvl[U];
+        if (l != cur) {
+          if (cur >= 0) rt[n++] = ((uint32_t)j << 16) | (uint32_t)cur;
+          cur = l;
+        }
+      }
+      if (cur >= 0) rt[n++] = ((uint32_t)j << 16) | (uint32_t)cur;
+      rt[n] = 0xffffffffu;
+    }
+    __syncthreads();
+  }
   if (P.off_pfx >= 0) {
     Smem sm;
     sm.tau = s_tau;
@@ -135,6 +159,35 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
 #pragma unroll
         for (int i = 0; i < T; ++i) acc[i] = finf();
       };
+      if (A.off_runs >= 0) {
+        const uint32_t *rt = s_runs + (size_t)ubase * rw;
+        int j = 0;
+        for (int r = 0;; ++r) {
+          const uint32_t e = rt[r];
+          if (e == 0xffffffffu) break;
+          const int jend = (int)(e >> 16);
+          cur = (int)(e & 0xffffu);
+          for (; j + 1 < jend; j += 2) {  // two columns: FADD2 per row pair + FMNMX3
+            const float2 bv = s_tb[j], bw = s_tb[j + 1];
+#pragma unroll
+            for (int i = 0; i < T; i += 2) {
+              float x0, x1, y0, y1;
+              add2b(x0, x1, Qa[i], Qa[i + 1], bv.x);
+              add2b(y0, y1, Qa[i], Qa[i + 1], bw.x);
+              acc[i] = min3(acc[i], x0, y0);
+              acc[i + 1] = min3(acc[i + 1], x1, y1);
+            }
+          }
+          if (j < jend) {
+            const float bx = s_tb[j].x;
+#pragma unroll
+            for (int i = 0; i < T; ++i) acc[i] = fminf(acc[i], __fadd_rn(Qa[i], bx));
+            ++j;
+          }
+          fold();
+        }
+        continue;
+      }
       for (int j = 0; j < P.Kb;) {
         const float2 bv = s_tb[j];
         const int U = ubase + __float_as_int(bv.y);
@@ -224,6 +277,10 @@ size_t levels_smem_bytes(const SearchArgs &s, int L, int bmax, LevelArgs *A) {
   off = a16(off + (size_t)L * 8);
   const size_t off_lvl = off;
   off = a16(off + (size_t)(bmax + 1) * 2);
+  const size_t runs_bytes = (size_t)(bmax + 1) * (size_t)(s.Kb + 1) * 4;
+  const bool runs = runs_bytes <= 48 * 1024;  // (C4: 9.8 KB; long b rows keep the per-column walk)
+  const size_t off_runs = off;
+  if (runs) off = a16(off + runs_bytes);
   if (A) {
     A->s.off_u = (int)off_u;
     A->s.off_pfx = pfx ? (int)off_pfx : -1;
@@ -231,6 +288,7 @@ size_t levels_smem_bytes(const SearchArgs &s, int L, int bmax, LevelArgs *A) {
     A->off_tb = (int)off_tb;
     A->off_best = (int)off_best;
     A->off_lvl = (int)off_lvl;
+    A->off_runs = runs ? (int)off_runs : -1;
     A->smem_bytes = (int)off;
   }
   return off;
