@@ -144,20 +144,27 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
       for (int i = 0; i < T; ++i) Qa[i] = __fadd_rn(Qr[i], av.x);
       int cur = -1;
       // fold the run's row minima into the block's best key of level `cur`
-      auto fold = [&]() {
+      // (the rows' canonical indices are read only when the run's minimum can still improve the
+      // level's best: its value bits alone bound the key from below)
+      auto fold = [&](bool reset) {
         float m = acc[0];
 #pragma unroll
         for (int i = 1; i < T; ++i) m = fminf(m, acc[i]);
         if (m < finf()) {
-          uint32_t bs = 0xffffffffu;
+          const unsigned long long hi = (unsigned long long)__float_as_uint(m) << 32;
+          if (hi <= s_best[cur]) {
+            uint32_t bs = 0xffffffffu;
 #pragma unroll
-          for (int i = 0; i < T; ++i)
-            if (acc[i] == m) bs = min(bs, (chunk * P.L + __ldg(P.tile_e + (size_t)tile * T + i)) * (uint32_t)P.Ka + (uint32_t)a);
-          const unsigned long long key = ((unsigned long long)__float_as_uint(m) << 32) | bs;
-          if (key < s_best[cur]) atomicMin(s_best + cur, key);
+            for (int i = 0; i < T; ++i)
+              if (acc[i] == m) bs = min(bs, (chunk * P.L + __ldg(P.tile_e + (size_t)tile * T + i)) * (uint32_t)P.Ka + (uint32_t)a);
+            const unsigned long long key = hi | bs;
+            if (key < s_best[cur]) atomicMin(s_best + cur, key);
+          }
         }
+        if (reset) {
 #pragma unroll
-        for (int i = 0; i < T; ++i) acc[i] = finf();
+          for (int i = 0; i < T; ++i) acc[i] = finf();
+        }
       };
       if (A.off_runs >= 0) {
         const uint32_t *rt = s_runs + (size_t)ubase * rw;
@@ -167,6 +174,24 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
           if (e == 0xffffffffu) break;
           const int jend = (int)(e >> 16);
           cur = (int)(e & 0xffffu);
+          // the run's first column(s) initialise the row minima (no reset after the previous fold)
+          if (j + 1 < jend) {
+            const float2 bv = s_tb[j], bw = s_tb[j + 1];
+#pragma unroll
+            for (int i = 0; i < T; i += 2) {
+              float x0, x1, y0, y1;
+              add2b(x0, x1, Qa[i], Qa[i + 1], bv.x);
+              add2b(y0, y1, Qa[i], Qa[i + 1], bw.x);
+              acc[i] = fminf(x0, y0);
+              acc[i + 1] = fminf(x1, y1);
+            }
+            j += 2;
+          } else {
+            const float bx = s_tb[j].x;
+#pragma unroll
+            for (int i = 0; i < T; ++i) acc[i] = __fadd_rn(Qa[i], bx);
+            ++j;
+          }
           for (; j + 1 < jend; j += 2) {  // two columns: FADD2 per row pair + FMNMX3
             const float2 bv = s_tb[j], bw = s_tb[j + 1];
 #pragma unroll
@@ -184,9 +209,9 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
             for (int i = 0; i < T; ++i) acc[i] = fminf(acc[i], __fadd_rn(Qa[i], bx));
             ++j;
           }
-          fold();
+          fold(false);
         }
-        continue;
+        continue;  // (every run initialises the row minima itself: no reset between a options)
       }
       for (int j = 0; j < P.Kb;) {
         const float2 bv = s_tb[j];
@@ -194,7 +219,7 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
         if (U > A.bmax) break;  // u-sorted: the rest is over every budget
         const int l = s_lvl[U];
         if (l != cur) {
-          if (cur >= 0) fold();
+          if (cur >= 0) fold(true);
           cur = l;
         }
         if (j + 1 < P.Kb) {  // two columns of the same level: FADD2 per row pair + FMNMX3
@@ -217,7 +242,7 @@ __global__ void __launch_bounds__(kLvlThreads, 2) k_search_levels(const __grid_c
         for (int i = 0; i < T; ++i) acc[i] = fminf(acc[i], __fadd_rn(Qa[i], bv.x));
         ++j;
       }
-      if (cur >= 0) fold();
+      if (cur >= 0) fold(true);
     }
   }
   __syncthreads();
